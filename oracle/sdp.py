@@ -1,0 +1,224 @@
+"""SDP elements, operators and the Schur complement, literally.  TEST INFRASTRUCTURE ONLY.
+
+Follows PAPER.md Sec. III.B "SDP Problem Elements" and Algorithm 2:
+* basis E_k of S^n (Eqs. 4-5) under reading R2:
+  k < n -> (k,k); then offsets o = 1..n-1, rows i = 0..n-1-o -> (i, i+o);
+  E = e_a e_b^T + e_b e_a^T (unnormalised) off the diagonal.  The printed formula
+  defines exactly the first n-1 of these off-diagonal elements (the first
+  super-diagonal) and the paper notes "any other basis could be used";
+* V_<h>(x) = sum_j E_j x_{j + Ntil(<h>-1)} (Eq. 30);
+* blocks B_{i,j} (Eq. 31): P-blocks j < L: sum_h beta_{h,j} V_h(e_i);
+  Lyapunov blocks L+m: -sum_h (H_{h,m}^T V_h(e_i) + V_h(e_i) H_{h,m});
+* B(X) = [tr(B_1 X) ... tr(B_K X)]^T,
+  B^T(y) = sum_i y_i B_i (Eq. AT);
+* lambda_{k,l} = sum_blocks tr(B_k Z^{-1} B_l X) (Eq. T2).
+
+Block order: P-blocks 0..L-1 in W_{dp+d1} order, then Lyapunov blocks in
+W_{dp+da+d2} order.  Dual index i = k + Ntil*h (0-based).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+from . import polya
+from .monomials import enumerate_W
+
+__all__ = ["basis", "trE", "Problem", "build_problem", "vmap", "F_block", "F_stack",
+           "apply_literal", "apply_vmap", "adjoint_literal", "adjoint_trace",
+           "schur_literal", "schur_entries", "schur_probe"]
+
+
+def basis(n: int):
+    """[(a, b)] for k = 0..Ntil-1 (reading R2, diagonal-major)."""
+    out = [(k, k) for k in range(n)]
+    for o in range(1, n):
+        for i in range(n - o):
+            out.append((i, i + o))
+    return out
+
+
+def E_matrix(n: int, ab):
+    a, b = ab
+    E = np.zeros((n, n))
+    E[a, b] = 1.0
+    E[b, a] = 1.0
+    return E
+
+
+def trE(ab, M):
+    """tr(E_k M): M[a,a] on the diagonal, M[a,b] + M[b,a] off it."""
+    a, b = ab
+    return M[a, a] if a == b else M[a, b] + M[b, a]
+
+
+@dataclasses.dataclass
+class Problem:
+    n: int
+    l: int
+    dp: int
+    da: int
+    d1: int
+    d2: int
+    delta: float
+    L0: int
+    L: int
+    M: int
+    Ntil: int
+    K: int
+    beta: np.ndarray          # (L0, L) int64
+    H: np.ndarray             # (L0, M, n, n)
+    c: np.ndarray             # (L,)
+    A: np.ndarray
+    E: list
+
+    @property
+    def nblocks(self):
+        return self.L + self.M
+
+    def active(self, h: int, b: int) -> bool:
+        """Whether F^b_{(h,.)} is structurally non-zero."""
+        if b < self.L:
+            return self.beta[h, b] != 0
+        return bool(np.any(self.H[h, b - self.L] != 0))
+
+
+def build_problem(A, n, l, dp, d1, d2, da=1, delta=1e-3) -> Problem:
+    """Algorithm 1's outputs in dense form: beta, H, C (and K)."""
+    beta = polya.beta_table(l, dp, d1)
+    H = polya.H_table(A, l, dp, d2, da)
+    L0, L = beta.shape
+    M = H.shape[1]
+    Ntil = n * (n + 1) // 2
+    c = polya.C_scalars(beta, l, dp, delta)
+    return Problem(n, l, dp, da, d1, d2, delta, L0, L, M, Ntil, L0 * Ntil, beta, H, c, A, basis(n))
+
+
+def vmap(P: Problem, x, h: int):
+    """V_<h>(x) = sum_j E_j x_{j+Ntil h} (Eq. 30) as a dense symmetric n x n matrix."""
+    ia, ib = _ab(P.n)
+    seg = np.asarray(x[P.Ntil * h:P.Ntil * (h + 1)], dtype=np.float64)
+    out = np.zeros((P.n, P.n))
+    out[ia, ib] += seg
+    off = ia != ib
+    out[ib[off], ia[off]] += seg[off]
+    return out
+
+
+def _ab(n):
+    ab = np.array(basis(n), dtype=np.int64).reshape(-1, 2)
+    return ab[:, 0], ab[:, 1]
+
+
+def trE_all(n, M):
+    """[tr(E_k M)]_k for every basis element at once (same rule as ``trE``)."""
+    ia, ib = _ab(n)
+    return np.where(ia == ib, M[ia, ia], M[ia, ib] + M[ib, ia])
+
+
+def F_block(P: Problem, i: int, b: int):
+    """B_{i,b} of Eq. (31), dense n x n."""
+    h, k = divmod(i, P.Ntil)
+    E = E_matrix(P.n, P.E[k])
+    if b < P.L:
+        return float(P.beta[h, b]) * E
+    Hm = P.H[h, b - P.L]
+    return -(Hm.T @ E + E @ Hm)
+
+
+def F_stack(P: Problem, b: int, rows=None):
+    """(len(rows), n, n) stack of B_{i,b} for i in rows (default all K)."""
+    rows = range(P.K) if rows is None else rows
+    return np.array([F_block(P, i, b) for i in rows])
+
+
+def apply_literal(P: Problem, y):
+    """B^T(y) = sum_i y_i B_i (Eq. AT), blockwise, dense F."""
+    out = np.zeros((P.nblocks, P.n, P.n))
+    for b in range(P.nblocks):
+        for i in range(P.K):
+            if y[i] != 0.0:
+                out[b] += y[i] * F_block(P, i, b)
+    return out
+
+
+def apply_vmap(P: Problem, y):
+    """B^T(y) via Eq. (31) with e_i replaced by y (V is linear, Eq. 30):
+    P-block j: sum_h beta_{h,j} V_h(y); Lyapunov block m: -sum_h (H^T V_h(y) + V_h(y) H)."""
+    out = np.zeros((P.nblocks, P.n, P.n))
+    V = [vmap(P, y, h) for h in range(P.L0)]
+    for j in range(P.L):
+        for h in range(P.L0):
+            out[j] += float(P.beta[h, j]) * V[h]
+    for m in range(P.M):
+        for h in range(P.L0):
+            Hm = P.H[h, m]
+            out[P.L + m] -= Hm.T @ V[h] + V[h] @ Hm
+    return out
+
+
+def adjoint_literal(P: Problem, Xb):
+    """B(X)_i = sum_b tr(B_{i,b} X_b), dense F."""
+    y = np.zeros(P.K)
+    for i in range(P.K):
+        for b in range(P.nblocks):
+            y[i] += np.trace(F_block(P, i, b) @ Xb[b])
+    return y
+
+
+def adjoint_trace(P: Problem, Xb):
+    """B(X)_i with tr(B_{i,b} X_b) expanded by cyclicity of the trace:
+    P-block: beta tr(E_k X); Lyapunov: -tr(H^T E X) - tr(E H X) = -tr(E_k (X H^T + H X))."""
+    y = np.zeros(P.K)
+    for h in range(P.L0):
+        for b in range(P.nblocks):
+            if b < P.L:
+                if P.beta[h, b] == 0:
+                    continue
+                M = float(P.beta[h, b]) * Xb[b]
+            else:
+                Hm = P.H[h, b - P.L]
+                if not np.any(Hm):
+                    continue
+                M = -(Xb[b] @ Hm.T + Hm @ Xb[b])
+            y[P.Ntil * h:P.Ntil * (h + 1)] += trE_all(P.n, M)
+    return y
+
+
+def schur_literal(P: Problem, Xb, Wb, rows=None):
+    """lambda_{k,l} = sum_b tr(B_{k,b} Z_b^{-1} B_{l,b} X_b) (Eq. T2) for k in rows, all l.
+    Per block: Y_l = W_b F_l X_b (two library matmuls), then
+    tr(F_k Y_l) = sum_pq F_k[p,q] Y_l[q,p] (one library matmul over the flattened blocks)."""
+    rows = list(range(P.K)) if rows is None else list(rows)
+    G = np.zeros((len(rows), P.K))
+    n2 = P.n * P.n
+    for b in range(P.nblocks):
+        Fb = F_stack(P, b)
+        Y = np.matmul(np.matmul(Wb[b], Fb), Xb[b])
+        Yt = Y.transpose(0, 2, 1).reshape(P.K, n2)
+        G += Fb[rows].reshape(len(rows), n2) @ Yt.T
+    return G
+
+
+def schur_entries(P: Problem, Xb, Wb, pairs):
+    """lambda_{k,l} for an explicit list of (k, l) pairs, one trace product at a time,
+    skipping blocks where B_{k,b} or B_{l,b} is structurally zero."""
+    out = np.zeros(len(pairs))
+    for t, (k, l) in enumerate(pairs):
+        hk, hl = k // P.Ntil, l // P.Ntil
+        s = 0.0
+        for b in range(P.nblocks):
+            if not (P.active(hk, b) and P.active(hl, b)):
+                continue
+            s += np.trace(F_block(P, k, b) @ Wb[b] @ F_block(P, l, b) @ Xb[b])
+        out[t] = s
+    return out
+
+
+def schur_probe(P: Problem, Xb, Wb, v):
+    """(G v)_k = sum_l lambda_{k,l} v_l = sum_b tr(B_{k,b} W_b (sum_l v_l B_{l,b}) X_b)
+    = B(W B^T(v) X)_k by linearity of Eq. (T2) in B_l."""
+    Fv = apply_vmap(P, v)
+    Y = np.matmul(np.matmul(Wb, Fv), Xb)
+    return adjoint_trace(P, Y)
