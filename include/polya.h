@@ -1,0 +1,179 @@
+/*
+ * polya.h -- C ABI of the B200-native hot path of Kamyar, Peet & Peet,
+ * "Solving Large-Scale Robust Stability Problems by Exploiting the Parallel
+ * Structure of Polya's Theorem" (IEEE TAC 2013, arxiv 1411.3769).
+ *
+ * Citations "PAPER.md:n" are lines of the paper's LaTeX source; "R1".."R16"
+ * are the readings of ambiguous passages listed in DESIGN.md.
+ *
+ * Problem: robust stability of x' = A(alpha) x,
+ * alpha in the unit simplex, A(alpha) = sum_{lambda in W_da} A_lambda alpha^lambda.
+ * Polya's multipliers turn P(alpha) > 0 and A^T P + P A < 0 into L + M
+ * coefficient LMIs ("blocks"), posed as one block-diagonal SDP (Eqs. 26-32,
+ * PAPER.md:341-379):
+ *   blocks b = 0 .. L-1      P-blocks,        gamma_b in W_{dp+d1}  (Eq. LMI_3)
+ *   blocks b = L .. L+M-1    Lyapunov blocks, gamma_b in W_{dp+da+d2} (Eq. LMI_4)
+ *   dual index i = k + Ntil*h (0-based), h in W_dp, k in the basis of S^n (R2),
+ *   Ntil = n(n+1)/2, K = |W_dp| * Ntil (Eq. K).
+ *   F_i^b = beta_{h,b} E_k                      (P-block, Eq. 31 case I)
+ *   F_i^b = -(H_{h,m}^T E_k + E_k H_{h,m})       (Lyapunov block m=b-L, case II)
+ *
+ * Conventions (binding for every entry point):
+ *  - 0-based indices.  The paper's <gamma> = position + 1 in W_d, W_d ordered by
+ *    PAPER.md:58's prose (descending lexicographic; reading R1).
+ *  - Basis of S^n (reading R2, diagonal-major): k < n -> (k,k); then for offset
+ *    o = 1..n-1 and row a = 0..n-1-o: (a, a+o).  E = e_a e_b^T + e_b e_a^T off the
+ *    diagonal (unnormalised), so y holds actual matrix entries.
+ *  - Matrices are row-major, contiguous, FP64.  A "block stack" is
+ *    double[nblocks][n][n] in block order above.
+ *  - Pointers named *_host are host memory; *_dev are device memory on the
+ *    context's device (caller-owned, 16-byte aligned; torch tensors qualify).
+ *  - apply / adjoint / schur are stream-ordered and asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).  Asynchronous
+ *    kernel faults surface at polya_sync() or the next call.
+ *  - Every entry point returns a polya_status; nothing aborts or throws across
+ *    the boundary.  polya_last_error(ctx) gives a human-readable detail.
+ *  - One context per rank / GPU; a context is not thread-safe; no global state.
+ */
+#ifndef POLYA_H_
+#define POLYA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct polya_ctx polya_ctx;
+
+typedef enum {
+  POLYA_OK = 0,
+  POLYA_EINVAL = 1,     /* bad dimension, null pointer, unsupported option        */
+  POLYA_EOVERFLOW = 2,  /* checked int64 failure on f(l,d), K, K*K or a byte size */
+  POLYA_ENOMEM = 3,     /* device or host allocation failed                       */
+  POLYA_ECUDA = 4,      /* CUDA runtime / kernel error                            */
+  POLYA_ENCCL = 5,      /* reserved (multi-GPU collectives)                       */
+  POLYA_ENOTPD = 6,     /* a Z block or the Schur complement is not positive definite */
+  POLYA_ESTEP = 7,      /* line search found no admissible step                   */
+  POLYA_EMAXIT = 8      /* reserved (iteration limit of a driver)                 */
+} polya_status;
+
+/* Problem shape.  delta > 0 is the P-positivity margin of Eq. Cj ("a small
+ * positive parameter"; R9 default 1e-3).  rank / nranks select
+ * this context's share of the Schur complement (output-tile sharding, see
+ * polya_schur); nranks = 1 for a single GPU. */
+typedef struct {
+  int32_t n, l, dp, da, d1, d2;
+  double delta;
+  int32_t rank, nranks;
+} polya_config;
+
+typedef struct {
+  int64_t L0;        /* |W_dp|                        Eq. L0 */
+  int64_t L;         /* |W_{dp+d1}|  P-blocks          Eq. L */
+  int64_t M;         /* |W_{dp+da+d2}| Lyapunov blocks Eq. M */
+  int64_t nblocks;   /* L + M                                                    */
+  int64_t Ntil;      /* n(n+1)/2                                                 */
+  int64_t K;         /* L0 * Ntil, dual dimension      Eq. K */
+  int64_t nnz_beta;  /* #(h, P-block) with beta != 0 (h <= gamma)                */
+  int64_t nnz_H;     /* #(h, Lyapunov block) with h + lambda <= gamma for some lambda */
+  int64_t npairs;    /* #(h <= h') dual-row pairs = L0(L0+1)/2                   */
+  int64_t pair0, pair1;   /* this rank's pairs [pair0, pair1) of the pair order   */
+  int64_t item0, item1;   /* this rank's Schur work items [item0, item1)          */
+  double useful_flops_schur;  /* W_G: algorithmic FP64 FLOPs of one polya_schur on
+                                 this rank (upper triangle) */
+  int64_t tiles_bytes;  /* bytes of G in POLYA_G_PAIR_TILES layout on this rank   */
+} polya_dims;
+
+/* Output layouts of the Schur complement G (symmetric K x K):
+ *  POLYA_G_FULL       double[K][K] row-major.  Entries of this rank's work items
+ *                     are written together with their mirror images (bitwise
+ *                     symmetric); other entries are left untouched.
+ *  POLYA_G_PAIR_TILES this rank's pair tiles p = pair0 .. pair1-1, each
+ *                     double[Ntil][Ntil] row-major = G[h*Ntil.., h'*Ntil..] for the
+ *                     p-th pair (h <= h') of the order (h ascending, h' ascending);
+ *                     diagonal tiles (h = h') are stored full and symmetric.       */
+typedef enum { POLYA_G_FULL = 0, POLYA_G_PAIR_TILES = 1 } polya_G_layout;
+
+/* Algorithm 1 without materialising B_i: enumerates W_dp,
+ * W_{dp+d1}, W_{dp+da+d2}; beta (Eq. beta, closed form multinomial(d1; gamma-h));
+ * H (Eq. H, closed form sum_lambda multinomial(d2; gamma-h-lambda) A_lambda,
+ * computed on the device); C (Eq. Cj); block descriptors; this rank's share.
+ * A_host: double[f(l,da)][n][n], coefficient of alpha^lambda in W_da order; copied.
+ * Synchronous.  Selects the current CUDA device at call time as the ctx's device.
+ * Errors: EINVAL (n<1, l<1, dp<0, da<0, d1<0, d2<0, delta<=0, rank outside
+ * [0,nranks), null pointers), EOVERFLOW, ENOMEM, ECUDA.  *out = NULL on error. */
+polya_status polya_setup(const polya_config* cfg, const double* A_host, polya_ctx** out);
+
+polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* out);
+
+/* Exponent table `which` (0: W_dp, 1: W_{dp+d1}, 2: W_{dp+da+d2}, 3: W_da) as
+ * int32[f(l,d)][l], in the R1 order.  Synchronous. */
+polya_status polya_get_exponents(const polya_ctx* ctx, int which, int32_t* out_host);
+
+/* beta as int64[L0][L] (zeros where h is not <= gamma).  Synchronous. */
+polya_status polya_get_beta(const polya_ctx* ctx, int64_t* out_host);
+
+/* H as double[L0][M][n][n] (zeros where structurally zero), copied back from the
+ * device.  Synchronous. */
+polya_status polya_get_H(const polya_ctx* ctx, double* out_host);
+
+/* c_j with C_j = c_j I_n for the L P-blocks (Eq. Cj); C is 0 on
+ * Lyapunov blocks.  Synchronous. */
+polya_status polya_get_C(const polya_ctx* ctx, double* out_host);
+
+/* Forward map B^T(y) = sum_i y_i B_i (Eq. AT), blockwise:
+ * P-block j: sum_h beta_{h,j} V_h(y); Lyapunov block m: -(S + S^T), S = sum_h V_h(y) H_{h,m}.
+ * y_dev: double[K]; blocks_dev: double[nblocks][n][n] (all blocks, written fully). */
+polya_status polya_apply(polya_ctx* ctx, const double* y_dev, double* blocks_dev, void* stream);
+
+/* Adjoint B(X)_i = sum_b tr(F_i^b X_b).  X_dev: double[nblocks][n][n]
+ * (need not be symmetric; only its symmetric part matters); y_dev: double[K], overwritten. */
+polya_status polya_adjoint(polya_ctx* ctx, const double* X_dev, double* y_dev, void* stream);
+
+/* Schur complement matrix (Eq. T2; Case 1):
+ *   G_{ij} = sum_b tr(F_i^b Z_b^{-1} F_j^b X_b)
+ * X_dev, Zinv_dev: double[nblocks][n][n]; both triangles are read and the
+ * expansion assumes exact symmetry (callers symmetrise).  G_dev per layout.
+ * This rank computes its work items [item0, item1) (output-tile sharding: inputs
+ * replicated on every rank, no inter-GPU traffic).  Uses the rank-structured
+ * expansion of DESIGN.md ("4-term raw GEMM + fold"), never the dense B_i.       */
+polya_status polya_schur(polya_ctx* ctx, const double* X_dev, const double* Zinv_dev,
+                         double* G_dev, int layout, void* stream);
+
+/* One predictor-corrector iteration of Algorithm 2 with the
+ * readings R3-R6, on a single rank (nranks must be 1).  State lives on the device:
+ * X, Z: double[nblocks][n][n] (symmetric PD), y: double[K]; updated in place.
+ * mu is the barrier parameter of the previous step (Eq. mu).
+ * The K x K factorisation uses cuSOLVER dpotrf/dpotrs (timed separately in stats).
+ * Synchronous (returns after the step).  Errors: ENOTPD, ESTEP, ECUDA, ENOMEM.   */
+typedef struct { double* X; double* Z; double* y; double mu; int32_t iter; } polya_ipm_state;
+typedef struct {
+  double gap;      /* |a^T y - tr(C X)| after the step (stopping rule) */
+  double mu;       /* new barrier parameter (1/3) sum tr(Z X)  (R4)                  */
+  double tp, td;   /* primal / dual step sizes (R5)                                  */
+  double phi, psi; /* primal cost tr(C X), dual cost a^T y                            */
+  float ms_schur, ms_factor, ms_other;
+} polya_ipm_stats;
+polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, polya_ipm_stats* stats, void* stream);
+
+/* Phase timing of polya_schur with CUDA events recorded on the call's stream:
+ * enable != 0 turns the events on for subsequent calls; polya_get_timing waits for the
+ * last call's events and returns the milliseconds of the SCM precompute (padding, U, V,
+ * Q, R; kernel K3) and of the assembly kernel K4. */
+polya_status polya_set_timing(polya_ctx* ctx, int enable);
+polya_status polya_get_timing(polya_ctx* ctx, float* ms_pre, float* ms_assemble);
+
+/* Surfaces asynchronous errors (device synchronise + last-error check). */
+polya_status polya_sync(polya_ctx* ctx);
+const char* polya_strerror(polya_status s);
+const char* polya_last_error(const polya_ctx* ctx);
+/* Number of kernel launches this context has issued so far (for bench.py's
+ * gpu_launches count). */
+int64_t polya_launch_count(const polya_ctx* ctx);
+void polya_destroy(polya_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLYA_H_ */

@@ -1,0 +1,223 @@
+"""Python binding of libpolya.so (include/polya.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; PyTorch only
+provides device memory and the stream.  There is no CPU fallback: if the
+shared library is missing or CUDA is unavailable, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "EXPORTS", "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
+G_FULL, G_PAIR_TILES = 0, 1
+EXPORTS = ["polya_setup", "polya_dims_get", "polya_get_exponents", "polya_get_beta", "polya_get_H",
+           "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
+           "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
+           "polya_get_timing"]
+
+
+class PolyaError(RuntimeError):
+    pass
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("l", ctypes.c_int32), ("dp", ctypes.c_int32), ("da", ctypes.c_int32),
+                ("d1", ctypes.c_int32), ("d2", ctypes.c_int32), ("delta", ctypes.c_double),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in ("L0", "L", "M", "nblocks", "Ntil", "K", "nnz_beta", "nnz_H",
+                                              "npairs", "pair0", "pair1", "item0", "item1")] + \
+               [("useful_flops_schur", ctypes.c_double), ("tiles_bytes", ctypes.c_int64)]
+
+
+class _IpmState(ctypes.Structure):
+    _fields_ = [("X", ctypes.c_void_p), ("Z", ctypes.c_void_p), ("y", ctypes.c_void_p),
+                ("mu", ctypes.c_double), ("iter", ctypes.c_int32)]
+
+
+class _IpmStats(ctypes.Structure):
+    _fields_ = [("gap", ctypes.c_double), ("mu", ctypes.c_double), ("tp", ctypes.c_double), ("td", ctypes.c_double),
+                ("phi", ctypes.c_double), ("psi", ctypes.c_double), ("ms_schur", ctypes.c_float),
+                ("ms_factor", ctypes.c_float), ("ms_other", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpolya.so (loud failure if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1411_3769_b200.build` (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
+    L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
+    L.polya_get_exponents.argtypes = [vp, ctypes.c_int, vp]
+    L.polya_get_beta.argtypes = [vp, vp]
+    L.polya_get_H.argtypes = [vp, vp]
+    L.polya_get_C.argtypes = [vp, vp]
+    L.polya_apply.argtypes = [vp, vp, vp, vp]
+    L.polya_adjoint.argtypes = [vp, vp, vp, vp]
+    L.polya_schur.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
+    L.polya_ipm_step.argtypes = [vp, ctypes.POINTER(_IpmState), ctypes.POINTER(_IpmStats), vp]
+    L.polya_sync.argtypes = [vp]
+    L.polya_set_timing.argtypes = [vp, ctypes.c_int]
+    L.polya_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
+    L.polya_strerror.argtypes = [ctypes.c_int]
+    L.polya_strerror.restype = ctypes.c_char_p
+    L.polya_last_error.argtypes = [vp]
+    L.polya_last_error.restype = ctypes.c_char_p
+    L.polya_launch_count.argtypes = [vp]
+    L.polya_launch_count.restype = i64
+    L.polya_destroy.argtypes = [vp]
+    L.polya_destroy.restype = None
+    for name in EXPORTS:
+        if name not in ("polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy"):
+            getattr(L, name).restype = ctypes.c_int
+    del i32, dbl
+    _lib = L
+    return L
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_ptr(t, numel=None, name="tensor"):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise PolyaError(f"{name} must be a CUDA torch tensor")
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise PolyaError(f"{name} must be contiguous float64")
+    if numel is not None and t.numel() != numel:
+        raise PolyaError(f"{name} has {t.numel()} elements, expected {numel}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Polya:
+    """One context = one rank / GPU (``polya_setup``).  ``A`` is the host array
+    double[f(l,da)][n][n] of A(alpha)'s coefficients in W_da order."""
+
+    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1):
+        L = lib()
+        A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+        cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks)
+        h = ctypes.c_void_p()
+        st = L.polya_setup(ctypes.byref(cfg), A.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h))
+        if st != 0:
+            raise PolyaError(f"polya_setup: {L.polya_strerror(st).decode()}")
+        self._h = h
+        self.n, self.l, self.dp, self.da, self.d1, self.d2 = n, l, dp, da, d1, d2
+        self.delta, self.rank, self.nranks = delta, rank, nranks
+        d = _Dims()
+        self._check(L.polya_dims_get(self._h, ctypes.byref(d)), "polya_dims_get")
+        self.dims = {k: getattr(d, k) for k, _ in _Dims._fields_}
+        for k in ("L0", "L", "M", "nblocks", "Ntil", "K"):
+            setattr(self, k, int(self.dims[k]))
+
+    def _check(self, st, what):
+        if st != 0:
+            L = lib()
+            raise PolyaError(f"{what}: {L.polya_strerror(st).decode()} ({L.polya_last_error(self._h).decode()})")
+
+    # -- set-up queries ----------------------------------------------------------------------------
+    def exponents(self, which):
+        counts = {0: self.L0, 1: self.L, 2: self.M}
+        if which == 3:
+            from math import comb
+            cnt = comb(self.l + self.da - 1, self.l - 1)
+        else:
+            cnt = counts[which]
+        out = np.zeros((cnt, self.l), dtype=np.int32)
+        self._check(lib().polya_get_exponents(self._h, which, out.ctypes.data_as(ctypes.c_void_p)), "get_exponents")
+        return out
+
+    def beta(self):
+        out = np.zeros((self.L0, self.L), dtype=np.int64)
+        self._check(lib().polya_get_beta(self._h, out.ctypes.data_as(ctypes.c_void_p)), "get_beta")
+        return out
+
+    def H(self):
+        out = np.zeros((self.L0, self.M, self.n, self.n), dtype=np.float64)
+        self._check(lib().polya_get_H(self._h, out.ctypes.data_as(ctypes.c_void_p)), "get_H")
+        return out
+
+    def C(self):
+        out = np.zeros(self.L, dtype=np.float64)
+        self._check(lib().polya_get_C(self._h, out.ctypes.data_as(ctypes.c_void_p)), "get_C")
+        return out
+
+    # -- operators ----------------------------------------------------------------------------------
+    def apply(self, y, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((self.nblocks, self.n, self.n), dtype=torch.float64, device=y.device)
+        self._check(lib().polya_apply(self._h, _dev_ptr(y, self.K, "y"), _dev_ptr(out, self.nblocks * self.n ** 2, "out"),
+                                      _stream_ptr(stream)), "polya_apply")
+        return out
+
+    def adjoint(self, X, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.K, dtype=torch.float64, device=X.device)
+        self._check(lib().polya_adjoint(self._h, _dev_ptr(X, self.nblocks * self.n ** 2, "X"), _dev_ptr(out, self.K, "y"),
+                                        _stream_ptr(stream)), "polya_adjoint")
+        return out
+
+    def schur(self, X, Zinv, G=None, layout=G_FULL, stream=None):
+        import torch
+        if G is None:
+            if layout == G_FULL:
+                G = torch.zeros((self.K, self.K), dtype=torch.float64, device=X.device)
+            else:
+                npl = self.dims["pair1"] - self.dims["pair0"]
+                G = torch.zeros((npl, self.Ntil, self.Ntil), dtype=torch.float64, device=X.device)
+        nbn = self.nblocks * self.n ** 2
+        self._check(lib().polya_schur(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"), _dev_ptr(G, None, "G"),
+                                      layout, _stream_ptr(stream)), "polya_schur")
+        return G
+
+    def ipm_step(self, X, Z, y, mu, it=0, stream=None):
+        st = _IpmState(_dev_ptr(X, None, "X").value, _dev_ptr(Z, None, "Z").value, _dev_ptr(y, self.K, "y").value,
+                       float(mu), int(it))
+        stats = _IpmStats()
+        self._check(lib().polya_ipm_step(self._h, ctypes.byref(st), ctypes.byref(stats), _stream_ptr(stream)),
+                    "polya_ipm_step")
+        return {k: getattr(stats, k) for k, _ in _IpmStats._fields_}
+
+    def set_timing(self, on=True):
+        self._check(lib().polya_set_timing(self._h, int(bool(on))), "polya_set_timing")
+
+    def timing(self):
+        a, b = ctypes.c_float(), ctypes.c_float()
+        self._check(lib().polya_get_timing(self._h, ctypes.byref(a), ctypes.byref(b)), "polya_get_timing")
+        return float(a.value), float(b.value)
+
+    def sync(self):
+        self._check(lib().polya_sync(self._h), "polya_sync")
+
+    def launch_count(self):
+        return int(lib().polya_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().polya_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,245 @@
+// kernels.cu -- set-up, operator and batched-GEMM kernels for sm_100a.
+//
+// K1 setup_H    : H_{h,gamma} = sum_lambda multinomial(d2; gamma-h-lambda) A_lambda (Eq. H)
+// pad_copy      : caller block stack [nb][n][n] -> zero-padded np x np arena matrices
+// K3 gemm       : batched C = sum_t alpha_t A_t op(B_t) on np x np arena matrices, FP64 DMMA (mma.sync
+//                 m8n8k4 f64; tcgen05 has no f64 kind on sm_100a), used for the SCM precompute
+//                 (U, V, Q, R), the forward map and the adjoint
+// K8 vmap/apply : B^T(y) blocks (Eq. AT with Eq. 31)
+// K9 adjoint    : B(X)_i = sum_b tr(F_i^b X_b), segmented reduction over blocks
+#include <algorithm>
+
+#include "polya_internal.h"
+
+namespace polya {
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// svec position of the basis element (a, b), a <= b, under reading R2 (diagonal-major).
+__device__ __forceinline__ int64_t svec_idx(int a, int b, int n) {
+  const int o = b - a;
+  if (o == 0) return a;
+  return (int64_t)n + (int64_t)(o - 1) * n - (int64_t)(o - 1) * o / 2 + a;
+}
+
+__global__ void k_setup_H(double* __restrict__ arena, int64_t ms, int np, int n, int nA,
+                          const double* __restrict__ A, const double* __restrict__ Hw, int64_t id_H) {
+  const int t = blockIdx.x;
+  double* H = arena + (id_H + t) * ms;
+  const double* w = Hw + (int64_t)t * nA;
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    double v = 0.0;
+    if (i < n && j < n)
+      for (int a = 0; a < nA; ++a) v += w[a] * A[((int64_t)a * n + i) * n + j];
+    H[e] = v;
+  }
+}
+
+__global__ void k_pad_copy(double* __restrict__ arena, int64_t ms, int np, int n, const double* __restrict__ src,
+                           int64_t id0, int sym) {
+  const int64_t b = blockIdx.x;
+  double* dst = arena + (id0 + b) * ms;
+  const double* s = src + b * n * n;
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    double v = 0.0;
+    if (i < n && j < n) v = sym ? 0.5 * (s[i * n + j] + s[j * n + i]) : s[i * n + j];
+    dst[e] = v;
+  }
+}
+
+// Batched GEMM on np x np arena matrices; CTA = one 32x32 tile of one output matrix, 4 warps,
+// each warp a 16x16 block = 2x2 DMMA m8n8 tiles.  K is staged 8 at a time through shared memory
+// in k-major layout (row stride 40 doubles: conflict-free fragment reads).
+constexpr int GT = 32;
+constexpr int GS = 40;
+__global__ void __launch_bounds__(128) k_gemm(double* __restrict__ arena, int64_t ms, int np,
+                                              const GemmItem* __restrict__ items,
+                                              const GemmTerm* __restrict__ terms, int tiles) {
+  __shared__ __align__(16) double As[8 * GS];
+  __shared__ __align__(16) double Bs[8 * GS];
+  const GemmItem it = items[blockIdx.y];
+  const int ti = blockIdx.x / tiles, tj = blockIdx.x - ti * tiles;
+  const int i0 = ti * GT, j0 = tj * GT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 16;
+  double acc[2][2][2] = {};
+  for (int q = it.tbeg; q < it.tend; ++q) {
+    const GemmTerm tm = terms[q];
+    const double* A = arena + (int64_t)tm.a_id * ms;
+    const double* B = arena + (int64_t)tm.b_id * ms;
+    for (int k0 = 0; k0 < np; k0 += 8) {
+      {  // A: 32 rows x 8 k -> As[k][i]
+        const int idx = tid * 2, i = idx >> 3, k = idx & 7;
+        double2 v = make_double2(0.0, 0.0);
+        if (i0 + i < np) v = *reinterpret_cast<const double2*>(A + (int64_t)(i0 + i) * np + k0 + k);
+        As[k * GS + i] = tm.alpha * v.x;
+        As[(k + 1) * GS + i] = tm.alpha * v.y;
+      }
+      if (!tm.transB) {  // B[k][j]: 8 k x 32 j
+        const int idx = tid * 2, k = idx >> 5, j = idx & 31;
+        double2 v = make_double2(0.0, 0.0);
+        if (j0 + j < np) v = *reinterpret_cast<const double2*>(B + (int64_t)(k0 + k) * np + j0 + j);
+        *reinterpret_cast<double2*>(&Bs[k * GS + j]) = v;
+      } else {  // B[k][j] = Bm[j][k]
+        const int idx = tid * 2, j = idx >> 3, k = idx & 7;
+        double2 v = make_double2(0.0, 0.0);
+        if (j0 + j < np) v = *reinterpret_cast<const double2*>(B + (int64_t)(j0 + j) * np + k0 + k);
+        Bs[k * GS + j] = v.x;
+        Bs[(k + 1) * GS + j] = v.y;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        double a[2], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) a[mi] = As[(ks * 4 + t) * GS + wr + mi * 8 + g];
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) b[nj] = Bs[(ks * 4 + t) * GS + wc + nj * 8 + g];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+      }
+      __syncthreads();
+    }
+  }
+  double* C = arena + (int64_t)it.c_id * ms;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) {
+      const int i = i0 + wr + mi * 8 + g, j = j0 + wc + nj * 8 + 2 * t;
+      if (i < np && j < np) *reinterpret_cast<double2*>(C + (int64_t)i * np + j) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+    }
+}
+
+// V_h(y) (Eq. 30) for every h into the arena.
+__global__ void k_vmap(double* __restrict__ arena, int64_t ms, int np, int n, int64_t Ntil,
+                       const double* __restrict__ y, int64_t id_Vy) {
+  const int h = blockIdx.x;
+  double* V = arena + (id_Vy + h) * ms;
+  const double* yh = y + (int64_t)h * Ntil;
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    double v = 0.0;
+    if (i < n && j < n) v = yh[svec_idx(min(i, j), max(i, j), n)];
+    V[e] = v;
+  }
+}
+
+// B^T(y) blocks: P-block j: sum_h beta_{h,j} V_h(y); Lyapunov m: -(S_m + S_m^T), S_m = sum_h V_h H_{h,m}.
+__global__ void k_apply_out(const double* __restrict__ arena, int64_t ms, int np, int n, int64_t Ntil, int64_t L,
+                            const double* __restrict__ y, const int32_t* __restrict__ bP_beg,
+                            const int32_t* __restrict__ bP_h, const double* __restrict__ bP_w, int64_t id_S,
+                            double* __restrict__ out) {
+  const int64_t b = blockIdx.x;
+  double* o = out + b * n * n;
+  if (b < L) {
+    const int e0 = bP_beg[b], e1 = bP_beg[b + 1];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      const int64_t k = svec_idx(min(i, j), max(i, j), n);
+      double v = 0.0;
+      for (int q = e0; q < e1; ++q) v += bP_w[q] * y[(int64_t)bP_h[q] * Ntil + k];
+      o[e] = v;
+    }
+  } else {
+    const double* S = arena + (id_S + (b - L)) * ms;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      o[e] = -(S[i * np + j] + S[j * np + i]);
+    }
+  }
+}
+
+// y_(h,k) = sum_{j: beta_hj != 0} beta_hj [Xs_j]_k - 2 sum_{m: H_hm != 0} [H_hm Xs_m]_k,
+// [M]_k = M_aa (k diagonal) or M_ab + M_ba, Xs = sym(X) (polya_adjoint), T_t = H_t Xs_m in the arena.
+__global__ void k_adjoint_reduce(const double* __restrict__ arena, int64_t ms, int np, int n, int64_t Ntil,
+                                 const int32_t* __restrict__ hP_beg, const int32_t* __restrict__ hP_j,
+                                 const double* __restrict__ hP_w, const int32_t* __restrict__ hL_beg,
+                                 const int32_t* __restrict__ hL_t, int64_t id_Xt, int64_t id_T,
+                                 double* __restrict__ y) {
+  const int h = blockIdx.y;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= Ntil) return;
+  // invert svec_idx: diagonal first, then offsets o = 1.. with n - o entries each
+  int a, b;
+  if (k < n) { a = b = (int)k; }
+  else {
+    int64_t r = k - n;
+    int o = 1;
+    while (r >= n - o) { r -= n - o; ++o; }
+    a = (int)r;
+    b = a + o;
+  }
+  const int64_t ab = (int64_t)a * np + b, ba = (int64_t)b * np + a;
+  double v = 0.0;
+  for (int q = hP_beg[h]; q < hP_beg[h + 1]; ++q) {
+    const double* X = arena + (id_Xt + hP_j[q]) * ms;
+    v += hP_w[q] * (a == b ? X[ab] : X[ab] + X[ba]);
+  }
+  for (int q = hL_beg[h]; q < hL_beg[h + 1]; ++q) {
+    const double* T = arena + (id_T + hL_t[q]) * ms;
+    v -= 2.0 * (a == b ? T[ab] : T[ab] + T[ba]);
+  }
+  y[(int64_t)h * Ntil + k] = v;
+}
+
+}  // namespace
+
+cudaError_t launch_setup_H(Ctx& c, cudaStream_t s) {
+  const int64_t nnzH = (int64_t)c.Hh.size();
+  if (nnzH == 0) return cudaSuccess;
+  k_setup_H<<<(unsigned)nnzH, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, (int)c.nA, c.dA, c.dHw, c.id_H);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_copy(Ctx& c, const double* src, int64_t id0, int64_t count, int sym, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  k_pad_copy<<<(unsigned)count, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, src, id0, sym);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, int64_t nitems, cudaStream_t s) {
+  if (nitems == 0) return cudaSuccess;
+  const int tiles = (int)((c.np + GT - 1) / GT);
+  for (int64_t off = 0; off < nitems; off += 65535) {
+    const int64_t cnt = std::min<int64_t>(65535, nitems - off);
+    dim3 grid((unsigned)(tiles * tiles), (unsigned)cnt);
+    k_gemm<<<grid, 128, 0, s>>>(c.arena, c.mstride, (int)c.np, items + off, terms, tiles);
+    ++c.launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s) {
+  k_vmap<<<(unsigned)c.L0, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.Ntil, y, c.id_Vy);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s) {
+  k_apply_out<<<(unsigned)c.nb, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.Ntil, c.L, y, c.d_bP_beg,
+                                              c.d_bP_h, c.d_bP_w, c.id_S, out);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s) {
+  dim3 grid((unsigned)((c.Ntil + 127) / 128), (unsigned)c.L0);
+  k_adjoint_reduce<<<grid, 128, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.Ntil, c.d_hP_beg, c.d_hP_j,
+                                         c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.id_Xt, c.id_T, y);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+}  // namespace polya

@@ -1,0 +1,601 @@
+// polya_host.cpp -- host side of the C ABI (include/polya.h): Algorithm 1's set-up
+// re-designed for one B200 per rank, plus the entry points that
+// marshal device pointers into the kernels of kernels.cu / schur.cu / ipm.cu.
+//
+// Set-up uses the closed forms of the Polya coefficients:
+//   beta_{h,gamma} = multinomial(d1; gamma - h)                        (Eq. beta)
+//   H_{h,gamma}    = sum_{lambda in W_da} multinomial(d2; gamma-h-lambda) A_lambda  (Eq. H, 226-235)
+//   c_gamma        = delta * multinomial(dp + d1; gamma)               (Eq. Cj, 347-351)
+// which equal the paper's recursions (each recursion step is one multiplication by
+// sum_i alpha_i, so d steps give the multinomial expansion of (sum_i alpha_i)^d).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "polya_internal.h"
+
+using namespace polya;
+
+namespace {
+
+struct Fail {
+  polya_status s;
+  std::string msg;
+};
+
+#define CU(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) throw Fail{POLYA_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+int64_t mul_chk(int64_t a, int64_t b) {
+  int64_t r;
+  if (__builtin_mul_overflow(a, b, &r)) throw Fail{POLYA_EOVERFLOW, "int64 overflow"};
+  return r;
+}
+int64_t add_chk(int64_t a, int64_t b) {
+  int64_t r;
+  if (__builtin_add_overflow(a, b, &r)) throw Fail{POLYA_EOVERFLOW, "int64 overflow"};
+  return r;
+}
+
+// C(nn, kk), checked.
+int64_t binom(int64_t nn, int64_t kk) {
+  if (kk < 0 || kk > nn) return 0;
+  kk = std::min(kk, nn - kk);
+  __int128 r = 1;
+  for (int64_t i = 0; i < kk; ++i) {
+    r = r * (nn - i) / (i + 1);
+    if (r > (__int128)INT64_MAX) throw Fail{POLYA_EOVERFLOW, "binomial overflow"};
+  }
+  return (int64_t)r;
+}
+
+// Eq. (2): f(l, d) = C(l + d - 1, l - 1), 0 for l = 0.
+int64_t card(int64_t l, int64_t d) { return l == 0 ? 0 : binom(add_chk(l, d) - 1, l - 1); }
+
+// multinomial(d; parts) = prod_i C(p_1 + .. + p_i, p_i); 0 if a part is negative or sum != d.
+int64_t multinomial(int64_t d, const int32_t* parts, int64_t l) {
+  int64_t s = 0, r = 1;
+  for (int64_t i = 0; i < l; ++i) {
+    if (parts[i] < 0) return 0;
+    s += parts[i];
+    r = mul_chk(r, binom(s, parts[i]));
+  }
+  return s == d ? r : 0;
+}
+
+// W_d in the prose order of PAPER.md:58 (reading R1): descending lexicographic.
+void enumerate(int64_t l, int64_t d, std::vector<int32_t>& out) {
+  out.clear();
+  std::vector<int32_t> cur(l, 0);
+  // recursive descent: position i takes values from `rem` down to 0
+  struct Rec {
+    static void go(int64_t i, int64_t l, int64_t rem, std::vector<int32_t>& cur, std::vector<int32_t>& out) {
+      if (i == l - 1) {
+        cur[i] = (int32_t)rem;
+        out.insert(out.end(), cur.begin(), cur.end());
+        return;
+      }
+      for (int64_t v = rem; v >= 0; --v) {
+        cur[i] = (int32_t)v;
+        go(i + 1, l, rem - v, cur, out);
+      }
+    }
+  };
+  Rec::go(0, l, d, cur, out);
+}
+
+template <class T>
+T* dalloc(int64_t count) {
+  if (count <= 0) return nullptr;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Fail{POLYA_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+  }
+  return (T*)p;
+}
+template <class T>
+T* dupload(const std::vector<T>& v) {
+  T* p = dalloc<T>((int64_t)v.size());
+  if (p) CU(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+void build(Ctx& c, const double* A_host) {
+  const polya_config& g = c.cfg;
+  c.n = g.n;
+  c.l = g.l;
+  c.L0 = card(g.l, g.dp);
+  c.L = card(g.l, (int64_t)g.dp + g.d1);
+  c.M = card(g.l, (int64_t)g.dp + g.da + g.d2);
+  c.nA = card(g.l, g.da);
+  c.nb = add_chk(c.L, c.M);
+  c.Ntil = mul_chk(c.n, c.n + 1) / 2;
+  c.K = mul_chk(c.L0, c.Ntil);
+  (void)mul_chk(c.K, c.K);  // K*K must be representable (FULL layout indexing)
+  c.np = (c.n + kChunk - 1) / kChunk * kChunk;
+  c.r = c.np / kChunk;
+  c.ncls = c.r * (c.r + 1) / 2;
+  c.mstride = mul_chk(c.np, c.np);
+  const int64_t l = c.l;
+
+  enumerate(l, g.dp, c.Wp);
+  enumerate(l, (int64_t)g.dp + g.d1, c.WL);
+  enumerate(l, (int64_t)g.dp + g.da + g.d2, c.WM);
+  enumerate(l, g.da, c.Wa);
+  if ((int64_t)c.Wp.size() != c.L0 * l || (int64_t)c.WL.size() != c.L * l ||
+      (int64_t)c.WM.size() != c.M * l || (int64_t)c.Wa.size() != c.nA * l)
+    throw Fail{POLYA_EOVERFLOW, "enumeration size mismatch"};
+
+  // beta (Eq. beta) and C (Eq. Cj)
+  std::vector<int32_t> tmp(l);
+  c.beta.assign(c.L0 * c.L, 0);
+  c.c.assign(c.L, 0.0);
+  c.nnz_beta = 0;
+  for (int64_t j = 0; j < c.L; ++j) {
+    const int32_t* gj = &c.WL[j * l];
+    for (int64_t h = 0; h < c.L0; ++h) {
+      for (int64_t i = 0; i < l; ++i) tmp[i] = gj[i] - c.Wp[h * l + i];
+      int64_t b = multinomial(g.d1, tmp.data(), l);
+      c.beta[h * c.L + j] = b;
+      if (b) ++c.nnz_beta;
+    }
+    c.c[j] = g.delta * (double)multinomial((int64_t)g.dp + g.d1, gj, l);
+  }
+  // nonzero H entries (h, m), m-major, with their integer weights per lambda
+  c.Hidx.assign(c.L0 * c.M, -1);
+  c.Hh.clear(); c.Hm.clear(); c.Hw.clear();
+  std::vector<double> w(c.nA);
+  for (int64_t m = 0; m < c.M; ++m) {
+    const int32_t* gm = &c.WM[m * l];
+    for (int64_t h = 0; h < c.L0; ++h) {
+      bool nz = false;
+      for (int64_t a = 0; a < c.nA; ++a) {
+        for (int64_t i = 0; i < l; ++i) tmp[i] = gm[i] - c.Wp[h * l + i] - c.Wa[a * l + i];
+        int64_t v = multinomial(g.d2, tmp.data(), l);
+        w[a] = (double)v;
+        if (v) nz = true;
+      }
+      if (!nz) continue;
+      c.Hidx[h * c.M + m] = (int32_t)c.Hh.size();
+      c.Hh.push_back((int32_t)h);
+      c.Hm.push_back((int32_t)m);
+      c.Hw.insert(c.Hw.end(), w.begin(), w.end());
+    }
+  }
+  const int64_t nnzH = (int64_t)c.Hh.size();
+
+  // ---- pairs (h <= h'), their k-entries, work items, rank partition ---------------------------
+  c.npairs = c.L0 * (c.L0 + 1) / 2;
+  std::vector<int32_t> ph(c.npairs), ph2(c.npairs);
+  std::vector<int64_t> pK(c.npairs), pItems(c.npairs);
+  {
+    int64_t p = 0;
+    for (int64_t h = 0; h < c.L0; ++h)
+      for (int64_t h2 = h; h2 < c.L0; ++h2, ++p) {
+        ph[p] = (int32_t)h;
+        ph2[p] = (int32_t)h2;
+        int64_t kp = 0;
+        for (int64_t m = 0; m < c.M; ++m)
+          if (c.Hidx[h * c.M + m] >= 0 && c.Hidx[h2 * c.M + m] >= 0) kp += 4;
+        for (int64_t j = 0; j < c.L; ++j)
+          if (c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) kp += 1;
+        pK[p] = kp;
+        pItems[p] = (h == h2) ? c.ncls * (c.ncls + 1) / 2 : c.ncls * c.ncls;
+      }
+  }
+  c.pair_item_global.assign(c.npairs + 1, 0);
+  std::vector<double> cost_prefix(c.npairs + 1, 0.0);
+  double n4 = (double)c.n * c.n * c.n * c.n;
+  c.useful_flops_total = 0;
+  for (int64_t p = 0; p < c.npairs; ++p) {
+    c.pair_item_global[p + 1] = add_chk(c.pair_item_global[p], pItems[p]);
+    cost_prefix[p + 1] = cost_prefix[p] + (double)pItems[p] * (double)std::max<int64_t>(pK[p], 1);
+    c.useful_flops_total += (ph[p] == ph2[p] ? 1.0 : 2.0) * n4 * (double)pK[p];
+  }
+  c.items_total = c.pair_item_global[c.npairs];
+  auto item_at_cost = [&](double target) -> int64_t {
+    if (target <= 0) return 0;
+    if (target >= cost_prefix[c.npairs]) return c.items_total;
+    int64_t p = std::upper_bound(cost_prefix.begin(), cost_prefix.end(), target) - cost_prefix.begin() - 1;
+    double per = (double)std::max<int64_t>(pK[p], 1);
+    int64_t within = (int64_t)std::ceil((target - cost_prefix[p]) / per);
+    return std::min(c.pair_item_global[p] + within, c.pair_item_global[p + 1]);
+  };
+  const double total_cost = cost_prefix[c.npairs];
+  c.item0 = item_at_cost(total_cost * g.rank / g.nranks);
+  c.item1 = item_at_cost(total_cost * (g.rank + 1) / g.nranks);
+  if (g.rank == g.nranks - 1) c.item1 = c.items_total;
+  if (g.rank == 0) c.item0 = 0;
+  c.pair0 = c.pair1 = 0;
+  if (c.item1 > c.item0) {
+    c.pair0 = std::upper_bound(c.pair_item_global.begin(), c.pair_item_global.end(), c.item0) -
+              c.pair_item_global.begin() - 1;
+    c.pair1 = std::upper_bound(c.pair_item_global.begin(), c.pair_item_global.end(), c.item1 - 1) -
+              c.pair_item_global.begin();
+  }
+  c.useful_flops_rank = 0;
+  for (int64_t p = c.pair0; p < c.pair1; ++p) {
+    int64_t a = std::max(c.item0, c.pair_item_global[p]), b = std::min(c.item1, c.pair_item_global[p + 1]);
+    c.useful_flops_rank += (ph[p] == ph2[p] ? 1.0 : 2.0) * n4 * pK[p] * (double)(b - a) / (double)pItems[p];
+  }
+  c.npairs_local = c.pair1 - c.pair0;
+
+  // ---- arena layout --------------------------------------------------------------------------
+  // Q, R: one per (local pair, Lyapunov block active for both rows)
+  int64_t nQR = 0;
+  for (int64_t p = c.pair0; p < c.pair1; ++p) nQR += (pK[p] - [&] {
+      int64_t v = 0;
+      for (int64_t j = 0; j < c.L; ++j)
+        if (c.beta[ph[p] * c.L + j] && c.beta[ph2[p] * c.L + j]) ++v;
+      return v;
+    }()) / 4;
+  c.nQR = nQR;
+  int64_t id = 0;
+  c.id_X = id; id += c.nb;
+  c.id_W = id; id += c.nb;
+  c.id_H = id; id += nnzH;
+  c.id_U = id; id += nnzH;
+  c.id_V = id; id += nnzH;
+  c.id_Q = id; id += nQR;
+  c.id_R = id; id += nQR;
+  c.id_Xt = id; id += c.nb;
+  c.id_T = id; id += nnzH;
+  c.id_Vy = id; id += c.L0;
+  c.id_S = id; id += c.M;
+  c.nmats = id;
+  if (c.nmats > INT32_MAX) throw Fail{POLYA_EOVERFLOW, "too many arena matrices"};
+  c.arena = dalloc<double>(mul_chk(c.nmats, c.mstride));
+  CU(cudaMemset(c.arena, 0, (size_t)c.nmats * c.mstride * sizeof(double)));
+
+  // ---- batched GEMM descriptors ---------------------------------------------------------------
+  {
+    std::vector<GemmItem> it;
+    std::vector<GemmTerm> tm;
+    // U_t = H_t X_{L+m}, V_t = H_t W_{L+m}     (a7: SCM precompute)
+    for (int64_t t = 0; t < nnzH; ++t) {
+      int32_t b = (int32_t)(c.L + c.Hm[t]);
+      it.push_back({(int32_t)(c.id_U + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_X + b), 0, 0, 1.0});
+      it.push_back({(int32_t)(c.id_V + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_W + b), 0, 0, 1.0});
+    }
+    c.n_items_UV = (int64_t)it.size();
+    c.d_items_UV = dupload(it);
+    c.d_terms_UV = dupload(tm);
+    // adjoint: T_t = H_t Xt_{L+m}
+    it.clear(); tm.clear();
+    for (int64_t t = 0; t < nnzH; ++t) {
+      it.push_back({(int32_t)(c.id_T + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_Xt + c.L + c.Hm[t]), 0, 0, 1.0});
+    }
+    c.n_items_T = (int64_t)it.size();
+    c.d_items_T = dupload(it);
+    c.d_terms_T = dupload(tm);
+    // apply: S_m = sum_h V_h(y) H_{h,m}
+    it.clear(); tm.clear();
+    for (int64_t m = 0; m < c.M; ++m) {
+      int32_t b0 = (int32_t)tm.size();
+      for (int64_t h = 0; h < c.L0; ++h) {
+        int32_t t = c.Hidx[h * c.M + m];
+        if (t >= 0) tm.push_back({(int32_t)(c.id_Vy + h), (int32_t)(c.id_H + t), 0, 0, 1.0});
+      }
+      it.push_back({(int32_t)(c.id_S + m), b0, (int32_t)tm.size(), 0});
+    }
+    c.n_items_S = (int64_t)it.size();
+    c.d_items_S = dupload(it);
+    c.d_terms_S = dupload(tm);
+  }
+
+  // ---- Schur tables for this rank's pairs ------------------------------------------------------
+  {
+    std::vector<int32_t> qh, qh2, kL, kR, kf;
+    std::vector<int64_t> kbeg, pitem;
+    std::vector<double> ks;
+    std::vector<GemmItem> it;
+    std::vector<GemmTerm> tm;
+    int64_t q = 0;
+    kbeg.push_back(0);
+    pitem.push_back(c.pair_item_global[c.pair0]);
+    for (int64_t p = c.pair0; p < c.pair1; ++p) {
+      const int64_t h = ph[p], h2 = ph2[p];
+      qh.push_back((int32_t)h);
+      qh2.push_back((int32_t)h2);
+      for (int64_t m = 0; m < c.M; ++m) {
+        int32_t th = c.Hidx[h * c.M + m], th2 = c.Hidx[h2 * c.M + m];
+        if (th < 0 || th2 < 0) continue;
+        const int32_t b = (int32_t)(c.L + m);
+        const int32_t idQ = (int32_t)(c.id_Q + q), idR = (int32_t)(c.id_R + q);
+        // Q_{hh'} = U_h H_{h'}^T,  R_{h'h} = V_{h'} H_h^T
+        it.push_back({idQ, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        tm.push_back({(int32_t)(c.id_U + th), (int32_t)(c.id_H + th2), 1, 0, 1.0});
+        it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        tm.push_back({(int32_t)(c.id_V + th2), (int32_t)(c.id_H + th), 1, 0, 1.0});
+        ++q;
+        // T1 = U_{h'}^T[b1,c1] V_h^T[d1,a1]; T2 = X[b1,c1] R_{h'h}[d1,a1];
+        // T3 = Q_{hh'}[b1,c1] W[d1,a1];     T4 = U_h[b1,c1] V_{h'}[d1,a1]   (O7)
+        kL.push_back((int32_t)(c.id_U + th2)); kR.push_back((int32_t)(c.id_V + th)); kf.push_back(3); ks.push_back(1.0);
+        kL.push_back((int32_t)(c.id_X + b));   kR.push_back(idR);                     kf.push_back(0); ks.push_back(1.0);
+        kL.push_back(idQ);                     kR.push_back((int32_t)(c.id_W + b));   kf.push_back(0); ks.push_back(1.0);
+        kL.push_back((int32_t)(c.id_U + th));  kR.push_back((int32_t)(c.id_V + th2)); kf.push_back(0); ks.push_back(1.0);
+      }
+      for (int64_t j = 0; j < c.L; ++j) {
+        int64_t b1 = c.beta[h * c.L + j], b2 = c.beta[h2 * c.L + j];
+        if (!b1 || !b2) continue;
+        kL.push_back((int32_t)(c.id_X + j)); kR.push_back((int32_t)(c.id_W + j)); kf.push_back(0);
+        ks.push_back((double)b1 * (double)b2);
+      }
+      kbeg.push_back((int64_t)kL.size());
+      pitem.push_back(c.pair_item_global[p + 1]);
+    }
+    c.nk_local = (int64_t)kL.size();
+    c.n_items_QR = (int64_t)it.size();
+    c.d_items_QR = dupload(it);
+    c.d_terms_QR = dupload(tm);
+    c.st.pair_h = dupload(qh);
+    c.st.pair_h2 = dupload(qh2);
+    c.st.pair_kbeg = dupload(kbeg);
+    c.st.pair_item = dupload(pitem);
+    c.st.k_L = dupload(kL);
+    c.st.k_R = dupload(kR);
+    c.st.k_flags = dupload(kf);
+    c.st.k_scale = dupload(ks);
+    std::vector<int32_t> ca, cb;
+    for (int64_t i = 0; i < c.r; ++i)
+      for (int64_t j = i; j < c.r; ++j) { ca.push_back((int32_t)i); cb.push_back((int32_t)j); }
+    c.st.cls_a = dupload(ca);
+    c.st.cls_b = dupload(cb);
+    c.st.counter = dalloc<unsigned long long>(1);
+  }
+
+  // ---- apply / adjoint tables -------------------------------------------------------------------
+  {
+    std::vector<int32_t> bbeg{0}, bh, hbeg{0}, hj, lbeg{0}, lt, lm;
+    std::vector<double> bw, hw;
+    for (int64_t j = 0; j < c.L; ++j) {
+      for (int64_t h = 0; h < c.L0; ++h)
+        if (c.beta[h * c.L + j]) { bh.push_back((int32_t)h); bw.push_back((double)c.beta[h * c.L + j]); }
+      bbeg.push_back((int32_t)bh.size());
+    }
+    for (int64_t h = 0; h < c.L0; ++h) {
+      for (int64_t j = 0; j < c.L; ++j)
+        if (c.beta[h * c.L + j]) { hj.push_back((int32_t)j); hw.push_back((double)c.beta[h * c.L + j]); }
+      hbeg.push_back((int32_t)hj.size());
+      for (int64_t m = 0; m < c.M; ++m)
+        if (c.Hidx[h * c.M + m] >= 0) { lt.push_back(c.Hidx[h * c.M + m]); lm.push_back((int32_t)m); }
+      lbeg.push_back((int32_t)lt.size());
+    }
+    c.d_bP_beg = dupload(bbeg); c.d_bP_h = dupload(bh); c.d_bP_w = dupload(bw);
+    c.d_hP_beg = dupload(hbeg); c.d_hP_j = dupload(hj); c.d_hP_w = dupload(hw);
+    c.d_hL_beg = dupload(lbeg); c.d_hL_t = dupload(lt); c.d_hL_m = dupload(lm);
+  }
+
+  // ---- H on the device (kernel K1) ----------------------------------------------------------------
+  c.dA = dalloc<double>(mul_chk(c.nA, mul_chk(c.n, c.n)));
+  CU(cudaMemcpy(c.dA, A_host, (size_t)c.nA * c.n * c.n * sizeof(double), cudaMemcpyHostToDevice));
+  c.dHw = dupload(c.Hw);
+  CU(launch_setup_H(c, 0));
+  CU(cudaDeviceSynchronize());
+}
+
+void free_ctx(Ctx& c) {
+  void* ps[] = {c.arena, c.dA, c.dHw, c.dHm, c.dHgam, c.d_items_UV, c.d_terms_UV, c.d_items_QR, c.d_terms_QR,
+                c.d_items_T, c.d_terms_T, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
+                c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
+                c.st.pair_kbeg, c.st.pair_item, c.st.k_L, c.st.k_R, c.st.k_flags, c.st.k_scale,
+                c.st.cls_a, c.st.cls_b, c.st.counter};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+}
+
+polya_status fail(polya_ctx* ctx, const Fail& f) {
+  if (ctx) ctx->c.last_error = f.msg;
+  return f.s;
+}
+
+}  // namespace
+
+// ---- ABI ----------------------------------------------------------------------------------------
+
+extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_host, polya_ctx** out) {
+  if (!out) return POLYA_EINVAL;
+  *out = nullptr;
+  if (!cfg || !A_host) return POLYA_EINVAL;
+  const polya_config& g = *cfg;
+  if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
+      g.rank < 0 || g.rank >= g.nranks)
+    return POLYA_EINVAL;
+  polya_ctx* ctx = new (std::nothrow) polya_ctx();
+  if (!ctx) return POLYA_ENOMEM;
+  ctx->c.cfg = g;
+  try {
+    if (cudaGetDevice(&ctx->c.device) != cudaSuccess) throw Fail{POLYA_ECUDA, "no CUDA device"};
+    build(ctx->c, A_host);
+  } catch (const Fail& f) {
+    polya_status s = f.s;
+    fprintf(stderr, "polya_setup: %s\n", f.msg.c_str());
+    free_ctx(ctx->c);
+    delete ctx;
+    return s;
+  } catch (const std::bad_alloc&) {
+    free_ctx(ctx->c);
+    delete ctx;
+    return POLYA_ENOMEM;
+  }
+  *out = ctx;
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* o) {
+  if (!ctx || !o) return POLYA_EINVAL;
+  const Ctx& c = ctx->c;
+  o->L0 = c.L0; o->L = c.L; o->M = c.M; o->nblocks = c.nb; o->Ntil = c.Ntil; o->K = c.K;
+  o->nnz_beta = c.nnz_beta; o->nnz_H = (int64_t)c.Hh.size();
+  o->npairs = c.npairs; o->pair0 = c.pair0; o->pair1 = c.pair1; o->item0 = c.item0; o->item1 = c.item1;
+  o->useful_flops_schur = c.useful_flops_rank;
+  o->tiles_bytes = c.npairs_local * c.Ntil * c.Ntil * (int64_t)sizeof(double);
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_get_exponents(const polya_ctx* ctx, int which, int32_t* out) {
+  if (!ctx || !out) return POLYA_EINVAL;
+  const Ctx& c = ctx->c;
+  const std::vector<int32_t>* v = which == 0 ? &c.Wp : which == 1 ? &c.WL : which == 2 ? &c.WM : which == 3 ? &c.Wa : nullptr;
+  if (!v) return POLYA_EINVAL;
+  std::memcpy(out, v->data(), v->size() * sizeof(int32_t));
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_get_beta(const polya_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return POLYA_EINVAL;
+  std::memcpy(out, ctx->c.beta.data(), ctx->c.beta.size() * sizeof(int64_t));
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_get_C(const polya_ctx* ctx, double* out) {
+  if (!ctx || !out) return POLYA_EINVAL;
+  std::memcpy(out, ctx->c.c.data(), ctx->c.c.size() * sizeof(double));
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_get_H(const polya_ctx* ctx, double* out) {
+  if (!ctx || !out) return POLYA_EINVAL;
+  const Ctx& c = ctx->c;
+  const int64_t n = c.n, nn = n * n;
+  std::memset(out, 0, (size_t)c.L0 * c.M * nn * sizeof(double));
+  std::vector<double> buf(c.mstride);
+  for (size_t t = 0; t < c.Hh.size(); ++t) {
+    cudaError_t e = cudaMemcpy(buf.data(), c.arena + (c.id_H + (int64_t)t) * c.mstride, c.mstride * sizeof(double),
+                               cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      const_cast<polya_ctx*>(ctx)->c.last_error = cudaGetErrorString(e);
+      return POLYA_ECUDA;
+    }
+    double* dst = out + ((int64_t)c.Hh[t] * c.M + c.Hm[t]) * nn;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) dst[i * n + j] = buf[i * c.np + j];
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_apply(polya_ctx* ctx, const double* y, double* out, void* stream) {
+  if (!ctx || !y || !out) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    CU(launch_vmap(c, y, s));
+    CU(launch_gemm(c, c.d_items_S, c.d_terms_S, c.n_items_S, s));
+    CU(launch_apply_out(c, y, out, s));
+  } catch (const Fail& f) {
+    return fail(ctx, f);
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_adjoint(polya_ctx* ctx, const double* X, double* y, void* stream) {
+  if (!ctx || !X || !y) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    CU(launch_pad_copy(c, X, c.id_Xt, c.nb, 1, s));
+    CU(launch_gemm(c, c.d_items_T, c.d_terms_T, c.n_items_T, s));
+    CU(launch_adjoint_reduce(c, y, s));
+  } catch (const Fail& f) {
+    return fail(ctx, f);
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_schur(polya_ctx* ctx, const double* X, const double* Zinv, double* G, int layout,
+                                    void* stream) {
+  if (!ctx || !X || !Zinv || !G) return POLYA_EINVAL;
+  if (layout != POLYA_G_FULL && layout != POLYA_G_PAIR_TILES) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    if (c.timing) CU(cudaEventRecord(c.ev[0], s));
+    CU(launch_pad_copy(c, X, c.id_X, c.nb, 0, s));
+    CU(launch_pad_copy(c, Zinv, c.id_W, c.nb, 0, s));
+    CU(launch_gemm(c, c.d_items_UV, c.d_terms_UV, c.n_items_UV, s));
+    CU(launch_gemm(c, c.d_items_QR, c.d_terms_QR, c.n_items_QR, s));
+    if (c.timing) CU(cudaEventRecord(c.ev[1], s));
+    CU(launch_schur(c, G, layout, s));
+    if (c.timing) CU(cudaEventRecord(c.ev[2], s));
+  } catch (const Fail& f) {
+    return fail(ctx, f);
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_set_timing(polya_ctx* ctx, int enable) {
+  if (!ctx) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (enable && !c.ev[0]) {
+    for (auto& e : c.ev)
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        c.last_error = "cudaEventCreate failed";
+        return POLYA_ECUDA;
+      }
+  }
+  c.timing = enable != 0;
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_get_timing(polya_ctx* ctx, float* ms_pre, float* ms_assemble) {
+  if (!ctx || !ms_pre || !ms_assemble) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (!c.ev[0]) return POLYA_EINVAL;
+  if (cudaEventSynchronize(c.ev[2]) != cudaSuccess || cudaEventElapsedTime(ms_pre, c.ev[0], c.ev[1]) != cudaSuccess ||
+      cudaEventElapsedTime(ms_assemble, c.ev[1], c.ev[2]) != cudaSuccess) {
+    c.last_error = "timing events not recorded";
+    return POLYA_ECUDA;
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_sync(polya_ctx* ctx) {
+  if (!ctx) return POLYA_EINVAL;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ctx->c.last_error = cudaGetErrorString(e);
+    return POLYA_ECUDA;
+  }
+  return POLYA_OK;
+}
+
+extern "C" const char* polya_strerror(polya_status s) {
+  switch (s) {
+    case POLYA_OK: return "ok";
+    case POLYA_EINVAL: return "invalid argument";
+    case POLYA_EOVERFLOW: return "integer overflow in problem size";
+    case POLYA_ENOMEM: return "out of memory";
+    case POLYA_ECUDA: return "CUDA error";
+    case POLYA_ENCCL: return "NCCL error";
+    case POLYA_ENOTPD: return "matrix not positive definite";
+    case POLYA_ESTEP: return "no admissible step";
+    case POLYA_EMAXIT: return "iteration limit";
+  }
+  return "unknown status";
+}
+
+extern "C" const char* polya_last_error(const polya_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : ""; }
+
+extern "C" int64_t polya_launch_count(const polya_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+void polya_ipm_free(polya::Ctx& c);  // ipm.cu
+
+extern "C" void polya_destroy(polya_ctx* ctx) {
+  if (!ctx) return;
+  polya_ipm_free(ctx->c);
+  for (auto& e : ctx->c.ev)
+    if (e) cudaEventDestroy(e);
+  free_ctx(ctx->c);
+  delete ctx;
+}

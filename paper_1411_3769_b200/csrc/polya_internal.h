@@ -1,0 +1,112 @@
+// polya_internal.h -- context layout and kernel launchers shared by polya_host.cpp and the .cu files.
+// Not part of the ABI (include/polya.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/polya.h"
+
+namespace polya {
+
+constexpr int kChunk = 8;  // index chunk q of the Schur "class blocks" (kernel K4)
+
+// One term of a batched GEMM item: C += alpha * A[a_id] * op(B[b_id]), all np x np arena matrices.
+struct GemmTerm {
+  int32_t a_id, b_id;
+  int32_t transB;
+  int32_t pad_;
+  double alpha;
+};
+// One output matrix of a batched GEMM: C[c_id] = sum_{t in [tbeg,tend)} terms[t].
+struct GemmItem {
+  int32_t c_id, tbeg, tend, pad_;
+};
+
+// Device-side tables of the Schur assembly (kernel K4).
+struct SchurTables {
+  int32_t* pair_h = nullptr;      // [npairs_local]      h  (row block of the pair)
+  int32_t* pair_h2 = nullptr;     // [npairs_local]      h' (column block), h <= h'
+  int64_t* pair_kbeg = nullptr;   // [npairs_local + 1]  k-entry range of each pair
+  int64_t* pair_item = nullptr;   // [npairs_local + 1]  global work-item prefix (offset item_base)
+  int32_t* k_L = nullptr;         // [nk] arena id of the left factor  L_k
+  int32_t* k_R = nullptr;         // [nk] arena id of the right factor R_k
+  int32_t* k_flags = nullptr;     // [nk] bit0: L transposed, bit1: R transposed
+  double* k_scale = nullptr;      // [nk] scale of L_k (beta_h beta_h' on P-block terms, else 1)
+  int32_t* cls_a = nullptr;       // [ncls] chunk index i of class (i <= j)
+  int32_t* cls_b = nullptr;       // [ncls] chunk index j
+  unsigned long long* counter = nullptr;  // dynamic work counter
+};
+
+struct Ctx {
+  polya_config cfg{};
+  int device = 0;
+  int64_t n = 0, l = 0, L0 = 0, L = 0, M = 0, nb = 0, Ntil = 0, K = 0, nA = 0;
+  int64_t np = 0;        // padded matrix dimension (multiple of kChunk)
+  int64_t r = 0;         // number of index chunks = np / kChunk
+  int64_t ncls = 0;      // r (r+1) / 2 unordered chunk classes
+  std::vector<int32_t> Wp, WL, WM, Wa;  // exponent tables, row-major [count][l]
+  std::vector<int64_t> beta;           // [L0][L]
+  std::vector<double> c;               // [L]
+  std::vector<int32_t> Hh, Hm;         // nonzero H entries t -> (h, m), m-major
+  std::vector<int32_t> Hidx;           // [L0][M] -> t or -1
+  std::vector<double> Hw;              // [nnzH][nA] integer weights multinomial(d2; gamma-h-lambda)
+  // pairs and work items
+  int64_t npairs = 0, pair0 = 0, pair1 = 0;
+  int64_t items_total = 0, item0 = 0, item1 = 0;
+  std::vector<int64_t> pair_item_global;  // [npairs + 1]
+  double useful_flops_total = 0, useful_flops_rank = 0;
+  // arena (np x np matrices)
+  int64_t mstride = 0, nmats = 0;
+  int64_t id_X = 0, id_W = 0, id_H = 0, id_U = 0, id_V = 0, id_Q = 0, id_R = 0, id_Xt = 0, id_T = 0,
+          id_Vy = 0, id_S = 0;
+  int64_t nQR = 0;
+  double* arena = nullptr;
+  double* dA = nullptr;
+  double* dHw = nullptr;
+  int32_t* dHm = nullptr;   // [nnzH] (h, m) for setup_H: packed pairs
+  int32_t* dHgam = nullptr; // [nnzH][nA][l] unused placeholder
+  // batched gemm descriptors
+  GemmItem* d_items_UV = nullptr; GemmTerm* d_terms_UV = nullptr; int64_t n_items_UV = 0;
+  GemmItem* d_items_QR = nullptr; GemmTerm* d_terms_QR = nullptr; int64_t n_items_QR = 0;
+  GemmItem* d_items_T = nullptr; GemmTerm* d_terms_T = nullptr; int64_t n_items_T = 0;
+  GemmItem* d_items_S = nullptr; GemmTerm* d_terms_S = nullptr; int64_t n_items_S = 0;
+  // apply / adjoint tables
+  int32_t* d_bP_beg = nullptr;   // [L+1]  P-block active-h ranges
+  int32_t* d_bP_h = nullptr;     // [nnz_beta]
+  double* d_bP_w = nullptr;      // [nnz_beta] beta
+  int32_t* d_hP_beg = nullptr;   // [L0+1]  per h: P-blocks with beta != 0
+  int32_t* d_hP_j = nullptr;
+  double* d_hP_w = nullptr;
+  int32_t* d_hL_beg = nullptr;   // [L0+1]  per h: nonzero H entries t (m ascending)
+  int32_t* d_hL_t = nullptr;
+  int32_t* d_hL_m = nullptr;
+  int64_t nnz_beta = 0;
+  SchurTables st;
+  int64_t nk_local = 0, npairs_local = 0;
+  // IPM workspace (allocated lazily)
+  void* ipm = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  std::string last_error;
+  int64_t launches = 0;
+};
+
+// ---- kernel launchers (kernels.cu / schur.cu) -------------------------------------------------
+cudaError_t launch_setup_H(Ctx& c, cudaStream_t s);
+cudaError_t launch_pad_copy(Ctx& c, const double* src, int64_t id0, int64_t count, int symmetrize,
+                            cudaStream_t s);
+cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, int64_t nitems,
+                        cudaStream_t s);
+cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
+cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s);
+cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
+cudaError_t launch_schur(Ctx& c, double* G, int layout, cudaStream_t s);
+
+}  // namespace polya
+
+struct polya_ctx {
+  polya::Ctx c;
+};

@@ -1,0 +1,51 @@
+"""CPU-side checks of the C ABI: the library builds for sm_100a, loads, and exports every
+entry point include/polya.h declares (no compute calls: there is no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "polya.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(polya_[A-Za-z_0-9]+)\s*\(", src)))
+
+
+def test_library_builds_loads_and_exports_header_symbols():
+    from paper_1411_3769_b200 import build as b
+    lib_path = b.build()
+    import paper_1411_3769_b200 as pb
+    L = pb.lib()
+    names = _declared()
+    assert len(names) >= 15
+    for nm in names:
+        assert hasattr(L, nm), nm
+    assert set(pb.EXPORTS) <= set(names)
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True).stdout
+    for nm in names:
+        assert re.search(rf"\bT {nm}$", out, flags=re.M), nm
+
+
+def test_sass_is_sm100a_and_uses_fp64_mma():
+    from paper_1411_3769_b200 import build as b
+    lib_path = b.build()
+    out = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "DMMA.8x8x4" in out       # FP64 tensor-core MMA in the Schur / GEMM kernels
+
+
+def test_invalid_arguments_are_rejected_without_a_gpu():
+    import paper_1411_3769_b200 as pb
+    L = pb.lib()
+    h = ctypes.c_void_p()
+    assert L.polya_setup(None, None, ctypes.byref(h)) == 1          # POLYA_EINVAL
+    cfg = pb._Config(0, 2, 1, 1, 1, 1, 1e-3, 0, 1)                    # n = 0
+    assert L.polya_setup(ctypes.byref(cfg), ctypes.c_void_p(1), ctypes.byref(h)) == 1
+    cfg = pb._Config(4, 2, 1, 1, 1, 1, 0.0, 0, 1)                     # delta = 0
+    assert L.polya_setup(ctypes.byref(cfg), ctypes.c_void_p(1), ctypes.byref(h)) == 1
+    cfg = pb._Config(4, 2, 1, 1, 1, 1, 1e-3, 2, 2)                    # rank outside [0, nranks)
+    assert L.polya_setup(ctypes.byref(cfg), ctypes.c_void_p(1), ctypes.byref(h)) == 1
+    assert L.polya_strerror(2) == b"integer overflow in problem size"
