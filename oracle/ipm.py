@@ -1,0 +1,105 @@
+"""One iteration of the primal-dual predictor-corrector method, Algorithm 2.  TEST INFRASTRUCTURE ONLY.
+
+Follows PAPER.md Sec. IV.A (Eqs. 33-46) and Algorithm 2 step by
+step, on block stacks (every iterate lies in S_{L,M,n}, Theorem 3):
+
+  Rd  = -B^T(y) + Z + C                                    (Eq. G; reading R13)
+  O1  = B(Z^-1 Rd X) - a,  a = 1                           (Processors/Root step 1)
+  G   = [tr(B_k Z^-1 B_l X)]                               (Eq. T2)
+  dy^ = G^-1 O1                                            (Eq. SAE1)
+  dZ^ = B^T(y) - Z - C + B^T(dy^) = -Rd + B^T(dy^)         (Eq. delZ_hat)
+  dX^ = -X + Z^-1 (Rd - B^T(dy^)) X, symmetrised           (reading R3)
+  O2  = mu B(Z^-1) - B(Z^-1 dZ^ dX^)                       (Processors/Root step 2)
+  dy- = G^-1 O2                                            (Eq. SAE2)
+  dZ- = B^T(dy-)                                           (Eq. delz_bar)
+  dX- = mu Z^-1 - Z^-1 dZ^ dX^ - Z^-1 dZ- X, symmetrised   (Eq. delx_bar)
+  t_p, t_d: reading R5 (fraction 0.98 of the distance to the PSD boundary, capped at 1)
+  X += t_p dX,  Z += t_d dZ,  y += t_d dy                  (Eqs. 33-35; reading R6)
+  mu = (1/3) sum tr(Z X) / N, N = (L+M) n the order of X (reading R4: the literal (1/3) tr(ZX)
+       of P:591/729/871 makes the target grow ~10x per step and the method diverge on config 1;
+       read as the centring factor 1/3 times the average complementarity),
+  phi = tr(C X),  psi = a^T y,  gap = |phi - psi|
+
+Library primitives used as steps: matrix products, inverse, a dense linear solve and a
+symmetric eigenvalue routine.  Parity with the CUDA path is "iterates to ~1e-8 over a
+few steps" (reading R15: the IPM's certificate is not unique).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import sdp
+
+__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks"]
+
+
+def C_blocks(P):
+    """C = diag(c_1 I, ..., c_L I, 0, ..., 0) (Eq. C, Eq. Cj)."""
+    C = np.zeros((P.nblocks, P.n, P.n))
+    for j in range(P.L):
+        C[j] = P.c[j] * np.eye(P.n)
+    return C
+
+
+def initial_state(P):
+    """Algorithm 2 initialisation: X = Z = I, y = 0, mu = barrier(Z, X)."""
+    X = np.broadcast_to(np.eye(P.n), (P.nblocks, P.n, P.n)).copy()
+    Z = X.copy()
+    y = np.zeros(P.K)
+    return X, Z, y, barrier(P, Z, X)
+
+
+def barrier(P, Z, X):
+    """Reading R4: mu = (1/3) sum_b tr(Z_b X_b) / ((L+M) n)."""
+    return sum(np.trace(Z[b] @ X[b]) for b in range(P.nblocks)) / (3.0 * P.nblocks * P.n)
+
+
+def _sym(M):
+    return 0.5 * (M + np.swapaxes(M, -1, -2))
+
+
+def step_length(S, dS, frac=0.98):
+    """Reading R5: t = min(1, frac * t_max), t_max = sup{t : S_b + t dS_b >= 0 for all b}
+    = 1 / max(0, -min_b lambda_min(L_b^-1 dS_b L_b^-T)), S_b = L_b L_b^T."""
+    lam = np.inf
+    for b in range(S.shape[0]):
+        Lc = np.linalg.cholesky(S[b])
+        Li = np.linalg.inv(Lc)
+        ev = np.linalg.eigvalsh(_sym(Li @ dS[b] @ Li.T))
+        lam = min(lam, ev.min())
+    if lam >= 0:
+        return 1.0
+    return min(1.0, frac * (1.0 / -lam))
+
+
+def ipm_step(P, X, Z, y, mu):
+    """One iteration; returns (X, Z, y, stats)."""
+    C = C_blocks(P)
+    W = np.linalg.inv(Z)
+    W = _sym(W)
+    BTy = sdp.apply_vmap(P, y)
+    Rd = -BTy + Z + C
+    O1 = sdp.adjoint_trace(P, W @ Rd @ X) - 1.0
+    G = sdp.schur_literal(P, X, W)
+    dy1 = np.linalg.solve(G, O1)
+    BTd1 = sdp.apply_vmap(P, dy1)
+    dZ1 = -Rd + BTd1
+    dX1 = _sym(-X + W @ (Rd - BTd1) @ X)
+    delta = sdp.adjoint_trace(P, W)
+    tau = sdp.adjoint_trace(P, W @ dZ1 @ dX1)
+    O2 = mu * delta - tau
+    dy2 = np.linalg.solve(G, O2)
+    dZ2 = sdp.apply_vmap(P, dy2)
+    dX2 = _sym(mu * W - W @ dZ1 @ dX1 - W @ dZ2 @ X)
+    dX, dZ, dy = dX1 + dX2, dZ1 + dZ2, dy1 + dy2
+    tp = step_length(X, dX)
+    td = step_length(Z, dZ)
+    X = X + tp * dX
+    Z = Z + td * dZ
+    y = y + td * dy
+    mu_new = barrier(P, Z, X)
+    phi = float(sum(np.trace(C[b] @ X[b]) for b in range(P.nblocks)))
+    psi = float(y.sum())
+    stats = dict(gap=abs(phi - psi), mu=mu_new, tp=tp, td=td, phi=phi, psi=psi,
+                 dy1=dy1, dy2=dy2, dX1=dX1, dZ1=dZ1, dX2=dX2, dZ2=dZ2, G=G, O1=O1, O2=O2, Rd=Rd, W=W)
+    return X, Z, y, stats

@@ -54,6 +54,19 @@ __global__ void k_pad_copy(double* __restrict__ arena, int64_t ms, int np, int n
   }
 }
 
+// dst_i = w_i * src_i on arena matrices (pre-scaled P-block copies beta_hj X_j, beta_hj W_j).
+__global__ void k_scale_copy(double* __restrict__ arena, int64_t ms, const int32_t* __restrict__ dst,
+                             const int32_t* __restrict__ src, const double* __restrict__ w) {
+  const int e = blockIdx.x;
+  const double2* s = reinterpret_cast<const double2*>(arena + (int64_t)src[e] * ms);
+  double2* d = reinterpret_cast<double2*>(arena + (int64_t)dst[e] * ms);
+  const double we = w[e];
+  for (int64_t i = threadIdx.x; i < ms / 2; i += blockDim.x) {
+    double2 v = s[i];
+    d[i] = make_double2(we * v.x, we * v.y);
+  }
+}
+
 // Batched GEMM on np x np arena matrices; CTA = one 32x32 tile of one output matrix, 4 warps,
 // each warp a 16x16 block = 2x2 DMMA m8n8 tiles.  K is staged 8 at a time through shared memory
 // in k-major layout (row stride 40 doubles: conflict-free fragment reads).
@@ -205,6 +218,13 @@ cudaError_t launch_setup_H(Ctx& c, cudaStream_t s) {
 cudaError_t launch_pad_copy(Ctx& c, const double* src, int64_t id0, int64_t count, int sym, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
   k_pad_copy<<<(unsigned)count, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, src, id0, sym);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_copy(Ctx& c, cudaStream_t s) {
+  if (c.n_sc == 0) return cudaSuccess;
+  k_scale_copy<<<(unsigned)c.n_sc, 256, 0, s>>>(c.arena, c.mstride, c.d_sc_dst, c.d_sc_src, c.d_sc_w);
   ++c.launches;
   return cudaGetLastError();
 }

@@ -123,6 +123,7 @@ void build(Ctx& c, const double* A_host) {
   c.r = c.np / kChunk;
   c.ncls = c.r * (c.r + 1) / 2;
   c.mstride = mul_chk(c.np, c.np);
+  if (c.mstride >= (int64_t)1 << 31) throw Fail{POLYA_EOVERFLOW, "n too large for 32-bit tile offsets"};
   const int64_t l = c.l;
 
   enumerate(l, g.dp, c.Wp);
@@ -148,6 +149,17 @@ void build(Ctx& c, const double* A_host) {
     }
     c.c[j] = g.delta * (double)multinomial((int64_t)g.dp + g.d1, gj, l);
   }
+  // nonzero beta entries (h, j) -> e (h-major): slots of the pre-scaled copies beta_hj X_j, beta_hj W_j
+  std::vector<int32_t> bidx(c.L0 * c.L, -1);
+  std::vector<int32_t> be_src;
+  std::vector<double> be_w;
+  for (int64_t h = 0; h < c.L0; ++h)
+    for (int64_t j = 0; j < c.L; ++j)
+      if (c.beta[h * c.L + j]) {
+        bidx[h * c.L + j] = (int32_t)be_src.size();
+        be_src.push_back((int32_t)j);
+        be_w.push_back((double)c.beta[h * c.L + j]);
+      }
   // nonzero H entries (h, m), m-major, with their integer weights per lambda
   c.Hidx.assign(c.L0 * c.M, -1);
   c.Hh.clear(); c.Hm.clear(); c.Hw.clear();
@@ -174,19 +186,21 @@ void build(Ctx& c, const double* A_host) {
   // ---- pairs (h <= h'), their k-entries, work items, rank partition ---------------------------
   c.npairs = c.L0 * (c.L0 + 1) / 2;
   std::vector<int32_t> ph(c.npairs), ph2(c.npairs);
-  std::vector<int64_t> pK(c.npairs), pItems(c.npairs);
+  std::vector<int64_t> pK(c.npairs), pKpad(c.npairs), pItems(c.npairs), pMu(c.npairs);
   {
     int64_t p = 0;
     for (int64_t h = 0; h < c.L0; ++h)
       for (int64_t h2 = h; h2 < c.L0; ++h2, ++p) {
         ph[p] = (int32_t)h;
         ph2[p] = (int32_t)h2;
-        int64_t kp = 0;
+        int64_t mu = 0, nu = 0;
         for (int64_t m = 0; m < c.M; ++m)
-          if (c.Hidx[h * c.M + m] >= 0 && c.Hidx[h2 * c.M + m] >= 0) kp += 4;
+          if (c.Hidx[h * c.M + m] >= 0 && c.Hidx[h2 * c.M + m] >= 0) ++mu;
         for (int64_t j = 0; j < c.L; ++j)
-          if (c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) kp += 1;
-        pK[p] = kp;
+          if (c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) ++nu;
+        pMu[p] = mu;
+        pK[p] = 4 * mu + nu;                        // K_pair = 4 mu_hh' + nu_hh' (algorithmic)
+        pKpad[p] = (pK[p] + kKStage - 1) / kKStage * kKStage;  // zero-padded to whole stages
         pItems[p] = (h == h2) ? c.ncls * (c.ncls + 1) / 2 : c.ncls * c.ncls;
       }
   }
@@ -196,7 +210,7 @@ void build(Ctx& c, const double* A_host) {
   c.useful_flops_total = 0;
   for (int64_t p = 0; p < c.npairs; ++p) {
     c.pair_item_global[p + 1] = add_chk(c.pair_item_global[p], pItems[p]);
-    cost_prefix[p + 1] = cost_prefix[p] + (double)pItems[p] * (double)std::max<int64_t>(pK[p], 1);
+    cost_prefix[p + 1] = cost_prefix[p] + (double)pItems[p] * (double)std::max<int64_t>(pKpad[p], 1);
     c.useful_flops_total += (ph[p] == ph2[p] ? 1.0 : 2.0) * n4 * (double)pK[p];
   }
   c.items_total = c.pair_item_global[c.npairs];
@@ -204,7 +218,7 @@ void build(Ctx& c, const double* A_host) {
     if (target <= 0) return 0;
     if (target >= cost_prefix[c.npairs]) return c.items_total;
     int64_t p = std::upper_bound(cost_prefix.begin(), cost_prefix.end(), target) - cost_prefix.begin() - 1;
-    double per = (double)std::max<int64_t>(pK[p], 1);
+    double per = (double)std::max<int64_t>(pKpad[p], 1);
     int64_t within = (int64_t)std::ceil((target - cost_prefix[p]) / per);
     return std::min(c.pair_item_global[p] + within, c.pair_item_global[p + 1]);
   };
@@ -230,12 +244,7 @@ void build(Ctx& c, const double* A_host) {
   // ---- arena layout --------------------------------------------------------------------------
   // Q, R: one per (local pair, Lyapunov block active for both rows)
   int64_t nQR = 0;
-  for (int64_t p = c.pair0; p < c.pair1; ++p) nQR += (pK[p] - [&] {
-      int64_t v = 0;
-      for (int64_t j = 0; j < c.L; ++j)
-        if (c.beta[ph[p] * c.L + j] && c.beta[ph2[p] * c.L + j]) ++v;
-      return v;
-    }()) / 4;
+  for (int64_t p = c.pair0; p < c.pair1; ++p) nQR += pMu[p];
   c.nQR = nQR;
   int64_t id = 0;
   c.id_X = id; id += c.nb;
@@ -243,6 +252,11 @@ void build(Ctx& c, const double* A_host) {
   c.id_H = id; id += nnzH;
   c.id_U = id; id += nnzH;
   c.id_V = id; id += nnzH;
+  c.id_Ut = id; id += nnzH;
+  c.id_Vt = id; id += nnzH;
+  c.id_Zero = id; id += 1;
+  c.id_Xb = id; id += c.nnz_beta;
+  c.id_Wb = id; id += c.nnz_beta;
   c.id_Q = id; id += nQR;
   c.id_R = id; id += nQR;
   c.id_Xt = id; id += c.nb;
@@ -254,17 +268,35 @@ void build(Ctx& c, const double* A_host) {
   c.arena = dalloc<double>(mul_chk(c.nmats, c.mstride));
   CU(cudaMemset(c.arena, 0, (size_t)c.nmats * c.mstride * sizeof(double)));
 
+  // ---- pre-scaled P-block copies beta_hj X_j, beta_hj W_j (kernel scale_copy) -----------------
+  {
+    std::vector<int32_t> dst, src;
+    std::vector<double> w;
+    for (size_t e = 0; e < be_src.size(); ++e) {
+      dst.push_back((int32_t)(c.id_Xb + e)); src.push_back((int32_t)(c.id_X + be_src[e])); w.push_back(be_w[e]);
+      dst.push_back((int32_t)(c.id_Wb + e)); src.push_back((int32_t)(c.id_W + be_src[e])); w.push_back(be_w[e]);
+    }
+    c.n_sc = (int64_t)dst.size();
+    c.d_sc_dst = dupload(dst);
+    c.d_sc_src = dupload(src);
+    c.d_sc_w = dupload(w);
+  }
+
   // ---- batched GEMM descriptors ---------------------------------------------------------------
   {
     std::vector<GemmItem> it;
     std::vector<GemmTerm> tm;
-    // U_t = H_t X_{L+m}, V_t = H_t W_{L+m}     (a7: SCM precompute)
+    // U_t = H_t X_{L+m}, V_t = H_t W_{L+m}, and their transposes X H_t^T, W H_t^T   (a7)
     for (int64_t t = 0; t < nnzH; ++t) {
       int32_t b = (int32_t)(c.L + c.Hm[t]);
       it.push_back({(int32_t)(c.id_U + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
       tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_X + b), 0, 0, 1.0});
       it.push_back({(int32_t)(c.id_V + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
       tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_W + b), 0, 0, 1.0});
+      it.push_back({(int32_t)(c.id_Ut + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      tm.push_back({(int32_t)(c.id_X + b), (int32_t)(c.id_H + t), 1, 0, 1.0});
+      it.push_back({(int32_t)(c.id_Vt + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      tm.push_back({(int32_t)(c.id_W + b), (int32_t)(c.id_H + t), 1, 0, 1.0});
     }
     c.n_items_UV = (int64_t)it.size();
     c.d_items_UV = dupload(it);
@@ -320,7 +352,7 @@ void build(Ctx& c, const double* A_host) {
         ++q;
         // T1 = U_{h'}^T[b1,c1] V_h^T[d1,a1]; T2 = X[b1,c1] R_{h'h}[d1,a1];
         // T3 = Q_{hh'}[b1,c1] W[d1,a1];     T4 = U_h[b1,c1] V_{h'}[d1,a1]   (O7)
-        kL.push_back((int32_t)(c.id_U + th2)); kR.push_back((int32_t)(c.id_V + th)); kf.push_back(3); ks.push_back(1.0);
+        kL.push_back((int32_t)(c.id_Ut + th2)); kR.push_back((int32_t)(c.id_Vt + th)); kf.push_back(0); ks.push_back(1.0);
         kL.push_back((int32_t)(c.id_X + b));   kR.push_back(idR);                     kf.push_back(0); ks.push_back(1.0);
         kL.push_back(idQ);                     kR.push_back((int32_t)(c.id_W + b));   kf.push_back(0); ks.push_back(1.0);
         kL.push_back((int32_t)(c.id_U + th));  kR.push_back((int32_t)(c.id_V + th2)); kf.push_back(0); ks.push_back(1.0);
@@ -328,8 +360,12 @@ void build(Ctx& c, const double* A_host) {
       for (int64_t j = 0; j < c.L; ++j) {
         int64_t b1 = c.beta[h * c.L + j], b2 = c.beta[h2 * c.L + j];
         if (!b1 || !b2) continue;
-        kL.push_back((int32_t)(c.id_X + j)); kR.push_back((int32_t)(c.id_W + j)); kf.push_back(0);
-        ks.push_back((double)b1 * (double)b2);
+        // P-block term beta_hj beta_h'j X_j (x) W_j as (beta_hj X_j) (x) (beta_h'j W_j)
+        kL.push_back((int32_t)(c.id_Xb + bidx[h * c.L + j])); kR.push_back((int32_t)(c.id_Wb + bidx[h2 * c.L + j]));
+        kf.push_back(0); ks.push_back(1.0);
+      }
+      while ((int64_t)(kL.size() - kbeg.back()) % kKStage) {  // zero terms up to a whole stage
+        kL.push_back((int32_t)c.id_Zero); kR.push_back((int32_t)c.id_Zero); kf.push_back(0); ks.push_back(0.0);
       }
       kbeg.push_back((int64_t)kL.size());
       pitem.push_back(c.pair_item_global[p + 1]);
@@ -346,6 +382,11 @@ void build(Ctx& c, const double* A_host) {
     c.st.k_R = dupload(kR);
     c.st.k_flags = dupload(kf);
     c.st.k_scale = dupload(ks);
+    {
+      std::vector<int2> kd(kL.size());
+      for (size_t i = 0; i < kL.size(); ++i) kd[i] = make_int2(kL[i], kR[i]);
+      c.st.kdesc = dupload(kd);
+    }
     std::vector<int32_t> ca, cb;
     for (int64_t i = 0; i < c.r; ++i)
       for (int64_t j = i; j < c.r; ++j) { ca.push_back((int32_t)i); cb.push_back((int32_t)j); }
@@ -386,9 +427,9 @@ void build(Ctx& c, const double* A_host) {
 
 void free_ctx(Ctx& c) {
   void* ps[] = {c.arena, c.dA, c.dHw, c.dHm, c.dHgam, c.d_items_UV, c.d_terms_UV, c.d_items_QR, c.d_terms_QR,
-                c.d_items_T, c.d_terms_T, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
+                c.d_items_T, c.d_terms_T, c.d_sc_dst, c.d_sc_src, c.d_sc_w, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
-                c.st.pair_kbeg, c.st.pair_item, c.st.k_L, c.st.k_R, c.st.k_flags, c.st.k_scale,
+                c.st.pair_kbeg, c.st.pair_item, c.st.k_L, c.st.k_R, c.st.k_flags, c.st.k_scale, c.st.kdesc,
                 c.st.cls_a, c.st.cls_b, c.st.counter};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -522,6 +563,7 @@ extern "C" polya_status polya_schur(polya_ctx* ctx, const double* X, const doubl
     if (c.timing) CU(cudaEventRecord(c.ev[0], s));
     CU(launch_pad_copy(c, X, c.id_X, c.nb, 0, s));
     CU(launch_pad_copy(c, Zinv, c.id_W, c.nb, 0, s));
+    CU(launch_scale_copy(c, s));
     CU(launch_gemm(c, c.d_items_UV, c.d_terms_UV, c.n_items_UV, s));
     CU(launch_gemm(c, c.d_items_QR, c.d_terms_QR, c.n_items_QR, s));
     if (c.timing) CU(cudaEventRecord(c.ev[1], s));

@@ -12,6 +12,7 @@
 namespace polya {
 
 constexpr int kChunk = 8;  // index chunk q of the Schur "class blocks" (kernel K4)
+constexpr int kKStage = 8;  // k terms per K4 pipeline stage; pair k-lists are zero-padded to it
 
 // One term of a batched GEMM item: C += alpha * A[a_id] * op(B[b_id]), all np x np arena matrices.
 struct GemmTerm {
@@ -35,6 +36,7 @@ struct SchurTables {
   int32_t* k_R = nullptr;         // [nk] arena id of the right factor R_k
   int32_t* k_flags = nullptr;     // [nk] bit0: L transposed, bit1: R transposed
   double* k_scale = nullptr;      // [nk] scale of L_k (beta_h beta_h' on P-block terms, else 1)
+  int2* kdesc = nullptr;          // [nk] arena matrix ids (L_k, R_k) for K4
   int32_t* cls_a = nullptr;       // [ncls] chunk index i of class (i <= j)
   int32_t* cls_b = nullptr;       // [ncls] chunk index j
   unsigned long long* counter = nullptr;  // dynamic work counter
@@ -60,6 +62,8 @@ struct Ctx {
   double useful_flops_total = 0, useful_flops_rank = 0;
   // arena (np x np matrices)
   int64_t mstride = 0, nmats = 0;
+  int64_t id_Ut = 0, id_Vt = 0, id_Zero = 0, id_Xb = 0, id_Wb = 0;
+  int32_t* d_sc_dst = nullptr; int32_t* d_sc_src = nullptr; double* d_sc_w = nullptr; int64_t n_sc = 0;
   int64_t id_X = 0, id_W = 0, id_H = 0, id_U = 0, id_V = 0, id_Q = 0, id_R = 0, id_Xt = 0, id_T = 0,
           id_Vy = 0, id_S = 0;
   int64_t nQR = 0;
@@ -98,6 +102,7 @@ struct Ctx {
 cudaError_t launch_setup_H(Ctx& c, cudaStream_t s);
 cudaError_t launch_pad_copy(Ctx& c, const double* src, int64_t id0, int64_t count, int symmetrize,
                             cudaStream_t s);
+cudaError_t launch_scale_copy(Ctx& c, cudaStream_t s);
 cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, int64_t nitems,
                         cudaStream_t s);
 cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
