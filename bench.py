@@ -281,6 +281,30 @@ def run_gpu(args, cfg, cid):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
         del Gh
 
+    # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step; N=1 only) ----
+    ipm = None
+    if world == 1 and not args.no_ipm and ctx.K * ctx.K * 8 < 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+        del G
+        torch.cuda.empty_cache()
+        Xi = torch.eye(cfg.n, dtype=torch.float64, device=dev).repeat(ctx.nblocks, 1, 1).contiguous()
+        Zi = Xi.clone()
+        yi = torch.zeros(K, dtype=torch.float64, device=dev)
+        mu = float(ctx.nblocks * cfg.n) / (3.0 * ctx.nblocks * cfg.n)   # reading R4 at X = Z = I
+        runs = []
+        for it in range(2):                                            # the first call allocates G
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = ctx.ipm_step(Xi, Zi, yi, mu, it)
+            e1.record()
+            e1.synchronize()
+            mu = st["mu"]
+            runs.append((e0.elapsed_time(e1), st))
+        ms, st = runs[-1]
+        ipm = {"s_per_iteration": ms / 1e3, "ms_schur": st["ms_schur"], "ms_factorisation": st["ms_factor"],
+               "ms_other": st["ms_other"], "factorisation": "cuSOLVER dpotrf + 2 dpotrs on the K x K SCM (FULL)",
+               "iteration_measured": 2, "gap": st["gap"], "tp": st["tp"], "td": st["td"]}
+
     # ---- CPU oracle baseline (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -321,6 +345,7 @@ def run_gpu(args, cfg, cid):
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "gpu_launches_per_step": launches_per_step,
             "clocks": clocks,
+            "ipm_iteration": ipm,
         }
         print(json.dumps(line), flush=True)
     barrier()
@@ -338,6 +363,7 @@ def main():
     ap.add_argument("--config", default="4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ipm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

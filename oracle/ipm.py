@@ -26,11 +26,14 @@ few steps" (reading R15: the IPM's certificate is not unique).
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from . import sdp
+from .monomials import enumerate_W
 
-__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks"]
+__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "grid_check"]
 
 
 def C_blocks(P):
@@ -103,3 +106,20 @@ def ipm_step(P, X, Z, y, mu):
     stats = dict(gap=abs(phi - psi), mu=mu_new, tp=tp, td=td, phi=phi, psi=psi,
                  dy1=dy1, dy2=dy2, dX1=dX1, dZ1=dZ1, dX2=dX2, dZ2=dZ2, G=G, O1=O1, O2=O2, Rd=Rd, W=W)
     return X, Z, y, stats
+
+
+def grid_check(P, y, samples=1000, seed=0):
+    """O8 verdict check: P(alpha) = sum_h V_h(y) alpha^h (R7) at vertices, edge midpoints and
+    Dirichlet(1) samples: lambda_min P > 0 and lambda_max(A^T P + P A) < 0 (Theorem 1)."""
+    Wp = enumerate_W(P.l, P.dp)
+    Ph = [sdp.vmap(P, y, h) for h in range(P.L0)]
+    rng = np.random.default_rng(seed)
+    pts = [np.eye(P.l)[i] for i in range(P.l)]
+    pts += [0.5 * (np.eye(P.l)[i] + np.eye(P.l)[j]) for i in range(P.l) for j in range(i + 1, P.l)]
+    pts += list(rng.dirichlet(np.ones(P.l), size=samples))
+    for al in pts:
+        Pa = sum(math.prod(a ** e for a, e in zip(al, h)) * Ph[i] for i, h in enumerate(Wp))
+        Aa = sum(al[i] * P.A[i] for i in range(P.l))
+        if np.linalg.eigvalsh(Pa).min() <= 0 or np.linalg.eigvalsh(Aa.T @ Pa + Pa @ Aa).max() >= 0:
+            return False
+    return True

@@ -24,7 +24,7 @@ import numpy as np
 from .monomials import enumerate_W, index_map
 
 __all__ = ["poly_mul", "simplex_power", "beta_table", "H_table", "beta_recursion",
-           "H_recursion", "C_scalars", "counts"]
+           "H_recursion", "C_scalars", "counts", "H_row"]
 
 
 def poly_mul(p: dict, q: dict) -> dict:
@@ -141,3 +141,17 @@ def C_scalars(beta: np.ndarray, l: int, dp: int, delta: float) -> np.ndarray:
     Wp = enumerate_W(l, dp)
     w = np.array([math.factorial(dp) // math.prod(math.factorial(x) for x in h) for h in Wp], dtype=np.int64)
     return delta * (w @ beta).astype(np.float64)
+
+
+def H_row(A: np.ndarray, l: int, dp: int, d2: int, h_index: int, da: int = 1) -> np.ndarray:
+    """One row h of ``H_table`` (M x n x n), same polynomial multiplication, for large configs."""
+    Wp = enumerate_W(l, dp)
+    Wa = enumerate_W(l, da)
+    idx = index_map(l, dp + da + d2)
+    n = A.shape[-1]
+    Apoly = {lam: A[i] for i, lam in enumerate(Wa)}
+    prod = poly_mul(simplex_power(l, d2), poly_mul({Wp[h_index]: 1}, Apoly))
+    out = np.zeros((len(idx), n, n))
+    for e, c in prod.items():
+        out[idx[e]] += c
+    return out

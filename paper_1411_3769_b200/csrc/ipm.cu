@@ -1,11 +1,482 @@
-// ipm.cu -- polya_ipm_step: one predictor-corrector iteration of Algorithm 2.
+// ipm.cu -- polya_ipm_step: one predictor-corrector iteration of Algorithm 2
+// with the readings R3-R6 of DESIGN.md, on one GPU.  Every iterate is a block stack
+// double[nblocks][n][n] (Theorem 3: the iteration never leaves S_{L,M,n}).
+//
+//   W   = Z^-1 (blockwise Cholesky inverse)                 kernel k_block_inv
+//   Rd  = -B^T(y) + Z + C                                   (Eq. G; polya_apply + k_axpby)
+//   O1  = B(W Rd X) - 1                                     (Processors step 1, Eq. T1)
+//   G   = SCM (polya_schur, POLYA_G_FULL)                   (Eq. T2)
+//   potrf(G); dy^ = G^-1 O1                                 (Root step 1, Eq. SAE1; cuSOLVER)
+//   dZ^ = -Rd + B^T(dy^);  dX^ = sym(-X + W (Rd - B^T(dy^)) X)          (R3)
+//   O2  = mu B(W) - B(W dZ^ dX^);  dy- = G^-1 O2            (Processors/Root step 2, Eq. SAE2)
+//   dZ- = B^T(dy-);  dX- = sym(mu W - W dZ^ dX^ - W dZ- X)  (Processors step 3)
+//   t_p, t_d = min(1, 0.98 t_max), t_max by per-block bisection on positive definiteness (R5)
+//   X += t_p dX, Z += t_d dZ, y += t_d dy                   (Eqs. 33-35, R6)
+//   mu = tr(ZX) / (3 (L+M) n) (R4), phi = tr(CX), psi = sum y, gap = |phi - psi|   (Step 4)
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
 #include "polya_internal.h"
 
-void polya_ipm_free(polya::Ctx& c) { (void)c; }
+namespace polya {
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// C_b = alpha op(A_b) op(B_b) + beta C_b for every block b of n x n stacks (any n; guarded loads).
+// CTA = 32x32 tile of one block, 4 warps of 2x2 DMMA m8n8 tiles, K staged 8 at a time.
+__global__ void __launch_bounds__(128) k_bgemm(int n, const double* __restrict__ A, int ta,
+                                               const double* __restrict__ B, int tb, double* __restrict__ C,
+                                               double alpha, double beta, int tiles) {
+  __shared__ double As[8][40];
+  __shared__ double Bs[8][40];
+  const int64_t nn = (int64_t)n * n, b = blockIdx.y;
+  const double* Ab = A + b * nn;
+  const double* Bb = B + b * nn;
+  double* Cb = C + b * nn;
+  const int ti = blockIdx.x / tiles, tj = blockIdx.x - ti * tiles, i0 = ti * 32, j0 = tj * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 16;
+  double acc[2][2][2] = {};
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    for (int e = tid; e < 256; e += 128) {
+      const int r = e >> 3, k = e & 7;  // A tile: rows i0+r, k0+k
+      const int gi = i0 + r, gk = k0 + k;
+      As[k][r] = (gi < n && gk < n) ? (ta ? Ab[(int64_t)gk * n + gi] : Ab[(int64_t)gi * n + gk]) : 0.0;
+      const int gj = j0 + r;             // B tile: k0+k, cols j0+r
+      Bs[k][r] = (gj < n && gk < n) ? (tb ? Bb[(int64_t)gj * n + gk] : Bb[(int64_t)gk * n + gj]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      double a[2], bb[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) a[mi] = As[ks * 4 + t][wr + mi * 8 + g];
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) bb[nj] = Bs[ks * 4 + t][wc + nj * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], a[mi], bb[nj]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + wr + mi * 8 + g, j = j0 + wc + nj * 8 + 2 * t + e;
+        if (i < n && j < n) {
+          const int64_t o = (int64_t)i * n + j;
+          Cb[o] = alpha * acc[mi][nj][e] + (beta != 0.0 ? beta * Cb[o] : 0.0);
+        }
+      }
+}
+
+// out = a X + b Y (+ c * C_b on the P-blocks' diagonals when cdiag != nullptr), elementwise
+__global__ void k_axpby(int64_t total, int n, int64_t Lp, double a, const double* __restrict__ X, double b,
+                        const double* __restrict__ Y, double* __restrict__ out, const double* __restrict__ cdiag,
+                        double cs) {
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    double v = a * X[e] + (Y ? b * Y[e] : 0.0);
+    if (cdiag) {
+      const int64_t blk = e / nn, r = e - blk * nn;
+      if (blk < Lp && (r / n) == (r % n)) v += cs * cdiag[blk];
+    }
+    out[e] = v;
+  }
+}
+
+// out_b = (M_b + M_b^T) / 2
+__global__ void k_sym(int n, const double* __restrict__ M, double* __restrict__ out) {
+  const int64_t nn = (int64_t)n * n, b = blockIdx.x;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    if (i <= j) {
+      const double v = 0.5 * (M[b * nn + (int64_t)i * n + j] + M[b * nn + (int64_t)j * n + i]);
+      out[b * nn + (int64_t)i * n + j] = v;
+      out[b * nn + (int64_t)j * n + i] = v;
+    }
+  }
+}
+
+// In-shared-memory Cholesky of the n x n matrix S (row-major, lower factor in place).
+// Returns false (uniformly) if a pivot is not positive.
+__device__ bool smem_chol(double* S, int n) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (threadIdx.x == 0) {
+      const double d = S[k * n + k];
+      if (!(d > 0.0)) s_ok = 0;
+      S[k * n + k] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    if (!s_ok) return false;
+    const double dk = S[k * n + k];
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) S[i * n + k] /= dk;
+    __syncthreads();
+    for (int e = threadIdx.x; e < (n - k - 1) * (n - k - 1); e += blockDim.x) {
+      const int i = k + 1 + e / (n - k - 1), j = k + 1 + e % (n - k - 1);
+      if (j <= i) S[i * n + j] -= S[i * n + k] * S[j * n + k];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// W_b = Z_b^{-1} via Cholesky: L^{-1} by columns, then W = L^{-T} L^{-1}; exactly symmetric.
+__global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restrict__ W, int* __restrict__ fail) {
+  extern __shared__ double sm[];
+  double* S = sm;           // n*n: Cholesky factor
+  double* Li = sm + n * n;  // n*n: L^{-1} (lower)
+  const int64_t nn = (int64_t)n * n, b = blockIdx.x;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[e] = Z[b * nn + e];
+  __syncthreads();
+  if (!smem_chol(S, n)) {
+    if (threadIdx.x == 0) atomicExch(fail, 1);
+    return;
+  }
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {  // column j of L^{-1}
+    for (int i = 0; i < n; ++i) {
+      if (i < j) { Li[i * n + j] = 0.0; continue; }
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s -= S[i * n + k] * Li[k * n + j];
+      Li[i * n + j] = s / S[i * n + i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    if (i > j) continue;
+    double s = 0.0;
+    for (int k = j; k < n; ++k) s += Li[k * n + i] * Li[k * n + j];  // (L^-T L^-1)_{ij}, k >= max(i,j)
+    W[b * nn + (int64_t)i * n + j] = s;
+    W[b * nn + (int64_t)j * n + i] = s;
+  }
+}
+
+// Reading R5: t_b = sup{t in [0, tcap] : S_b + t dS_b positive definite}, by bisection on the
+// Cholesky test (60 halvings); t_b = tcap if S_b + tcap dS_b is positive definite.
+__global__ void k_block_tmax(int n, const double* __restrict__ S, const double* __restrict__ dS, double tcap,
+                             double* __restrict__ tout) {
+  extern __shared__ double sm[];
+  const int64_t nn = (int64_t)n * n, b = blockIdx.x;
+  auto pd = [&](double tt) -> bool {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sm[e] = S[b * nn + e] + tt * dS[b * nn + e];
+    __syncthreads();
+    const bool ok = smem_chol(sm, n);
+    __syncthreads();
+    return ok;
+  };
+  double lo = 0.0, hi = tcap;
+  if (pd(hi)) {
+    lo = hi;
+  } else {
+    for (int it = 0; it < 60; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (pd(mid)) lo = mid; else hi = mid;
+    }
+  }
+  if (threadIdx.x == 0) tout[b] = lo;
+}
+
+// partial sums: out[0] = sum_b tr(Z_b X_b) = sum Z.*X^T, out[1] = sum_{j<L} c_j tr(X_j), out[2] = sum y
+__global__ void k_scalars(int64_t total, int n, int64_t Lp, const double* __restrict__ Z, const double* __restrict__ X,
+                          const double* __restrict__ c, const double* __restrict__ y, int64_t K,
+                          double* __restrict__ part) {
+  __shared__ double red[3][256];
+  const int64_t nn = (int64_t)n * n;
+  double s0 = 0, s1 = 0, s2 = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = e / nn, r = e - blk * nn;
+    const int i = (int)(r / n), j = (int)(r % n);
+    s0 += Z[e] * X[blk * nn + (int64_t)j * n + i];
+    if (blk < Lp && i == j) s1 += c[blk] * X[e];
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x) s2 += y[e];
+  red[0][threadIdx.x] = s0; red[1][threadIdx.x] = s1; red[2][threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      for (int q = 0; q < 3; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) part[blockIdx.x * 3 + q] = red[q][0];
+}
+
+__global__ void k_vec_axpby(int64_t K, double a, const double* __restrict__ x, double b, const double* __restrict__ y,
+                            double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = a * x[e] + (y ? b * y[e] : 0.0);
+}
+
+__global__ void k_vec_shift(int64_t K, double cst, double* __restrict__ x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x)
+    x[e] += cst;
+}
+
+struct Ipm {
+  int64_t nb = 0, n = 0, K = 0;
+  double *W = nullptr, *Rd = nullptr, *T1 = nullptr, *T2 = nullptr, *dX1 = nullptr, *dZ1 = nullptr, *dX2 = nullptr,
+         *dZ2 = nullptr, *G = nullptr, *O1 = nullptr, *O2 = nullptr, *dy1 = nullptr, *dy2 = nullptr, *tmpK = nullptr,
+         *tb = nullptr, *part = nullptr, *dc = nullptr, *work = nullptr;
+  int* info = nullptr;
+  int* fail = nullptr;
+  int lwork = 0;
+  cusolverDnHandle_t sol = nullptr;
+  cudaEvent_t ev[6] = {};
+};
+
+constexpr int kScalarBlocks = 256;
+
+}  // namespace
+}  // namespace polya
+
+using namespace polya;
+
+void polya_ipm_free(polya::Ctx& c) {
+  Ipm* w = (Ipm*)c.ipm;
+  if (!w) return;
+  double* ps[] = {w->W, w->Rd, w->T1, w->T2, w->dX1, w->dZ1, w->dX2, w->dZ2, w->G, w->O1, w->O2,
+                  w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work};
+  for (double* p : ps)
+    if (p) cudaFree(p);
+  if (w->info) cudaFree(w->info);
+  if (w->fail) cudaFree(w->fail);
+  if (w->sol) cusolverDnDestroy(w->sol);
+  for (auto& e : w->ev)
+    if (e) cudaEventDestroy(e);
+  delete w;
+  c.ipm = nullptr;
+}
+
+namespace {
+
+struct IpmFail {
+  polya_status s;
+  std::string msg;
+};
+#define CK(x)                                                                                      \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess) throw IpmFail{e_ == cudaErrorMemoryAllocation ? POLYA_ENOMEM : POLYA_ECUDA, \
+                                         std::string(#x) + ": " + cudaGetErrorString(e_)};         \
+  } while (0)
+#define CS(x)                                                                                      \
+  do {                                                                                             \
+    cusolverStatus_t e_ = (x);                                                                     \
+    if (e_ != CUSOLVER_STATUS_SUCCESS) throw IpmFail{POLYA_ECUDA, std::string(#x) + " failed"};    \
+  } while (0)
+
+Ipm* ipm_ws(Ctx& c) {
+  if (c.ipm) return (Ipm*)c.ipm;
+  Ipm* w = new Ipm();
+  c.ipm = w;
+  w->nb = c.nb; w->n = c.n; w->K = c.K;
+  const size_t st = (size_t)c.nb * c.n * c.n * sizeof(double), kv = (size_t)c.K * sizeof(double);
+  double** stacks[] = {&w->W, &w->Rd, &w->T1, &w->T2, &w->dX1, &w->dZ1, &w->dX2, &w->dZ2};
+  for (double** p : stacks) CK(cudaMalloc(p, st));
+  double** vecs[] = {&w->O1, &w->O2, &w->dy1, &w->dy2, &w->tmpK};
+  for (double** p : vecs) CK(cudaMalloc(p, kv));
+  CK(cudaMalloc(&w->G, (size_t)c.K * c.K * sizeof(double)));
+  CK(cudaMalloc(&w->tb, (size_t)c.nb * sizeof(double)));
+  CK(cudaMalloc(&w->part, (size_t)kScalarBlocks * 3 * sizeof(double)));
+  CK(cudaMalloc(&w->dc, (size_t)std::max<int64_t>(c.L, 1) * sizeof(double)));
+  CK(cudaMemcpy(w->dc, c.c.data(), (size_t)c.L * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&w->info, sizeof(int)));
+  CK(cudaMalloc(&w->fail, sizeof(int)));
+  CS(cusolverDnCreate(&w->sol));
+  CS(cusolverDnDpotrf_bufferSize(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, &w->lwork));
+  CK(cudaMalloc(&w->work, (size_t)std::max(w->lwork, 1) * sizeof(double)));
+  for (auto& e : w->ev) CK(cudaEventCreate(&e));
+  return w;
+}
+
+void bgemm(Ctx& c, const double* A, int ta, const double* B, int tb, double* C, double alpha, double beta,
+           cudaStream_t s) {
+  const int tiles = (int)((c.n + 31) / 32);
+  dim3 grid((unsigned)(tiles * tiles), (unsigned)c.nb);
+  k_bgemm<<<grid, 128, 0, s>>>((int)c.n, A, ta, B, tb, C, alpha, beta, tiles);
+  ++c.launches;
+  CK(cudaGetLastError());
+}
+
+void axpby(Ctx& c, double a, const double* X, double b, const double* Y, double* out, const double* cdiag, double cs,
+           cudaStream_t s) {
+  const int64_t total = c.nb * c.n * c.n;
+  k_axpby<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(total, (int)c.n, c.L, a, X, b, Y, out,
+                                                                                 cdiag, cs);
+  ++c.launches;
+  CK(cudaGetLastError());
+}
+
+void sym(Ctx& c, const double* M, double* out, cudaStream_t s) {
+  k_sym<<<(unsigned)c.nb, 256, 0, s>>>((int)c.n, M, out);
+  ++c.launches;
+  CK(cudaGetLastError());
+}
+
+void vaxpby(Ctx& c, double a, const double* x, double b, const double* y, double* out, cudaStream_t s) {
+  k_vec_axpby<<<(unsigned)std::min<int64_t>((c.K + 255) / 256, 4096), 256, 0, s>>>(c.K, a, x, b, y, out);
+  ++c.launches;
+  CK(cudaGetLastError());
+}
+
+double step_len(Ctx& c, Ipm* w, const double* S, const double* dS, cudaStream_t s) {
+  const double frac = 0.98, tcap = 1.0 / frac;
+  const size_t sm = (size_t)c.n * c.n * sizeof(double);
+  CK(cudaFuncSetAttribute(k_block_tmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_block_tmax<<<(unsigned)c.nb, 256, sm, s>>>((int)c.n, S, dS, tcap, w->tb);
+  ++c.launches;
+  CK(cudaGetLastError());
+  std::vector<double> tb(c.nb);
+  CK(cudaMemcpyAsync(tb.data(), w->tb, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  double t = tcap;
+  for (double v : tb) t = std::min(t, v);
+  return std::min(1.0, frac * t);
+}
+
+polya_status call(polya_status st, Ctx& c) {
+  if (st != POLYA_OK) throw IpmFail{st, c.last_error};
+  return st;
+}
+
+}  // namespace
 
 extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, polya_ipm_stats* stats, void* stream) {
-  (void)st; (void)stats; (void)stream;
-  if (!ctx) return POLYA_EINVAL;
-  ctx->c.last_error = "polya_ipm_step: not built yet";
-  return POLYA_EINVAL;
+  if (!ctx || !st || !st->X || !st->Z || !st->y) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (c.cfg.nranks != 1) {
+    c.last_error = "polya_ipm_step runs on a single rank (distributed factorisation is out of scope)";
+    return POLYA_EINVAL;
+  }
+  if (c.n * c.n * 2 * (int64_t)sizeof(double) > 220 * 1024) {
+    c.last_error = "polya_ipm_step: block too large for the shared-memory Cholesky (n <= 120)";
+    return POLYA_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  double* X = st->X;
+  double* Z = st->Z;
+  double* y = st->y;
+  const double mu = st->mu;
+  try {
+    Ipm* w = ipm_ws(c);
+    CS(cusolverDnSetStream(w->sol, s));
+    CK(cudaEventRecord(w->ev[0], s));
+    // W = Z^-1
+    CK(cudaMemsetAsync(w->fail, 0, sizeof(int), s));
+    {
+      CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * (size_t)c.n * c.n * sizeof(double))));
+      k_block_inv<<<(unsigned)c.nb, 128, 2 * (size_t)c.n * c.n * sizeof(double), s>>>((int)c.n, Z, w->W, w->fail);
+      ++c.launches;
+      CK(cudaGetLastError());
+    }
+    // Rd = -B^T(y) + Z + C
+    call(polya_apply(ctx, y, w->T1, s), c);
+    axpby(c, -1.0, w->T1, 1.0, Z, w->Rd, w->dc, 1.0, s);
+    // O1 = B(W Rd X) - 1
+    bgemm(c, w->Rd, 0, X, 0, w->T2, 1.0, 0.0, s);
+    bgemm(c, w->W, 0, w->T2, 0, w->T1, 1.0, 0.0, s);
+    call(polya_adjoint(ctx, w->T1, w->O1, s), c);
+    k_vec_shift<<<(unsigned)std::min<int64_t>((c.K + 255) / 256, 4096), 256, 0, s>>>(c.K, -1.0, w->O1);  // - a
+    ++c.launches;
+    CK(cudaGetLastError());
+    // G (FULL layout), then its Cholesky factor (timed separately)
+    CK(cudaEventRecord(w->ev[1], s));
+    call(polya_schur(ctx, X, w->W, w->G, POLYA_G_FULL, s), c);
+    CK(cudaEventRecord(w->ev[2], s));
+    CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, w->work, w->lwork, w->info));
+    CK(cudaEventRecord(w->ev[3], s));
+    int hinfo = 0, hfail = 0;
+    CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hfail, w->fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hfail) throw IpmFail{POLYA_ENOTPD, "a Z block is not positive definite"};
+    if (hinfo != 0) throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite (potrf info " + std::to_string(hinfo) + ")"};
+    // dy^ = G^-1 O1
+    CK(cudaMemcpyAsync(w->dy1, w->O1, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy1, (int)c.K, w->info));
+    // dZ^ = -Rd + B^T(dy^);  dX^ = sym(-X + W (Rd - B^T(dy^)) X)
+    call(polya_apply(ctx, w->dy1, w->T1, s), c);
+    axpby(c, -1.0, w->Rd, 1.0, w->T1, w->dZ1, nullptr, 0.0, s);          // dZ^
+    axpby(c, 1.0, w->Rd, -1.0, w->T1, w->T2, nullptr, 0.0, s);           // Rd - B^T(dy^)
+    bgemm(c, w->T2, 0, X, 0, w->T1, 1.0, 0.0, s);                          // (Rd - B^T dy^) X
+    bgemm(c, w->W, 0, w->T1, 0, w->T2, 1.0, 0.0, s);                       // W (...) X
+    axpby(c, -1.0, X, 1.0, w->T2, w->T1, nullptr, 0.0, s);                 // -X + W (...) X
+    sym(c, w->T1, w->dX1, s);
+    // O2 = mu B(W) - B(W dZ^ dX^);  dy- = G^-1 O2
+    bgemm(c, w->dZ1, 0, w->dX1, 0, w->T1, 1.0, 0.0, s);                    // dZ^ dX^
+    bgemm(c, w->W, 0, w->T1, 0, w->T2, 1.0, 0.0, s);                       // W dZ^ dX^  (kept in T2)
+    call(polya_adjoint(ctx, w->W, w->tmpK, s), c);
+    call(polya_adjoint(ctx, w->T2, w->O2, s), c);
+    vaxpby(c, mu, w->tmpK, -1.0, w->O2, w->O2, s);
+    CK(cudaMemcpyAsync(w->dy2, w->O2, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy2, (int)c.K, w->info));
+    // dZ- = B^T(dy-);  dX- = sym(mu W - W dZ^ dX^ - W dZ- X)
+    call(polya_apply(ctx, w->dy2, w->dZ2, s), c);
+    bgemm(c, w->dZ2, 0, X, 0, w->T1, 1.0, 0.0, s);                         // dZ- X
+    bgemm(c, w->W, 0, w->T1, 0, w->T2, -1.0, -1.0, s);                     // T2 = -W dZ^ dX^ - W dZ- X
+    axpby(c, mu, w->W, 1.0, w->T2, w->T1, nullptr, 0.0, s);
+    sym(c, w->T1, w->dX2, s);
+    // totals (into dX1, dZ1, dy1)
+    axpby(c, 1.0, w->dX1, 1.0, w->dX2, w->dX1, nullptr, 0.0, s);
+    axpby(c, 1.0, w->dZ1, 1.0, w->dZ2, w->dZ1, nullptr, 0.0, s);
+    vaxpby(c, 1.0, w->dy1, 1.0, w->dy2, w->dy1, s);
+    // line search (R5) and update (R6)
+    const double tp = step_len(c, w, X, w->dX1, s);
+    const double td = step_len(c, w, Z, w->dZ1, s);
+    if (!(tp > 0.0) || !(td > 0.0)) throw IpmFail{POLYA_ESTEP, "no admissible step"};
+    axpby(c, 1.0, X, tp, w->dX1, X, nullptr, 0.0, s);
+    axpby(c, 1.0, Z, td, w->dZ1, Z, nullptr, 0.0, s);
+    vaxpby(c, 1.0, y, td, w->dy1, y, s);
+    // step 4 scalars
+    const int64_t total = c.nb * c.n * c.n;
+    k_scalars<<<kScalarBlocks, 256, 0, s>>>(total, (int)c.n, c.L, Z, X, w->dc, y, c.K, w->part);
+    ++c.launches;
+    CK(cudaGetLastError());
+    std::vector<double> part(kScalarBlocks * 3);
+    CK(cudaMemcpyAsync(part.data(), w->part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(w->ev[4], s));
+    CK(cudaStreamSynchronize(s));
+    double trzx = 0, phi = 0, psi = 0;
+    for (int b = 0; b < kScalarBlocks; ++b) { trzx += part[b * 3]; phi += part[b * 3 + 1]; psi += part[b * 3 + 2]; }
+    const double mu_new = trzx / (3.0 * (double)c.nb * (double)c.n);
+    st->mu = mu_new;
+    st->iter += 1;
+    if (stats) {
+      stats->gap = std::fabs(phi - psi);
+      stats->mu = mu_new;
+      stats->tp = tp;
+      stats->td = td;
+      stats->phi = phi;
+      stats->psi = psi;
+      float a = 0, b = 0, tot = 0;
+      cudaEventElapsedTime(&a, w->ev[1], w->ev[2]);
+      cudaEventElapsedTime(&b, w->ev[2], w->ev[3]);
+      cudaEventElapsedTime(&tot, w->ev[0], w->ev[4]);
+      stats->ms_schur = a;
+      stats->ms_factor = b;
+      stats->ms_other = tot - a - b;
+    }
+  } catch (const IpmFail& f) {
+    c.last_error = f.msg;
+    return f.s;
+  }
+  return POLYA_OK;
 }
