@@ -166,6 +166,16 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def reduce_over_ranks(x, op, device, world):
+    """Max / sum of a per-rank scalar over the process group (NCCL on GPUs, gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def run_gpu(args, cfg, cid):
     import torch
     import torch.distributed as dist
@@ -186,16 +196,10 @@ def run_gpu(args, cfg, cid):
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(x, "max", dev, world)
 
     def sum_over_ranks(x):
-        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce_over_ranks(x, "sum", dev, world)
 
     L0, L, M = counts(cfg)
     A, X, W = synth.make_case(cfg, L + M, seed=0)

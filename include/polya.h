@@ -107,6 +107,12 @@ polya_status polya_setup(const polya_config* cfg, const double* A_host, polya_ct
 
 polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* out);
 
+/* Host-only planning (no CUDA call, no A needed: the sparsity of beta and H depends
+ * only on the exponents): the dims this rank's polya_setup would report, including
+ * its share [item0, item1) of the Schur work items (cost-balanced prefix split of
+ * K_pair-weighted items across nranks).  Errors as polya_setup. */
+polya_status polya_plan(const polya_config* cfg, polya_dims* out);
+
 /* Exponent table `which` (0: W_dp, 1: W_{dp+d1}, 2: W_{dp+da+d2}, 3: W_da) as
  * int32[f(l,d)][l], in the R1 order.  Synchronous. */
 polya_status polya_get_exponents(const polya_ctx* ctx, int which, int32_t* out_host);

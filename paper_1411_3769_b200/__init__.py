@@ -15,7 +15,7 @@ __all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "EXPORTS", "L
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
 G_FULL, G_PAIR_TILES = 0, 1
-EXPORTS = ["polya_setup", "polya_dims_get", "polya_get_exponents", "polya_get_beta", "polya_get_H",
+EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents", "polya_get_beta", "polya_get_H",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
            "polya_get_timing"]
@@ -62,6 +62,7 @@ def lib():
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
     L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
+    L.polya_plan.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Dims)]
     L.polya_get_exponents.argtypes = [vp, ctypes.c_int, vp]
     L.polya_get_beta.argtypes = [vp, vp]
     L.polya_get_H.argtypes = [vp, vp]
@@ -87,6 +88,16 @@ def lib():
     del i32, dbl
     _lib = L
     return L
+
+
+def plan(n, l, dp, d1, d2, da=1, delta=1e-3, rank=0, nranks=1):
+    """polya_plan: host-only dims and this rank's share of the Schur work items (no GPU)."""
+    cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks)
+    d = _Dims()
+    st = lib().polya_plan(ctypes.byref(cfg), ctypes.byref(d))
+    if st != 0:
+        raise PolyaError(f"polya_plan: {lib().polya_strerror(st).decode()}")
+    return {k: getattr(d, k) for k, _ in _Dims._fields_}
 
 
 def _stream_ptr(stream=None):

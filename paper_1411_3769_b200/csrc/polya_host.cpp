@@ -107,7 +107,7 @@ T* dupload(const std::vector<T>& v) {
   return p;
 }
 
-void build(Ctx& c, const double* A_host) {
+void build(Ctx& c, const double* A_host, bool device = true) {
   const polya_config& g = c.cfg;
   c.n = g.n;
   c.l = g.l;
@@ -240,6 +240,7 @@ void build(Ctx& c, const double* A_host) {
     c.useful_flops_rank += (ph[p] == ph2[p] ? 1.0 : 2.0) * n4 * pK[p] * (double)(b - a) / (double)pItems[p];
   }
   c.npairs_local = c.pair1 - c.pair0;
+  if (!device) return;  // polya_plan: host-side bookkeeping only
 
   // ---- arena layout --------------------------------------------------------------------------
   // Q, R: one per (local pair, Lyapunov block active for both rows)
@@ -473,14 +474,36 @@ extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_hos
   return POLYA_OK;
 }
 
-extern "C" polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* o) {
-  if (!ctx || !o) return POLYA_EINVAL;
-  const Ctx& c = ctx->c;
+static void fill_dims(const Ctx& c, polya_dims* o) {
   o->L0 = c.L0; o->L = c.L; o->M = c.M; o->nblocks = c.nb; o->Ntil = c.Ntil; o->K = c.K;
   o->nnz_beta = c.nnz_beta; o->nnz_H = (int64_t)c.Hh.size();
   o->npairs = c.npairs; o->pair0 = c.pair0; o->pair1 = c.pair1; o->item0 = c.item0; o->item1 = c.item1;
   o->useful_flops_schur = c.useful_flops_rank;
   o->tiles_bytes = c.npairs_local * c.Ntil * c.Ntil * (int64_t)sizeof(double);
+}
+
+extern "C" polya_status polya_plan(const polya_config* cfg, polya_dims* out) {
+  if (!cfg || !out) return POLYA_EINVAL;
+  const polya_config& g = *cfg;
+  if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
+      g.rank < 0 || g.rank >= g.nranks)
+    return POLYA_EINVAL;
+  try {
+    Ctx c;
+    c.cfg = g;
+    build(c, nullptr, false);
+    fill_dims(c, out);
+  } catch (const Fail& f) {
+    return f.s;
+  } catch (const std::bad_alloc&) {
+    return POLYA_ENOMEM;
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* o) {
+  if (!ctx || !o) return POLYA_EINVAL;
+  fill_dims(ctx->c, o);
   return POLYA_OK;
 }
 
