@@ -200,7 +200,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
           if (c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) ++nu;
         pMu[p] = mu;
         pK[p] = 4 * mu + nu;                        // K_pair = 4 mu_hh' + nu_hh' (algorithmic)
-        pKpad[p] = (pK[p] + kKStage - 1) / kKStage * kKStage;  // zero-padded to whole stages
+        pKpad[p] = std::max<int64_t>(kKStage, (pK[p] + kKStage - 1) / kKStage * kKStage);  // whole stages, >= 1
         pItems[p] = (h == h2) ? c.ncls * (c.ncls + 1) / 2 : c.ncls * c.ncls;
       }
   }
@@ -365,7 +365,9 @@ void build(Ctx& c, const double* A_host, bool device = true) {
         kL.push_back((int32_t)(c.id_Xb + bidx[h * c.L + j])); kR.push_back((int32_t)(c.id_Wb + bidx[h2 * c.L + j]));
         kf.push_back(0); ks.push_back(1.0);
       }
-      while ((int64_t)(kL.size() - kbeg.back()) % kKStage) {  // zero terms up to a whole stage
+      // zero terms up to a whole stage; a pair with no common block still gets one (all-zero)
+      // stage so that every work item flows through the K4 pipeline
+      while ((int64_t)(kL.size() - kbeg.back()) % kKStage || (int64_t)kL.size() == kbeg.back()) {
         kL.push_back((int32_t)c.id_Zero); kR.push_back((int32_t)c.id_Zero); kf.push_back(0); ks.push_back(0.0);
       }
       kbeg.push_back((int64_t)kL.size());

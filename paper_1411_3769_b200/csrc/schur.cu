@@ -32,10 +32,12 @@ namespace {
 
 constexpr int Q = kChunk;  // 8
 constexpr int KB = 8;      // k terms per pipeline stage
-constexpr int NT = 128;    // 4 warps
+constexpr int NCW = 4;     // consumer (DMMA) warps: each a 4x4 grid of 8x8 tiles of the 64x64 sub-block
+constexpr int NT = (NCW + 1) * 32;  // + one producer warp (cp.async into an mbarrier ring)
+constexpr int NSTAGE = 4;  // ring depth
 constexpr int KS = 68;     // doubles per staged 8x8 tile: 64 + 4 pad (conflict-free LDS.64 fragments)
 constexpr int STAGE = 2 * KB * KS;  // doubles per stage: L[8 k][8 x][8 y] + R[8 k][8 z][8 w]
-constexpr size_t kSmemBytes = (2 * STAGE + Q * Q * Q * Q) * sizeof(double);
+constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 2 * NSTAGE * sizeof(uint64_t);
 
 struct SchurArgs {
   const double* arena;
@@ -90,15 +92,75 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sptr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(sptr(bar)) : "memory");
+}
+// arrive-on triggered when all prior cp.async of this thread have completed (no pending-count change)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(sptr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          sptr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory"); }
 
-__global__ void __launch_bounds__(NT, 4) k_schur(const SchurArgs p) {
+struct ItemInfo {
+  int pl, h, h2, sc, tc, ci, cj, ck, cl, nstage;
+  int64_t kb;
+};
+
+__device__ __forceinline__ ItemInfo decode_item(const SchurArgs& p, int64_t item) {
+  ItemInfo it;
+  int lo = 0, hi = p.npl;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (p.pair_item[mid] <= item) lo = mid; else hi = mid;
+  }
+  it.pl = lo;
+  it.h = p.pair_h[lo];
+  it.h2 = p.pair_h2[lo];
+  const int64_t rem = item - p.pair_item[lo];
+  if (it.h != it.h2) {
+    it.sc = (int)(rem / p.ncls);
+    it.tc = (int)(rem - (int64_t)it.sc * p.ncls);
+  } else {
+    int64_t r = rem;
+    int s = 0;
+    while (r >= p.ncls - s) { r -= p.ncls - s; ++s; }
+    it.sc = s;
+    it.tc = s + (int)r;
+  }
+  it.ci = p.cls_a[it.sc]; it.cj = p.cls_b[it.sc]; it.ck = p.cls_a[it.tc]; it.cl = p.cls_b[it.tc];
+  it.kb = p.pair_kbeg[lo];
+  it.nstage = (int)((p.pair_kbeg[lo + 1] - it.kb) / KB);   // k-lists are padded to whole stages
+  return it;
+}
+
+// chunk roles of orientation o: Raw[(x,y),(z,w)] with x in cX, y in cY, z in cZ, w in cW; the
+// local G index (a,b,c,d) is  o0: (w,x,y,z)  o1: (w,x,z,y)  o2: (x,w,y,z)  o3: (x,w,z,y)
+__device__ __forceinline__ void roles(int o, const ItemInfo& it, int& cX, int& cY, int& cZ, int& cW) {
+  cX = (o & 2) ? it.ci : it.cj;
+  cW = (o & 2) ? it.cj : it.ci;
+  cY = (o & 1) ? it.cl : it.ck;
+  cZ = (o & 1) ? it.ck : it.cl;
+}
+
+__global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
   extern __shared__ __align__(16) double smem[];
-  double* Gs = smem + 2 * STAGE;
+  double* Gs = smem + NSTAGE * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Gs + Q * Q * Q * Q);   // stage landed (32 producer arrivals)
+  uint64_t* empty = full + NSTAGE;                                      // stage consumed (NCW arrivals)
   __shared__ unsigned char s_diag[64][2];  // (lc, ld) of local pairs ordered by (ld-lc, lc)
-  __shared__ long long s_item;
   __shared__ int s_row[64], s_col[64];     // svec index of local (a,b) / (c,d) pairs, -1 if unused
+  __shared__ long long s_meta[NSTAGE];     // item index of the stage held by each ring slot
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   if (tid < 64) {  // diagonal order: consecutive entries have consecutive svec indices
@@ -107,122 +169,119 @@ __global__ void __launch_bounds__(NT, 4) k_schur(const SchurArgs p) {
       for (int lc = max(0, -dlt); lc <= min(Q - 1, Q - 1 - dlt); ++lc, ++idx)
         if (idx == tid) { s_diag[tid][0] = (unsigned char)lc; s_diag[tid][1] = (unsigned char)(lc + dlt); }
   }
-  // cp.async tasks of this thread per stage: 16-byte chunk (row sr, column pair sc2) of the tiles
-  // k = warp and k = warp + 4 of both operands
-  const int sr = lane >> 2, sc2 = lane & 3;
-  const int xw = 4 * (warp >> 1), zw = 4 * (warp & 1);  // warp's 4 x-tiles and 4 z-tiles
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_meta
+      mbar_init(empty + i, NCW);
+    }
+  }
+  __syncthreads();
+  const int n = p.n, np = p.np;
 
-  for (;;) {
-    if (tid == 0) s_item = (long long)atomicAdd(p.counter, 1ULL) + p.item0;
-    __syncthreads();
-    const int64_t item = s_item;
-    __syncthreads();
-    if (item >= p.item1) break;
-
-    int pl = 0;
-    {
-      int lo = 0, hi = p.npl;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (p.pair_item[mid] <= item) lo = mid; else hi = mid;
+  // Dynamic schedule: the producer pulls items from an atomic counter (pair-major order, so
+  // co-running CTAs share a pair's operands in L2) and tags the first stage of every item with
+  // its index in s_meta; the consumers learn the item sequence from the ring.
+  if (warp == NCW) {
+    // ===== producer warp: 16-byte cp.async chunks (row sr, column pair sc2) of all 16 tiles ====
+    const int sr = lane >> 2, sc2 = lane & 3;
+    uint32_t cnt = 0;
+    for (;;) {
+      unsigned long long got = 0;
+      if (lane == 0) got = atomicAdd(p.counter, 1ULL);
+      const int64_t item = p.item0 + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+      if (item >= p.item1) {  // end-of-work sentinel stage
+        const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+        mbar_wait(empty + slot, ph ^ 1);
+        if (lane == 0) s_meta[slot] = p.item1;
+        cp_async_mbar_arrive(full + slot);
+        if (lane == 0) mbar_arrive(full + slot);
+        break;
       }
-      pl = lo;
+      const ItemInfo it = decode_item(p, item);
+      const bool dS = (it.ci == it.cj), dT = (it.ck == it.cl);
+      for (int o = 0; o < 4; ++o) {
+        if ((o & 1) && dT) continue;
+        if ((o & 2) && dS) continue;
+        int cX, cY, cZ, cW;
+        roles(o, it, cX, cY, cZ, cW);
+        const int offL = (cX * Q + sr) * np + cY * Q + 2 * sc2;
+        const int offR = (cZ * Q + sr) * np + cW * Q + 2 * sc2;
+        int2 dcur = (lane < KB && it.nstage > 0) ? __ldg(p.kdesc + it.kb + lane) : make_int2(0, 0);
+        for (int s = 0; s < it.nstage; ++s) {
+          const int2 dnext = (lane < KB && s + 1 < it.nstage) ? __ldg(p.kdesc + it.kb + (int64_t)(s + 1) * KB + lane)
+                                                              : make_int2(0, 0);
+          const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+          mbar_wait(empty + slot, ph ^ 1);
+          if (lane == 0) s_meta[slot] = item;
+          double* T = smem + slot * STAGE + sr * Q + 2 * sc2;
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) {
+            const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, kk);
+            const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, kk);
+            cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL);
+            cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR);
+          }
+          cp_async_mbar_arrive(full + slot);
+          if (lane == 0) mbar_arrive(full + slot);   // releases s_meta[slot]
+          dcur = dnext;
+          ++cnt;
+        }
+      }
     }
-    const int h = p.pair_h[pl], h2 = p.pair_h2[pl];
-    const int64_t rem = item - p.pair_item[pl];
-    int sc, tc;
-    if (h != h2) {
-      sc = (int)(rem / p.ncls);
-      tc = (int)(rem - (int64_t)sc * p.ncls);
-    } else {
-      int64_t r = rem;
-      int s = 0;
-      while (r >= p.ncls - s) { r -= p.ncls - s; ++s; }
-      sc = s;
-      tc = s + (int)r;
-    }
-    const int ci = p.cls_a[sc], cj = p.cls_b[sc], ck = p.cls_a[tc], cl = p.cls_b[tc];
-    const bool dS = (ci == cj), dT = (ck == cl);
-    const int64_t kb = p.pair_kbeg[pl];
-    const int nstage = (int)((p.pair_kbeg[pl + 1] - kb) / KB);   // k-lists are padded to whole stages
-    const int n = p.n, np = p.np;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    return;
+  }
 
+  // ===== consumer warps: DMMA on ring stages, fold into Gs, epilogue ==========================
+  const int xw = 4 * (warp >> 1), zw = 4 * (warp & 1);  // warp's 4 x-tiles and 4 z-tiles
+  uint32_t cnt = 0;
+  for (;;) {
+    {  // the next ring stage is the first stage of the next item (or the end sentinel)
+      const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+      mbar_wait(full + slot, ph);
+    }
+    const int64_t item = s_meta[cnt % NSTAGE];
+    if (item >= p.item1) break;
+    const ItemInfo it = decode_item(p, item);
+    const bool dS = (it.ci == it.cj), dT = (it.ck == it.cl);
     bool first = true;
     for (int o = 0; o < 4; ++o) {
       if ((o & 1) && dT) continue;
       if ((o & 2) && dS) continue;
-      // Raw[(x,y),(z,w)], x in chunk cX, y in cY, z in cZ, w in cW; local G index (a,b,c,d) =
-      //   o0: (w,x,y,z)  o1: (w,x,z,y)  o2: (x,w,y,z)  o3: (x,w,z,y)
-      const int cX = (o & 2) ? ci : cj;
-      const int cW = (o & 2) ? cj : ci;
-      const int cY = (o & 1) ? cl : ck;
-      const int cZ = (o & 1) ? ck : cl;
+      int cX, cY, cZ, cW;
+      roles(o, it, cX, cY, cZ, cW);
       const int nvx = min(Q, n - cX * Q), nvz = min(Q, n - cZ * Q);
-      const int offL = (cX * Q + sr) * np + cY * Q + 2 * sc2;      // this thread's source offsets
-      const int offR = (cZ * Q + sr) * np + cW * Q + 2 * sc2;
-      const int dstT = sr * Q + 2 * sc2;                            // and target within a tile
-
+      // a warp whose x- or z-tiles all lie past a ragged chunk's end only multiplies zeros: skip
+      const bool active = (xw < nvx) && (zw < nvz);
       double acc[4][4][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      // a warp whose x- or z-tiles all lie past a ragged chunk's end only multiplies zeros: skip
-      const bool active = (xw < nvx) && (zw < nvz);
-
-      // 2-stage cp.async pipeline; the descriptors (arena matrix ids of L_k, R_k) of the next
-      // stage are fetched one stage ahead so no load waits on a dependent load
-      int2 dc[2], dn[2];
-      auto load_desc = [&](int s, int2* d) {
-        if (s < nstage) {
-          d[0] = __ldg(p.kdesc + kb + (int64_t)s * KB + warp);
-          d[1] = __ldg(p.kdesc + kb + (int64_t)s * KB + warp + 4);
-        }
-      };
-      auto issue = [&](int buf) {
-        double* T = smem + buf * STAGE + dstT;
+      for (int s = 0; s < it.nstage; ++s) {
+        const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+        mbar_wait(full + slot, ph);
+        if (active) {
+          const double* fA = smem + slot * STAGE + t * KS + xw * Q + g;   // A[y=g][k=t] of x-tile xw
+          const double* fB = fA + KB * KS + (zw - xw) * Q;                // B[k=t][w=g] of z-tile zw
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int kk = warp + 4 * q;
-          cp_async16(T + kk * KS, p.arena + (uint64_t)(unsigned)dc[q].x * p.ms32 + offL);
-          cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)(unsigned)dc[q].y * p.ms32 + offR);
-        }
-      };
-
-      if (nstage > 0) {
-        load_desc(0, dc);
-        issue(0);
-        cp_async_commit();
-        load_desc(1, dc);
-        const double* fA = smem + t * KS + xw * Q + g;   // fragment bases: A[y=g][k=t] of x-tile xw
-        const double* fB = smem + KB * KS + t * KS + zw * Q + g;
-        for (int s = 0; s < nstage; ++s) {
-          const int boff = (s & 1) * STAGE;
-          if (s + 1 < nstage) {
-            issue((s & 1) ^ 1);      // stage s+1 (descriptors arrived during stage s-1)
-            load_desc(s + 2, dn);
+          for (int k4 = 0; k4 < 2; ++k4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = fA[k4 * 4 * KS + i * Q];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = fB[k4 * 4 * KS + j * Q];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
           }
-          cp_async_commit();
-          cp_async_wait1();          // this thread's copies of stage s have landed
-          __syncthreads();           // ... and everybody else's
-          if (active) {
-#pragma unroll
-            for (int k4 = 0; k4 < 2; ++k4) {
-              double a[4], b[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) a[i] = fA[boff + k4 * 4 * KS + i * Q];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) b[j] = fB[boff + k4 * 4 * KS + j * Q];
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-            }
-          }
-          __syncthreads();           // buffer s&1 is refilled by the issue of iteration s+1
-          dc[0] = dn[0]; dc[1] = dn[1];
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+        ++cnt;
       }
+      consumer_sync();   // the previous fold / the previous item's epilogue is done with Gs
       // fold: thread holds Raw(x = xw+i, y = g, z = zw+j, w = 2t+e) -> Gs[(a,b,c,d)(o)]
       {
         int bx[4], bz[4], be[2];
@@ -255,11 +314,12 @@ __global__ void __launch_bounds__(NT, 4) k_schur(const SchurArgs p) {
         }
       }
       first = false;
-      __syncthreads();
     }
-
+    consumer_sync();     // all folds of the item are in Gs
     // ---- epilogue: fold diagonal classes and write G ----------------------------------------
-    if (tid < 128) {  // svec tables of the item's local pairs
+    const int h = it.h, h2 = it.h2, sc = it.sc, tc = it.tc, pl = it.pl;
+    const int ci = it.ci, cj = it.cj, ck = it.ck, cl = it.cl;
+    {  // svec tables of the item's local pairs (consumer threads 0..127)
       const int q = tid & 63;
       const int l1 = q >> 3, l2 = q & 7;
       const int c1 = (tid < 64) ? ci : ck, c2 = (tid < 64) ? cj : cl;
@@ -268,7 +328,7 @@ __global__ void __launch_bounds__(NT, 4) k_schur(const SchurArgs p) {
       const int v = (a < n && b < n && (!dg || l1 <= l2)) ? (int)svec_idx(a, b, n) : -1;
       if (tid < 64) s_row[q] = v; else s_col[q] = v;
     }
-    __syncthreads();
+    consumer_sync();
     const bool diag_pair = (h == h2);
     const bool same_cls = diag_pair && (sc == tc);
     const int64_t rowbase = (int64_t)h * p.Ntil, colbase = (int64_t)h2 * p.Ntil;
@@ -283,7 +343,7 @@ __global__ void __launch_bounds__(NT, 4) k_schur(const SchurArgs p) {
       const int f_swap = pass == 0 ? (Tc(fb) ^ fa) : (Ta(fb) ^ Tb(fa));
       const bool fdiag = pass == 0 ? dT : dS;   // the fixed pair's class is diagonal
       const bool vdiag = pass == 0 ? dS : dT;   // the varying pair's class is diagonal
-      for (int sl = tid >> 6; sl < 64; sl += NT / 64) {
+      for (int sl = tid >> 6; sl < 64; sl += NCW * 32 / 64) {
         const int u1 = sl >> 3, u2 = sl & 7;
         const int vidx = pass == 0 ? s_row[sl] : s_col[sl];
         if (vidx < 0) continue;
@@ -310,7 +370,6 @@ __global__ void __launch_bounds__(NT, 4) k_schur(const SchurArgs p) {
         }
       }
     }
-    // Gs / s_row / s_col are rewritten by the next item only after the syncs at the loop top
   }
 }
 
