@@ -13,7 +13,8 @@ import numpy as np
 
 __all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "EXPORTS", "LIB_PATH"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
+# POLYA_LIB overrides the library path (timing-experiment variants built by tools/schur_exp.py)
+LIB_PATH = os.environ.get("POLYA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
 G_FULL, G_PAIR_TILES = 0, 1
 EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents", "polya_get_beta", "polya_get_H",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",

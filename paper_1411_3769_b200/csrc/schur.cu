@@ -33,7 +33,11 @@ namespace {
 constexpr int Q = kChunk;  // 8
 constexpr int KB = 8;      // k terms per pipeline stage
 constexpr int NCW = 4;     // consumer (DMMA) warps: each a 4x4 grid of 8x8 tiles of the 64x64 sub-block
+#ifdef NT_OVERRIDE
+constexpr int NT = NT_OVERRIDE;
+#else
 constexpr int NT = (NCW + 1) * 32;  // + one producer warp (cp.async into an mbarrier ring)
+#endif
 constexpr int NSTAGE = 4;  // ring depth
 constexpr int KS = 68;     // doubles per staged 8x8 tile: 64 + 4 pad (conflict-free LDS.64 fragments)
 constexpr int STAGE = 2 * KB * KS;  // doubles per stage: L[8 k][8 x][8 y] + R[8 k][8 z][8 w]
@@ -117,50 +121,90 @@ struct ItemInfo {
   int64_t kb;
 };
 
-__device__ __forceinline__ ItemInfo decode_item(const SchurArgs& p, int64_t item) {
+// Item -> (pair, row class, column class).  `hint` is the pair of the CTA's previous item: items
+// are pulled in increasing order, so the pair is usually the same or the next one (one load);
+// otherwise a binary search.  Diagonal pairs enumerate classes sc <= tc row by row; the row is
+// found in closed form (no O(ncls) loop).
+__device__ __forceinline__ ItemInfo decode_item(const SchurArgs& p, int64_t item, int hint) {
   ItemInfo it;
-  int lo = 0, hi = p.npl;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (p.pair_item[mid] <= item) lo = mid; else hi = mid;
+  int lo = hint;
+  if (!(lo >= 0 && lo < p.npl && __ldg(p.pair_item + lo) <= item && item < __ldg(p.pair_item + lo + 1))) {
+    lo = 0;
+    int hi = p.npl;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(p.pair_item + mid) <= item) lo = mid; else hi = mid;
+    }
   }
   it.pl = lo;
-  it.h = p.pair_h[lo];
-  it.h2 = p.pair_h2[lo];
-  const int64_t rem = item - p.pair_item[lo];
+  it.h = __ldg(p.pair_h + lo);
+  it.h2 = __ldg(p.pair_h2 + lo);
+  const int64_t rem = item - __ldg(p.pair_item + lo);
   if (it.h != it.h2) {
     it.sc = (int)(rem / p.ncls);
     it.tc = (int)(rem - (int64_t)it.sc * p.ncls);
   } else {
-    int64_t r = rem;
-    int s = 0;
-    while (r >= p.ncls - s) { r -= p.ncls - s; ++s; }
-    it.sc = s;
-    it.tc = s + (int)r;
+    // row sc starts at st(sc) = sc*ncls - sc(sc-1)/2
+    const int64_t N = p.ncls;
+    const double N2 = 2.0 * (double)N + 1.0;
+    int64_t sc = (int64_t)((N2 - sqrt(N2 * N2 - 8.0 * (double)rem)) * 0.5);
+    sc = max((int64_t)0, min(sc, N - 1));
+    while (sc > 0 && sc * N - sc * (sc - 1) / 2 > rem) --sc;
+    while (sc + 1 < N && (sc + 1) * N - (sc + 1) * sc / 2 <= rem) ++sc;
+    it.sc = (int)sc;
+    it.tc = (int)(sc + rem - (sc * N - sc * (sc - 1) / 2));
   }
-  it.ci = p.cls_a[it.sc]; it.cj = p.cls_b[it.sc]; it.ck = p.cls_a[it.tc]; it.cl = p.cls_b[it.tc];
-  it.kb = p.pair_kbeg[lo];
-  it.nstage = (int)((p.pair_kbeg[lo + 1] - it.kb) / KB);   // k-lists are padded to whole stages
+  it.ci = __ldg(p.cls_a + it.sc); it.cj = __ldg(p.cls_b + it.sc);
+  it.ck = __ldg(p.cls_a + it.tc); it.cl = __ldg(p.cls_b + it.tc);
+  it.kb = __ldg(p.pair_kbeg + lo);
+  it.nstage = (int)((__ldg(p.pair_kbeg + lo + 1) - it.kb) / KB);   // k-lists are padded to whole stages
   return it;
 }
 
+// What the producer tells the consumers at the first stage of every item (and the end sentinel).
+struct __align__(16) SlotInfo {
+  long long item;
+  int pl, h, h2, sc, tc, ci, cj, ck, cl, nstage;
+};
+
 // chunk roles of orientation o: Raw[(x,y),(z,w)] with x in cX, y in cY, z in cZ, w in cW; the
 // local G index (a,b,c,d) is  o0: (w,x,y,z)  o1: (w,x,z,y)  o2: (x,w,y,z)  o3: (x,w,z,y)
-__device__ __forceinline__ void roles(int o, const ItemInfo& it, int& cX, int& cY, int& cZ, int& cW) {
+template <class I>
+__device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int& cZ, int& cW) {
   cX = (o & 2) ? it.ci : it.cj;
   cW = (o & 2) ? it.cj : it.ci;
   cY = (o & 1) ? it.cl : it.ck;
   cZ = (o & 1) ? it.ck : it.cl;
 }
 
-__global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
+#ifndef SCHUR_EXP
+#define SCHUR_EXP 0   // timing experiments only (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either,
+                      // 4 = no operand loads, 8 = no ragged-warp skip
+#endif
+#ifndef SCHUR_MINB
+#define SCHUR_MINB 3
+#endif
+
+// One G entry of the item from the folded block: canonical summation order (direct, s-swap,
+// t-swap, both) so that an entry and its mirror image are bitwise equal.  Table entries are
+// {svec index, Gs term direct, Gs term swapped, has swap}.
+__device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
+  double v = Gs[r.y ^ c.y];
+  if (r.w) v += Gs[r.z ^ c.y];
+  if (c.w) v += Gs[r.y ^ c.z];
+  if (r.w && c.w) v += Gs[r.z ^ c.z];
+  return v;
+}
+
+__global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   extern __shared__ __align__(16) double smem[];
   double* Gs = smem + NSTAGE * STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(Gs + Q * Q * Q * Q);   // stage landed (32 producer arrivals)
   uint64_t* empty = full + NSTAGE;                                      // stage consumed (NCW arrivals)
   __shared__ unsigned char s_diag[64][2];  // (lc, ld) of local pairs ordered by (ld-lc, lc)
-  __shared__ int s_row[64], s_col[64];     // svec index of local (a,b) / (c,d) pairs, -1 if unused
-  __shared__ long long s_meta[NSTAGE];     // item index of the stage held by each ring slot
+  __shared__ int4 s_rt[64], s_ct[64];      // epilogue tables of the item's valid row / column pairs
+  __shared__ int s_nrc[2];                 // their counts
+  __shared__ SlotInfo s_info[NSTAGE];      // item of the stage held by each ring slot (first stages)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   if (tid < 64) {  // diagonal order: consecutive entries have consecutive svec indices
@@ -171,7 +215,7 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
   }
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_meta
+      mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
       mbar_init(empty + i, NCW);
     }
   }
@@ -179,26 +223,35 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
   const int n = p.n, np = p.np;
 
   // Dynamic schedule: the producer pulls items from an atomic counter (pair-major order, so
-  // co-running CTAs share a pair's operands in L2) and tags the first stage of every item with
-  // its index in s_meta; the consumers learn the item sequence from the ring.
+  // co-running CTAs share a pair's operands in L2), one item ahead: while it streams item i it
+  // already holds the index, decode and first k-descriptors of item i+1, so no stage waits on
+  // an atomic, a table lookup or a descriptor load.  The consumers learn each item from s_info.
   if (warp == NCW) {
     // ===== producer warp: 16-byte cp.async chunks (row sr, column pair sc2) of all 16 tiles ====
     const int sr = lane >> 2, sc2 = lane & 3;
     uint32_t cnt = 0;
-    for (;;) {
-      unsigned long long got = 0;
+    unsigned long long got = 0;
+    if (lane == 0) got = atomicAdd(p.counter, 1ULL);
+    int64_t item = p.item0 + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+    ItemInfo it{};
+    int2 dfirst = make_int2(0, 0);
+    if (item < p.item1) {
+      it = decode_item(p, item, -1);
+      if (lane < KB) dfirst = __ldg(p.kdesc + it.kb + lane);
       if (lane == 0) got = atomicAdd(p.counter, 1ULL);
-      const int64_t item = p.item0 + (int64_t)__shfl_sync(0xffffffffu, got, 0);
-      if (item >= p.item1) {  // end-of-work sentinel stage
-        const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
-        mbar_wait(empty + slot, ph ^ 1);
-        if (lane == 0) s_meta[slot] = p.item1;
-        cp_async_mbar_arrive(full + slot);
-        if (lane == 0) mbar_arrive(full + slot);
-        break;
+    }
+    while (item < p.item1) {
+      // next item: index (requested one item ago), decode and first descriptors, in flight now
+      const int64_t item_n = p.item0 + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+      ItemInfo it_n{};
+      int2 dfirst_n = make_int2(0, 0);
+      if (item_n < p.item1) {
+        it_n = decode_item(p, item_n, it.pl);
+        if (lane < KB) dfirst_n = __ldg(p.kdesc + it_n.kb + lane);
+        if (lane == 0) got = atomicAdd(p.counter, 1ULL);
       }
-      const ItemInfo it = decode_item(p, item);
       const bool dS = (it.ci == it.cj), dT = (it.ck == it.cl);
+      bool first_stage = true;
       for (int o = 0; o < 4; ++o) {
         if ((o & 1) && dT) continue;
         if ((o & 2) && dS) continue;
@@ -206,27 +259,47 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
         roles(o, it, cX, cY, cZ, cW);
         const int offL = (cX * Q + sr) * np + cY * Q + 2 * sc2;
         const int offR = (cZ * Q + sr) * np + cW * Q + 2 * sc2;
-        int2 dcur = (lane < KB && it.nstage > 0) ? __ldg(p.kdesc + it.kb + lane) : make_int2(0, 0);
+        int2 dcur = dfirst;
         for (int s = 0; s < it.nstage; ++s) {
-          const int2 dnext = (lane < KB && s + 1 < it.nstage) ? __ldg(p.kdesc + it.kb + (int64_t)(s + 1) * KB + lane)
-                                                              : make_int2(0, 0);
+          // descriptors of the next stage: the next k-block, or the first one again (the next
+          // orientation walks the same k-list; the next item's were loaded above)
+          int2 dnext = dfirst;
+          if (s + 1 < it.nstage && lane < KB) dnext = __ldg(p.kdesc + it.kb + (int64_t)(s + 1) * KB + lane);
           const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
           mbar_wait(empty + slot, ph ^ 1);
-          if (lane == 0) s_meta[slot] = item;
+          if (first_stage && lane == 0) {
+            SlotInfo si;
+            si.item = item; si.pl = it.pl; si.h = it.h; si.h2 = it.h2; si.sc = it.sc; si.tc = it.tc;
+            si.ci = it.ci; si.cj = it.cj; si.ck = it.ck; si.cl = it.cl; si.nstage = it.nstage;
+            s_info[slot] = si;
+          }
+          first_stage = false;
           double* T = smem + slot * STAGE + sr * Q + 2 * sc2;
 #pragma unroll
           for (int kk = 0; kk < KB; ++kk) {
             const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, kk);
             const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, kk);
-            cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL);
-            cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR);
+            if (!(SCHUR_EXP & 4)) {   // experiment bit 4: no operand loads (timing of the DMMA side only)
+              cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL);
+              cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR);
+            }
           }
           cp_async_mbar_arrive(full + slot);
-          if (lane == 0) mbar_arrive(full + slot);   // releases s_meta[slot]
+          if (lane == 0) mbar_arrive(full + slot);   // releases s_info[slot]
           dcur = dnext;
           ++cnt;
         }
       }
+      item = item_n;
+      it = it_n;
+      dfirst = dfirst_n;
+    }
+    {  // end-of-work sentinel stage
+      const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+      mbar_wait(empty + slot, ph ^ 1);
+      if (lane == 0) s_info[slot].item = p.item1;
+      cp_async_mbar_arrive(full + slot);
+      if (lane == 0) mbar_arrive(full + slot);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     return;
@@ -240,9 +313,8 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
       const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
       mbar_wait(full + slot, ph);
     }
-    const int64_t item = s_meta[cnt % NSTAGE];
-    if (item >= p.item1) break;
-    const ItemInfo it = decode_item(p, item);
+    const SlotInfo it = s_info[cnt % NSTAGE];
+    if (it.item >= p.item1) break;
     const bool dS = (it.ci == it.cj), dT = (it.ck == it.cl);
     bool first = true;
     for (int o = 0; o < 4; ++o) {
@@ -252,7 +324,7 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
       roles(o, it, cX, cY, cZ, cW);
       const int nvx = min(Q, n - cX * Q), nvz = min(Q, n - cZ * Q);
       // a warp whose x- or z-tiles all lie past a ragged chunk's end only multiplies zeros: skip
-      const bool active = (xw < nvx) && (zw < nvz);
+      const bool active = ((SCHUR_EXP & 8) != 0) || ((xw < nvx) && (zw < nvz));   // bit 8: no ragged skip
       double acc[4][4][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -280,6 +352,16 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
         ++cnt;
+      }
+      if (SCHUR_EXP & 2) {   // timing experiment: no fold, no epilogue (a never-taken sink keeps the DMMAs)
+        double sum = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sum += acc[i][j][0] * acc[i][j][1];
+        if (sum == 1.2345e-300) p.G[tid] = sum;
+        first = false;
+        continue;
       }
       consumer_sync();   // the previous fold / the previous item's epilogue is done with Gs
       // fold: thread holds Raw(x = xw+i, y = g, z = zw+j, w = 2t+e) -> Gs[(a,b,c,d)(o)]
@@ -315,59 +397,58 @@ __global__ void __launch_bounds__(NT, 3) k_schur(const SchurArgs p) {
       }
       first = false;
     }
+    if (SCHUR_EXP & 3) continue;   // timing experiment: no epilogue
     consumer_sync();     // all folds of the item are in Gs
     // ---- epilogue: fold diagonal classes and write G ----------------------------------------
-    const int h = it.h, h2 = it.h2, sc = it.sc, tc = it.tc, pl = it.pl;
-    const int ci = it.ci, cj = it.cj, ck = it.ck, cl = it.cl;
-    {  // svec tables of the item's local pairs (consumer threads 0..127)
-      const int q = tid & 63;
-      const int l1 = q >> 3, l2 = q & 7;
-      const int c1 = (tid < 64) ? ci : ck, c2 = (tid < 64) ? cj : cl;
-      const bool dg = (tid < 64) ? dS : dT;
-      const int a = c1 * Q + l1, b = c2 * Q + l2;
-      const int v = (a < n && b < n && (!dg || l1 <= l2)) ? (int)svec_idx(a, b, n) : -1;
-      if (tid < 64) s_row[q] = v; else s_col[q] = v;
+    // Tables of the item's valid local pairs, compacted in diagonal order (consecutive entries
+    // have consecutive svec indices, so a warp's stores form contiguous runs): warp 0 the rows
+    // (a,b) of class (ci,cj), warp 1 the columns (c,d) of class (ck,cl).
+    if (warp < 2) {
+      const bool rows = (warp == 0);
+      const int c1 = rows ? it.ci : it.ck, c2 = rows ? it.cj : it.cl;
+      const bool dg = rows ? dS : dT;
+      int4* tab = rows ? s_rt : s_ct;
+      int base = 0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int q = lane + 32 * half;
+        const int u1 = s_diag[q][0], u2 = s_diag[q][1];
+        const int A = c1 * Q + u1, B = c2 * Q + u2;
+        const bool valid = (A < n) && (B < n) && (!dg || u1 <= u2);
+        const unsigned bal = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          const int pos = base + __popc(bal & ((1u << lane) - 1u));
+          tab[pos] = rows ? make_int4((int)svec_idx(A, B, n), Ta(u1) ^ Tb(u2), Ta(u2) ^ Tb(u1), dg && u1 != u2)
+                          : make_int4((int)svec_idx(A, B, n), Tc(u1) ^ u2, Tc(u2) ^ u1, dg && u1 != u2);
+        }
+        base += __popc(bal);
+      }
+      if (lane == 0) s_nrc[warp] = base;
     }
     consumer_sync();
-    const bool diag_pair = (h == h2);
-    const bool same_cls = diag_pair && (sc == tc);
-    const int64_t rowbase = (int64_t)h * p.Ntil, colbase = (int64_t)h2 * p.Ntil;
-    double* tile = p.G + (int64_t)pl * p.Ntil * p.Ntil;
-    for (int pass = 0; pass < 2; ++pass) {
-      // pass 0: direct entries, lanes along t (diagonal order); pass 1: mirror entries, lanes along s
-      if (pass == 1 && !(p.layout == POLYA_G_FULL || diag_pair)) break;
-      const int fa = s_diag[tid & 63][0], fb = s_diag[tid & 63][1];   // this thread's fixed pair
-      const int fidx = pass == 0 ? s_col[fa * Q + fb] : s_row[fa * Q + fb];
-      if (fidx < 0) continue;
-      const int f_direct = pass == 0 ? (Tc(fa) ^ fb) : (Ta(fa) ^ Tb(fb));
-      const int f_swap = pass == 0 ? (Tc(fb) ^ fa) : (Ta(fb) ^ Tb(fa));
-      const bool fdiag = pass == 0 ? dT : dS;   // the fixed pair's class is diagonal
-      const bool vdiag = pass == 0 ? dS : dT;   // the varying pair's class is diagonal
-      for (int sl = tid >> 6; sl < 64; sl += NCW * 32 / 64) {
-        const int u1 = sl >> 3, u2 = sl & 7;
-        const int vidx = pass == 0 ? s_row[sl] : s_col[sl];
-        if (vidx < 0) continue;
-        const int64_t s_ = pass == 0 ? vidx : fidx, t_ = pass == 0 ? fidx : vidx;
-        if (same_cls && s_ > t_) continue;
-        const int v_direct = pass == 0 ? (Ta(u1) ^ Tb(u2)) : (Tc(u1) ^ u2);
-        const int v_swap = pass == 0 ? (Ta(u2) ^ Tb(u1)) : (Tc(u2) ^ u1);
-        // canonical summation order (direct, s-swap, t-swap, both) in both passes, so that an
-        // entry and its mirror image are bitwise equal
-        const int s_d = pass == 0 ? v_direct : f_direct, s_s = pass == 0 ? v_swap : f_swap;
-        const int t_d = pass == 0 ? f_direct : v_direct, t_s = pass == 0 ? f_swap : v_swap;
-        const bool hs = pass == 0 ? (vdiag && u1 != u2) : (fdiag && fa != fb);
-        const bool ht = pass == 0 ? (fdiag && fa != fb) : (vdiag && u1 != u2);
-        double val = Gs[s_d ^ t_d];
-        if (hs) val += Gs[s_s ^ t_d];
-        if (ht) val += Gs[s_d ^ t_s];
-        if (hs && ht) val += Gs[s_s ^ t_s];
-        if (p.layout == POLYA_G_FULL) {
-          if (pass == 0) p.G[(rowbase + s_) * p.K + colbase + t_] = val;
-          else p.G[(colbase + t_) * p.K + rowbase + s_] = val;
-        } else {
-          if (pass == 0) tile[s_ * p.Ntil + t_] = val;
-          else tile[t_ * p.Ntil + s_] = val;
-        }
+    const int nr = s_nrc[0], nc = s_nrc[1];
+    const bool diag_pair = (it.h == it.h2);
+    const bool same_cls = diag_pair && (it.sc == it.tc);
+    const bool fullG = (p.layout == POLYA_G_FULL);
+    const int64_t rowbase = (int64_t)it.h * p.Ntil, colbase = (int64_t)it.h2 * p.Ntil;
+    double* tile = p.G + (int64_t)it.pl * p.Ntil * p.Ntil;
+    const int4 none = make_int4(-1, 0, 0, 0);
+    {  // pass 0: direct entries G[s][t], lanes along the columns t
+      const int4 cA = lane < nc ? s_ct[lane] : none, cB = lane + 32 < nc ? s_ct[lane + 32] : none;
+      for (int r = warp; r < nr; r += NCW) {
+        const int4 rw = s_rt[r];
+        double* dst = fullG ? p.G + (rowbase + rw.x) * p.K + colbase : tile + (int64_t)rw.x * p.Ntil;
+        if (cA.x >= 0 && !(same_cls && rw.x > cA.x)) dst[cA.x] = gval(Gs, rw, cA);
+        if (cB.x >= 0 && !(same_cls && rw.x > cB.x)) dst[cB.x] = gval(Gs, rw, cB);
+      }
+    }
+    if (fullG || diag_pair) {  // pass 1: mirror entries G[t][s], lanes along the rows s
+      const int4 rA = lane < nr ? s_rt[lane] : none, rB = lane + 32 < nr ? s_rt[lane + 32] : none;
+      for (int c = warp; c < nc; c += NCW) {
+        const int4 cl = s_ct[c];
+        double* dst = fullG ? p.G + (colbase + cl.x) * p.K + rowbase : tile + (int64_t)cl.x * p.Ntil;
+        if (rA.x >= 0 && !(same_cls && rA.x > cl.x)) dst[rA.x] = gval(Gs, rA, cl);
+        if (rB.x >= 0 && !(same_cls && rB.x > cl.x)) dst[rB.x] = gval(Gs, rB, cl);
       }
     }
   }
