@@ -204,8 +204,15 @@ def run_gpu(args, cfg, cid):
     L0, L, M = counts(cfg)
     A, X, W = synth.make_case(cfg, L + M, seed=0)
     t0 = time.perf_counter()
-    ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world)
+    blocks = args.shard == "blocks"
+    ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world,
+                   shard=pb.SHARD_BLOCKS if blocks else pb.SHARD_TILES)
     setup_s = time.perf_counter() - t0
+    if blocks:   # NCCL communicator of the library (id from rank 0, distributed over the process group)
+        uid = [pb.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0])
     K, N = ctx.K, ctx.Ntil
     npl = ctx.dims["pair1"] - ctx.dims["pair0"]
     wg_rank = ctx.dims["useful_flops_schur"]
@@ -214,14 +221,24 @@ def run_gpu(args, cfg, cid):
     Xd = torch.from_numpy(X).to(dev)
     Wd = torch.from_numpy(W).to(dev)
     y = torch.from_numpy(np.random.default_rng(1).normal(size=K)).to(dev)
-    G = torch.empty((max(npl, 1), N, N), dtype=torch.float64, device=dev)
+    if blocks:   # partial G over this rank's blocks (all pair tiles + padding) and its reduced panel
+        G = torch.zeros(world * ctx.dims["reduce_count"], dtype=torch.float64, device=dev)
+        Grecv = torch.empty(ctx.dims["reduce_count"], dtype=torch.float64, device=dev)
+    else:
+        G = torch.empty((max(npl, 1), N, N), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # 256 MiB > 126 MB L2
     ctx.set_timing(True)
+
+    ev_c = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
 
     def step():
         Bt = ctx.apply(y)
         yv = ctx.adjoint(Xd)
         ctx.schur(Xd, Wd, G=G, layout=pb.G_PAIR_TILES)
+        if blocks:
+            ev_c[0].record()
+            ctx.reduce_G(G, out=Grecv, layout=pb.G_PAIR_TILES)
+            ev_c[1].record()
         return Bt, yv
 
     for _ in range(args.warmup):
@@ -229,7 +246,7 @@ def run_gpu(args, cfg, cid):
     barrier()
     clk = ClockSampler(local)
     launches0 = ctx.launch_count()
-    step_ms, pre_ms, asm_ms = [], [], []
+    step_ms, pre_ms, asm_ms, comb_ms = [], [], [], []
     clk.start()
     time.sleep(0.3)
     barrier()
@@ -245,6 +262,8 @@ def run_gpu(args, cfg, cid):
         step_ms.append(e0.elapsed_time(e1))
         pre_ms.append(p)
         asm_ms.append(a)
+        if blocks:
+            comb_ms.append(ev_c[0].elapsed_time(ev_c[1]))
     barrier()
     clocks = clk.stop()
     launches = ctx.launch_count() - launches0
@@ -254,6 +273,7 @@ def run_gpu(args, cfg, cid):
     t_asm_rank = statistics.mean(asm_ms)
     t_pre = max_over_ranks(statistics.mean(pre_ms))
     t_asm = max_over_ranks(t_asm_rank)
+    t_comb = max_over_ranks(statistics.mean(comb_ms)) if blocks else 0.0
     value = wg_total / (t_step * 1e-3) / 1e12
 
     # ---- end to end through the public API: host (pinned) inputs -> device -> G back to host ----
@@ -262,7 +282,8 @@ def run_gpu(args, cfg, cid):
         Xh = torch.from_numpy(X).pin_memory()
         Wh = torch.from_numpy(W).pin_memory()
         yh = y.cpu().pin_memory()
-        Gh = torch.empty(G.shape, dtype=torch.float64).pin_memory()
+        Gres = Grecv if blocks else G          # the step's result on this rank
+        Gh = torch.empty(Gres.shape, dtype=torch.float64).pin_memory()
         h2d = Xh.numel() * 8 + Wh.numel() * 8 + yh.numel() * 8
         d2h = Gh.numel() * 8
         barrier()
@@ -275,7 +296,7 @@ def run_gpu(args, cfg, cid):
             Wd.copy_(Wh, non_blocking=True)
             y.copy_(yh, non_blocking=True)
             step()
-            Gh.copy_(G, non_blocking=True)
+            Gh.copy_(Gres, non_blocking=True)
             e1.record()
             e1.synchronize()
             e2e_ms.append(e0.elapsed_time(e1))
@@ -287,8 +308,9 @@ def run_gpu(args, cfg, cid):
 
     # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step; N=1 only) ----
     ipm = None
-    if world == 1 and not args.no_ipm and ctx.K * ctx.K * 8 < 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+    if world == 1 and not blocks and not args.no_ipm and ctx.K * ctx.K * 8 < 0.6 * torch.cuda.get_device_properties(dev).total_memory:
         del G
+        flush = None
         torch.cuda.empty_cache()
         Xi = torch.eye(cfg.n, dtype=torch.float64, device=dev).repeat(ctx.nblocks, 1, 1).contiguous()
         Zi = Xi.clone()
@@ -334,12 +356,16 @@ def run_gpu(args, cfg, cid):
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded synth/ generators; SURVEY 8(d))",
             "config": {"workload": workload_name(cfg, cid), "K": K, "nblocks": ctx.nblocks, "L0": ctx.L0,
-                       "step": "polya_apply + polya_adjoint + polya_schur (precompute + assembly)",
-                       "layout": "G pair tiles (upper, row-panel ready)", "parallelism": f"output-tile shards x{world}",
+                       "step": "polya_apply + polya_adjoint + polya_schur (precompute + assembly)"
+                               + (" + polya_reduce_G (NCCL ReduceScatter)" if blocks else ""),
+                       "layout": "G pair tiles (upper, row-panel ready)",
+                       "parallelism": (f"Polya-block shards x{world} + NCCL ReduceScatter of partial G" if blocks
+                                       else f"output-tile shards x{world}"),
                        "l2": "256 MiB memset between timed steps (outside the events); G write alone is "
                              f"{npl * N * N * 8 / 1e9:.1f} GB/step"},
             "breakdown_ms": {"schur_precompute": t_pre, "schur_assembly": t_asm,
-                             "apply_adjoint_and_rest": t_step - t_pre - t_asm, "setup_once_s": setup_s},
+                             "combine_nccl": t_comb,
+                             "apply_adjoint_and_rest": t_step - t_pre - t_asm - t_comb, "setup_once_s": setup_s},
             "tflops_schur_assembly_only": wg_total / (t_asm * 1e-3) / 1e12,
             "roofline": {"bound": "tensor", "kernel": "k_schur (K4, FP64 DMMA)", "achieved": achieved, "peak": peak,
                          "unit": UNIT, "frac": achieved / peak, "traffic": traffic,
@@ -366,6 +392,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shard", default="tiles", choices=["tiles", "blocks"],
+                    help="tiles: output-tile sharding, no data-path collective (default); blocks: the paper's "
+                         "Polya-block sharding with the partial G summed by NCCL ReduceScatter")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ipm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -52,20 +52,31 @@ typedef enum {
   POLYA_EOVERFLOW = 2,  /* checked int64 failure on f(l,d), K, K*K or a byte size */
   POLYA_ENOMEM = 3,     /* device or host allocation failed                       */
   POLYA_ECUDA = 4,      /* CUDA runtime / kernel error                            */
-  POLYA_ENCCL = 5,      /* reserved (multi-GPU collectives)                       */
+  POLYA_ENCCL = 5,      /* NCCL error, or a collective called without polya_nccl_init */
   POLYA_ENOTPD = 6,     /* a Z block or the Schur complement is not positive definite */
   POLYA_ESTEP = 7,      /* line search found no admissible step                   */
   POLYA_EMAXIT = 8      /* reserved (iteration limit of a driver)                 */
 } polya_status;
 
+/* How the Schur complement is split across ranks:
+ *  POLYA_SHARD_TILES   output-tile sharding: every rank holds all blocks' X, Z^{-1} and
+ *                      computes a cost-balanced range of G's work items completely; no
+ *                      inter-GPU traffic (the default).
+ *  POLYA_SHARD_BLOCKS  the paper's decentralised scheme: rank r owns a
+ *                      cost-balanced contiguous range [b0, b1) of the Polya blocks and computes
+ *                      the partial G^(r) = sum_{b in [b0,b1)} G^(b) over ALL entries; the partials
+ *                      are summed by polya_reduce_G (NCCL ReduceScatter / AllReduce).       */
+typedef enum { POLYA_SHARD_TILES = 0, POLYA_SHARD_BLOCKS = 1 } polya_shard;
+
 /* Problem shape.  delta > 0 is the P-positivity margin of Eq. Cj ("a small
  * positive parameter"; R9 default 1e-3).  rank / nranks select
- * this context's share of the Schur complement (output-tile sharding, see
- * polya_schur); nranks = 1 for a single GPU. */
+ * this context's share of the Schur complement (per `shard`, see polya_schur);
+ * nranks = 1 for a single GPU. */
 typedef struct {
   int32_t n, l, dp, da, d1, d2;
   double delta;
   int32_t rank, nranks;
+  int32_t shard;     /* polya_shard */
 } polya_config;
 
 typedef struct {
@@ -83,6 +94,10 @@ typedef struct {
   double useful_flops_schur;  /* W_G: algorithmic FP64 FLOPs of one polya_schur on
                                  this rank (upper triangle) */
   int64_t tiles_bytes;  /* bytes of G in POLYA_G_PAIR_TILES layout on this rank   */
+  int64_t b0, b1;       /* this rank's Polya blocks [b0, b1) (all blocks with SHARD_TILES) */
+  int64_t reduce_count; /* SHARD_BLOCKS: doubles each rank receives from polya_reduce_G in
+                           the PAIR_TILES layout = ceil(npairs*Ntil^2 / nranks); the partial-G
+                           buffer holds nranks*reduce_count doubles (zero padding at the end) */
 } polya_dims;
 
 /* Output layouts of the Schur complement G (symmetric K x K):
@@ -141,9 +156,12 @@ polya_status polya_adjoint(polya_ctx* ctx, const double* X_dev, double* y_dev, v
  *   G_{ij} = sum_b tr(F_i^b Z_b^{-1} F_j^b X_b)
  * X_dev, Zinv_dev: double[nblocks][n][n]; both triangles are read and the
  * expansion assumes exact symmetry (callers symmetrise).  G_dev per layout.
- * This rank computes its work items [item0, item1) (output-tile sharding: inputs
- * replicated on every rank, no inter-GPU traffic).  Uses the rank-structured
- * expansion of DESIGN.md ("4-term raw GEMM + fold"), never the dense B_i.       */
+ * SHARD_TILES: this rank computes its work items [item0, item1) completely (inputs
+ * replicated on every rank, no inter-GPU traffic).  SHARD_BLOCKS: this rank computes
+ * every entry of the partial sum over its blocks [b0, b1) (to be summed by
+ * polya_reduce_G); X_dev / Zinv_dev still hold all blocks, only [b0, b1) are read by
+ * the assembly.  Uses the rank-structured expansion of DESIGN.md ("4-term raw GEMM +
+ * fold"), never the dense B_i.                                                   */
 polya_status polya_schur(polya_ctx* ctx, const double* X_dev, const double* Zinv_dev,
                          double* G_dev, int layout, void* stream);
 
@@ -169,6 +187,22 @@ polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, polya_ipm_stats
  * Q, R; kernel K3) and of the assembly kernel K4. */
 polya_status polya_set_timing(polya_ctx* ctx, int enable);
 polya_status polya_get_timing(polya_ctx* ctx, float* ms_pre, float* ms_assemble);
+
+/* Multi-GPU combine of the block-sharded Schur complement (SHARD_BLOCKS; PAPER.md:749,
+ * 755-778: the root's gather of the workers' partial sums, here one NCCL collective over
+ * NVLink).  polya_nccl_unique_id (rank 0) fills a 128-byte id that the caller distributes;
+ * polya_nccl_init (every rank, collectively) creates the context's communicator with
+ * cfg.rank / cfg.nranks on the context's device.
+ * polya_reduce_G sums the ranks' partial G^(r) on `stream`:
+ *   layout PAIR_TILES: ncclReduceScatter of the flattened tile buffer Gpart_dev
+ *     (nranks*reduce_count doubles, as written by polya_schur + zero padding) into
+ *     Grecv_dev (reduce_count doubles) = elements [rank*reduce_count, (rank+1)*reduce_count)
+ *     of the summed tiles: a contiguous row-panel range, ready for a distributed factorisation;
+ *   layout FULL: ncclAllReduce of the K x K matrix (Grecv_dev may equal Gpart_dev).
+ * Errors: EINVAL (not SHARD_BLOCKS, null pointers), ENCCL (no communicator, NCCL failure). */
+polya_status polya_nccl_unique_id(char out_id[128]);
+polya_status polya_nccl_init(polya_ctx* ctx, const char id[128]);
+polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart_dev, double* Grecv_dev, int layout, void* stream);
 
 /* Surfaces asynchronous errors (device synchronise + last-error check). */
 polya_status polya_sync(polya_ctx* ctx);

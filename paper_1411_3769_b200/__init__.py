@@ -11,15 +11,17 @@ import os
 
 import numpy as np
 
-__all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "EXPORTS", "LIB_PATH"]
+__all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "SHARD_TILES", "SHARD_BLOCKS", "EXPORTS",
+           "LIB_PATH", "plan", "nccl_unique_id"]
 
 # POLYA_LIB overrides the library path (timing-experiment variants built by tools/schur_exp.py)
 LIB_PATH = os.environ.get("POLYA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
 G_FULL, G_PAIR_TILES = 0, 1
+SHARD_TILES, SHARD_BLOCKS = 0, 1
 EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents", "polya_get_beta", "polya_get_H",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
-           "polya_get_timing"]
+           "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G"]
 
 
 class PolyaError(RuntimeError):
@@ -29,13 +31,14 @@ class PolyaError(RuntimeError):
 class _Config(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("l", ctypes.c_int32), ("dp", ctypes.c_int32), ("da", ctypes.c_int32),
                 ("d1", ctypes.c_int32), ("d2", ctypes.c_int32), ("delta", ctypes.c_double),
-                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("shard", ctypes.c_int32)]
 
 
 class _Dims(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("L0", "L", "M", "nblocks", "Ntil", "K", "nnz_beta", "nnz_H",
                                               "npairs", "pair0", "pair1", "item0", "item1")] + \
-               [("useful_flops_schur", ctypes.c_double), ("tiles_bytes", ctypes.c_int64)]
+               [("useful_flops_schur", ctypes.c_double), ("tiles_bytes", ctypes.c_int64), ("b0", ctypes.c_int64),
+                ("b1", ctypes.c_int64), ("reduce_count", ctypes.c_int64)]
 
 
 class _IpmState(ctypes.Structure):
@@ -75,6 +78,9 @@ def lib():
     L.polya_sync.argtypes = [vp]
     L.polya_set_timing.argtypes = [vp, ctypes.c_int]
     L.polya_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
+    L.polya_nccl_unique_id.argtypes = [vp]
+    L.polya_nccl_init.argtypes = [vp, vp]
+    L.polya_reduce_G.argtypes = [vp, vp, vp, ctypes.c_int, vp]
     L.polya_strerror.argtypes = [ctypes.c_int]
     L.polya_strerror.restype = ctypes.c_char_p
     L.polya_last_error.argtypes = [vp]
@@ -91,14 +97,23 @@ def lib():
     return L
 
 
-def plan(n, l, dp, d1, d2, da=1, delta=1e-3, rank=0, nranks=1):
-    """polya_plan: host-only dims and this rank's share of the Schur work items (no GPU)."""
-    cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks)
+def plan(n, l, dp, d1, d2, da=1, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES):
+    """polya_plan: host-only dims and this rank's share of the Schur work (no GPU)."""
+    cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks, shard)
     d = _Dims()
     st = lib().polya_plan(ctypes.byref(cfg), ctypes.byref(d))
     if st != 0:
         raise PolyaError(f"polya_plan: {lib().polya_strerror(st).decode()}")
     return {k: getattr(d, k) for k, _ in _Dims._fields_}
+
+
+def nccl_unique_id():
+    """polya_nccl_unique_id (rank 0): 128 opaque bytes the caller distributes to every rank."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().polya_nccl_unique_id(buf)
+    if st != 0:
+        raise PolyaError(f"polya_nccl_unique_id: {lib().polya_strerror(st).decode()}")
+    return bytes(buf.raw)
 
 
 def _stream_ptr(stream=None):
@@ -122,17 +137,17 @@ class Polya:
     """One context = one rank / GPU (``polya_setup``).  ``A`` is the host array
     double[f(l,da)][n][n] of A(alpha)'s coefficients in W_da order."""
 
-    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1):
+    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES):
         L = lib()
         A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
-        cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks)
+        cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks, shard)
         h = ctypes.c_void_p()
         st = L.polya_setup(ctypes.byref(cfg), A.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h))
         if st != 0:
             raise PolyaError(f"polya_setup: {L.polya_strerror(st).decode()}")
         self._h = h
         self.n, self.l, self.dp, self.da, self.d1, self.d2 = n, l, dp, da, d1, d2
-        self.delta, self.rank, self.nranks = delta, rank, nranks
+        self.delta, self.rank, self.nranks, self.shard = delta, rank, nranks, shard
         d = _Dims()
         self._check(L.polya_dims_get(self._h, ctypes.byref(d)), "polya_dims_get")
         self.dims = {k: getattr(d, k) for k, _ in _Dims._fields_}
@@ -193,6 +208,8 @@ class Polya:
         if G is None:
             if layout == G_FULL:
                 G = torch.zeros((self.K, self.K), dtype=torch.float64, device=X.device)
+            elif self.shard == SHARD_BLOCKS:   # flat partial-G buffer: all pair tiles + zero padding
+                G = torch.zeros(self.nranks * self.dims["reduce_count"], dtype=torch.float64, device=X.device)
             else:
                 npl = self.dims["pair1"] - self.dims["pair0"]
                 G = torch.zeros((npl, self.Ntil, self.Ntil), dtype=torch.float64, device=X.device)
@@ -208,6 +225,22 @@ class Polya:
         self._check(lib().polya_ipm_step(self._h, ctypes.byref(st), ctypes.byref(stats), _stream_ptr(stream)),
                     "polya_ipm_step")
         return {k: getattr(stats, k) for k, _ in _IpmStats._fields_}
+
+    def nccl_init(self, uid):
+        """polya_nccl_init: collective over the nranks contexts (SHARD_BLOCKS combine)."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        self._check(lib().polya_nccl_init(self._h, buf), "polya_nccl_init")
+
+    def reduce_G(self, Gpart, out=None, layout=G_PAIR_TILES, stream=None):
+        """polya_reduce_G: sum of the ranks' partial G (ReduceScatter of the pair tiles, or AllReduce
+        of the FULL matrix)."""
+        import torch
+        if out is None:
+            out = (torch.empty(self.dims["reduce_count"], dtype=torch.float64, device=Gpart.device)
+                   if layout == G_PAIR_TILES else Gpart)
+        self._check(lib().polya_reduce_G(self._h, _dev_ptr(Gpart, None, "Gpart"), _dev_ptr(out, None, "Grecv"), layout,
+                                         _stream_ptr(stream)), "polya_reduce_G")
+        return out
 
     def set_timing(self, on=True):
         self._check(lib().polya_set_timing(self._h, int(bool(on))), "polya_set_timing")

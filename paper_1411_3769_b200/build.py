@@ -8,9 +8,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpolya.so")
-SOURCES = ["polya_host.cpp", "kernels.cu", "schur.cu", "ipm.cu"]
+SOURCES = ["polya_host.cpp", "kernels.cu", "schur.cu", "ipm.cu", "combine.cpp"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-lcusolver", "-lcublas"]
+         "-Xcompiler", "-fPIC", "-shared", "-lcusolver", "-lcublas", "-lnccl"]
 
 
 def _stale() -> bool:

@@ -183,6 +183,34 @@ void build(Ctx& c, const double* A_host, bool device = true) {
   }
   const int64_t nnzH = (int64_t)c.Hh.size();
 
+  // ---- block partition (SHARD_BLOCKS): contiguous cost-balanced ranges [b0, b1) -------------------
+  // A block's share of the Schur work is sum over its active (h, h') pairs of n^4 per raw term:
+  // nu_j^2 for a P-block, 4 mu_m^2 for a Lyapunov block; ties go to the lower index.
+  c.b0 = 0;
+  c.b1 = c.nb;
+  if (g.shard == POLYA_SHARD_BLOCKS) {
+    std::vector<double> bc(c.nb + 1, 0.0);
+    for (int64_t j = 0; j < c.L; ++j) {
+      int64_t nu = 0;
+      for (int64_t h = 0; h < c.L0; ++h) nu += c.beta[h * c.L + j] != 0;
+      bc[j + 1] = bc[j] + (double)(nu * nu);
+    }
+    for (int64_t m = 0; m < c.M; ++m) {
+      int64_t mu = 0;
+      for (int64_t h = 0; h < c.L0; ++h) mu += c.Hidx[h * c.M + m] >= 0;
+      bc[c.L + m + 1] = bc[c.L + m] + 4.0 * (double)(mu * mu);
+    }
+    auto at = [&](int64_t r) -> int64_t {
+      if (r <= 0) return 0;
+      if (r >= g.nranks) return c.nb;
+      const double target = bc[c.nb] * (double)r / (double)g.nranks;
+      return std::lower_bound(bc.begin(), bc.end(), target) - bc.begin();
+    };
+    c.b0 = at(g.rank);
+    c.b1 = std::max(c.b0, at(g.rank + 1));
+  }
+  auto owned = [&](int64_t b) { return b >= c.b0 && b < c.b1; };
+
   // ---- pairs (h <= h'), their k-entries, work items, rank partition ---------------------------
   c.npairs = c.L0 * (c.L0 + 1) / 2;
   std::vector<int32_t> ph(c.npairs), ph2(c.npairs);
@@ -195,9 +223,9 @@ void build(Ctx& c, const double* A_host, bool device = true) {
         ph2[p] = (int32_t)h2;
         int64_t mu = 0, nu = 0;
         for (int64_t m = 0; m < c.M; ++m)
-          if (c.Hidx[h * c.M + m] >= 0 && c.Hidx[h2 * c.M + m] >= 0) ++mu;
+          if (owned(c.L + m) && c.Hidx[h * c.M + m] >= 0 && c.Hidx[h2 * c.M + m] >= 0) ++mu;
         for (int64_t j = 0; j < c.L; ++j)
-          if (c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) ++nu;
+          if (owned(j) && c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) ++nu;
         pMu[p] = mu;
         pK[p] = 4 * mu + nu;                        // K_pair = 4 mu_hh' + nu_hh' (algorithmic)
         pKpad[p] = std::max<int64_t>(kKStage, (pK[p] + kKStage - 1) / kKStage * kKStage);  // whole stages, >= 1
@@ -227,6 +255,10 @@ void build(Ctx& c, const double* A_host, bool device = true) {
   c.item1 = item_at_cost(total_cost * (g.rank + 1) / g.nranks);
   if (g.rank == g.nranks - 1) c.item1 = c.items_total;
   if (g.rank == 0) c.item0 = 0;
+  if (g.shard == POLYA_SHARD_BLOCKS) {  // every rank assembles all entries of its partial sum
+    c.item0 = 0;
+    c.item1 = c.items_total;
+  }
   c.pair0 = c.pair1 = 0;
   if (c.item1 > c.item0) {
     c.pair0 = std::upper_bound(c.pair_item_global.begin(), c.pair_item_global.end(), c.item0) -
@@ -290,6 +322,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
     // U_t = H_t X_{L+m}, V_t = H_t W_{L+m}, and their transposes X H_t^T, W H_t^T   (a7)
     for (int64_t t = 0; t < nnzH; ++t) {
       int32_t b = (int32_t)(c.L + c.Hm[t]);
+      if (!owned(b)) continue;   // SHARD_BLOCKS: only this rank's Lyapunov blocks enter its partial G
       it.push_back({(int32_t)(c.id_U + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
       tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_X + b), 0, 0, 1.0});
       it.push_back({(int32_t)(c.id_V + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
@@ -342,7 +375,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
       qh2.push_back((int32_t)h2);
       for (int64_t m = 0; m < c.M; ++m) {
         int32_t th = c.Hidx[h * c.M + m], th2 = c.Hidx[h2 * c.M + m];
-        if (th < 0 || th2 < 0) continue;
+        if (th < 0 || th2 < 0 || !owned(c.L + m)) continue;
         const int32_t b = (int32_t)(c.L + m);
         const int32_t idQ = (int32_t)(c.id_Q + q), idR = (int32_t)(c.id_R + q);
         // Q_{hh'} = U_h H_{h'}^T,  R_{h'h} = V_{h'} H_h^T
@@ -360,7 +393,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
       }
       for (int64_t j = 0; j < c.L; ++j) {
         int64_t b1 = c.beta[h * c.L + j], b2 = c.beta[h2 * c.L + j];
-        if (!b1 || !b2) continue;
+        if (!b1 || !b2 || !owned(j)) continue;
         // P-block term beta_hj beta_h'j X_j (x) W_j as (beta_hj X_j) (x) (beta_h'j W_j)
         kL.push_back((int32_t)(c.id_Xb + bidx[h * c.L + j])); kR.push_back((int32_t)(c.id_Wb + bidx[h2 * c.L + j]));
         kf.push_back(0); ks.push_back(1.0);
@@ -453,7 +486,7 @@ extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_hos
   if (!cfg || !A_host) return POLYA_EINVAL;
   const polya_config& g = *cfg;
   if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
-      g.rank < 0 || g.rank >= g.nranks)
+      g.rank < 0 || g.rank >= g.nranks || (g.shard != POLYA_SHARD_TILES && g.shard != POLYA_SHARD_BLOCKS))
     return POLYA_EINVAL;
   polya_ctx* ctx = new (std::nothrow) polya_ctx();
   if (!ctx) return POLYA_ENOMEM;
@@ -482,13 +515,17 @@ static void fill_dims(const Ctx& c, polya_dims* o) {
   o->npairs = c.npairs; o->pair0 = c.pair0; o->pair1 = c.pair1; o->item0 = c.item0; o->item1 = c.item1;
   o->useful_flops_schur = c.useful_flops_rank;
   o->tiles_bytes = c.npairs_local * c.Ntil * c.Ntil * (int64_t)sizeof(double);
+  o->b0 = c.b0;
+  o->b1 = c.b1;
+  const int64_t tot = c.npairs * c.Ntil * c.Ntil;
+  o->reduce_count = c.cfg.shard == POLYA_SHARD_BLOCKS ? (tot + c.cfg.nranks - 1) / c.cfg.nranks : 0;
 }
 
 extern "C" polya_status polya_plan(const polya_config* cfg, polya_dims* out) {
   if (!cfg || !out) return POLYA_EINVAL;
   const polya_config& g = *cfg;
   if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
-      g.rank < 0 || g.rank >= g.nranks)
+      g.rank < 0 || g.rank >= g.nranks || (g.shard != POLYA_SHARD_TILES && g.shard != POLYA_SHARD_BLOCKS))
     return POLYA_EINVAL;
   try {
     Ctx c;
@@ -657,10 +694,12 @@ extern "C" const char* polya_last_error(const polya_ctx* ctx) { return ctx ? ctx
 extern "C" int64_t polya_launch_count(const polya_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
 void polya_ipm_free(polya::Ctx& c);  // ipm.cu
+namespace polya { void nccl_free(Ctx& c); }  // combine.cpp
 
 extern "C" void polya_destroy(polya_ctx* ctx) {
   if (!ctx) return;
   polya_ipm_free(ctx->c);
+  nccl_free(ctx->c);
   for (auto& e : ctx->c.ev)
     if (e) cudaEventDestroy(e);
   free_ctx(ctx->c);

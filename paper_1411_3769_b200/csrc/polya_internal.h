@@ -58,6 +58,8 @@ struct Ctx {
   // pairs and work items
   int64_t npairs = 0, pair0 = 0, pair1 = 0;
   int64_t items_total = 0, item0 = 0, item1 = 0;
+  int64_t b0 = 0, b1 = 0;  // this rank's Polya blocks (SHARD_BLOCKS; all blocks otherwise)
+  void* nccl = nullptr;    // ncclComm_t of polya_nccl_init (SHARD_BLOCKS combine)
   std::vector<int64_t> pair_item_global;  // [npairs + 1]
   double useful_flops_total = 0, useful_flops_rank = 0;
   // arena (np x np matrices)

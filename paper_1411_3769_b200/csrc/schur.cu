@@ -196,6 +196,105 @@ __device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
   return v;
 }
 
+// One orientation of an item on the consumer warps: the raw 64x64 sub-block
+// Raw[(x,y),(z,w)] = sum_k L_k[x,y] R_k[z,w] (x in cX, y in cY, z in cZ, w in cW) over the
+// item's nstage ring stages, then folded into Gs.  Warp (xw, zw) owns x in xw..xw+3 and
+// z in zw..zw+3.  MI = 4: M-tile i is x = xw+i with rows y = 0..7; MI = 2 (ragged y chunk,
+// <= 4 valid rows): M-tile i packs x = xw+2i+(g>>2) with y = g&3.  NJ likewise for (z, w) on the
+// N side, where the accumulator column 2t+e is w = 2t+e (NJ = 4) or z = zw+2j+(t>>1),
+// w = 2(t&1)+e (NJ = 2).
+template <int MI, int NJ>
+__device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
+                                       uint64_t* empty, uint32_t& cnt, int nstage, int o, int cX, int cZ,
+                                       bool first) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int xw = 4 * (warp >> 1), zw = 4 * (warp & 1);
+  const int n = p.n;
+  const int nvx = min(Q, n - cX * Q), nvz = min(Q, n - cZ * Q);
+  // a warp whose x- or z-tiles all lie past a ragged chunk's end only multiplies zeros: skip
+  const bool active = ((SCHUR_EXP & 8) != 0) || ((xw < nvx) && (zw < nvz));   // bit 8: no ragged skip
+  constexpr int AST = MI == 4 ? Q : 2 * Q, BST = NJ == 4 ? Q : 2 * Q;   // fragment strides per tile
+  const int aoff = xw * Q + (MI == 4 ? g : (g >> 2) * Q + (g & 3));
+  const int boff = zw * Q + (NJ == 4 ? g : (g >> 2) * Q + (g & 3));
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int s = 0; s < nstage; ++s) {
+    const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+    mbar_wait(full + slot, ph);
+    if (active) {
+      const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
+      const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
+#pragma unroll
+      for (int k4 = 0; k4 < 2; ++k4) {
+        double a[MI], b[NJ];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[i] = fA[k4 * 4 * KS + i * AST];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) b[j] = fB[k4 * 4 * KS + j * BST];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + slot);
+    ++cnt;
+  }
+  if (SCHUR_EXP & 2) {   // timing experiment: no fold, no epilogue (a never-taken sink keeps the DMMAs)
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) sum += acc[i][j][0] * acc[i][j][1];
+    if (sum == 1.2345e-300) p.G[tid] = sum;
+    return;
+  }
+  consumer_sync();   // the previous fold / the previous item's epilogue is done with Gs
+  // fold: acc[i][j][e] = Raw(x, y, z, w) -> Gs[(a,b,c,d)(o)], gs = Ta(a)^Tb(b)^Tc(c)^d split into
+  // per-coordinate terms: x -> (o&2 ? Ta : Tb), w -> (o&2 ? Tb : Ta), y -> (o&1 ? id : Tc),
+  // z -> (o&1 ? Tc : id)   (o0: (a,b,c,d) = (w,x,y,z), o1: (w,x,z,y), o2: (x,w,y,z), o3: (x,w,z,y))
+  int bx[MI], bz[NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int x = MI == 4 ? xw + i : xw + 2 * i + (g >> 2);
+    const int y = MI == 4 ? g : (g & 3);
+    bx[i] = ((o & 2) ? Ta(x) : Tb(x)) ^ ((o & 1) ? y : Tc(y));
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int z = NJ == 4 ? zw + j : zw + 2 * j + (t >> 1);
+      const int w = NJ == 4 ? 2 * t + e : 2 * (t & 1) + e;
+      bz[j][e] = ((o & 1) ? Tc(z) : z) ^ ((o & 2) ? Tb(w) : Ta(w));
+    }
+  if (first) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Gs[bx[i] ^ bz[j][e]] = acc[i][j][e];
+  } else {
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {  // 2*NJ independent read-modify-writes at a time
+      double old[NJ][2];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) old[j][e] = Gs[bx[i] ^ bz[j][e]];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Gs[bx[i] ^ bz[j][e]] = old[j][e] + acc[i][j][e];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   extern __shared__ __align__(16) double smem[];
   double* Gs = smem + NSTAGE * STAGE;
@@ -306,7 +405,6 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   }
 
   // ===== consumer warps: DMMA on ring stages, fold into Gs, epilogue ==========================
-  const int xw = 4 * (warp >> 1), zw = 4 * (warp & 1);  // warp's 4 x-tiles and 4 z-tiles
   uint32_t cnt = 0;
   for (;;) {
     {  // the next ring stage is the first stage of the next item (or the end sentinel)
@@ -322,79 +420,14 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
       if ((o & 2) && dS) continue;
       int cX, cY, cZ, cW;
       roles(o, it, cX, cY, cZ, cW);
-      const int nvx = min(Q, n - cX * Q), nvz = min(Q, n - cZ * Q);
-      // a warp whose x- or z-tiles all lie past a ragged chunk's end only multiplies zeros: skip
-      const bool active = ((SCHUR_EXP & 8) != 0) || ((xw < nvx) && (zw < nvz));   // bit 8: no ragged skip
-      double acc[4][4][2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      for (int s = 0; s < it.nstage; ++s) {
-        const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
-        mbar_wait(full + slot, ph);
-        if (active) {
-          const double* fA = smem + slot * STAGE + t * KS + xw * Q + g;   // A[y=g][k=t] of x-tile xw
-          const double* fB = fA + KB * KS + (zw - xw) * Q;                // B[k=t][w=g] of z-tile zw
-#pragma unroll
-          for (int k4 = 0; k4 < 2; ++k4) {
-            double a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = fA[k4 * 4 * KS + i * Q];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = fB[k4 * 4 * KS + j * Q];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + slot);
-        ++cnt;
-      }
-      if (SCHUR_EXP & 2) {   // timing experiment: no fold, no epilogue (a never-taken sink keeps the DMMAs)
-        double sum = 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) sum += acc[i][j][0] * acc[i][j][1];
-        if (sum == 1.2345e-300) p.G[tid] = sum;
-        first = false;
-        continue;
-      }
-      consumer_sync();   // the previous fold / the previous item's epilogue is done with Gs
-      // fold: thread holds Raw(x = xw+i, y = g, z = zw+j, w = 2t+e) -> Gs[(a,b,c,d)(o)]
-      {
-        int bx[4], bz[4], be[2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) bx[i] = (o & 2) ? Ta(xw + i) : Tb(xw + i);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bz[j] = (o & 1) ? Tc(zw + j) : (zw + j);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) be[e] = ((o & 2) ? Tb(2 * t + e) : Ta(2 * t + e)) ^ ((o & 1) ? g : Tc(g));
-        if (first) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) Gs[be[e] ^ bx[i] ^ bz[j]] = acc[i][j][e];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {  // 8 independent read-modify-writes at a time
-            double old[4][2];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) old[j][e] = Gs[be[e] ^ bx[i] ^ bz[j]];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) Gs[be[e] ^ bx[i] ^ bz[j]] = old[j][e] + acc[i][j][e];
-          }
-        }
-      }
+      // ragged chunk (n not a multiple of 8) in an MMA dimension (y: M rows, w: N columns): with
+      // <= 4 valid indices, pack two x (or z) values into one 8-row MMA tile instead of
+      // multiplying 8-row tiles that are half zeros
+      const bool rY = (n - cY * Q) <= 4, rW = (n - cW * Q) <= 4;
+      if (!rY && !rW) orient<4, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
+      else if (rY && !rW) orient<2, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
+      else if (!rY && rW) orient<4, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
+      else orient<2, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
       first = false;
     }
     if (SCHUR_EXP & 3) continue;   // timing experiment: no epilogue
@@ -433,22 +466,46 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
     const int64_t rowbase = (int64_t)it.h * p.Ntil, colbase = (int64_t)it.h2 * p.Ntil;
     double* tile = p.G + (int64_t)it.pl * p.Ntil * p.Ntil;
     const int4 none = make_int4(-1, 0, 0, 0);
-    {  // pass 0: direct entries G[s][t], lanes along the columns t
+    {  // pass 0: direct entries G[s][t], lanes along the columns t; 4 rows per warp in flight
       const int4 cA = lane < nc ? s_ct[lane] : none, cB = lane + 32 < nc ? s_ct[lane + 32] : none;
-      for (int r = warp; r < nr; r += NCW) {
-        const int4 rw = s_rt[r];
-        double* dst = fullG ? p.G + (rowbase + rw.x) * p.K + colbase : tile + (int64_t)rw.x * p.Ntil;
-        if (cA.x >= 0 && !(same_cls && rw.x > cA.x)) dst[cA.x] = gval(Gs, rw, cA);
-        if (cB.x >= 0 && !(same_cls && rw.x > cB.x)) dst[cB.x] = gval(Gs, rw, cB);
+      for (int r0 = warp; r0 < nr; r0 += 4 * NCW) {
+        int4 rw[4];
+        double vA[4], vB[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rw[u] = r0 + u * NCW < nr ? s_rt[r0 + u * NCW] : none;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          vA[u] = (rw[u].x >= 0 && cA.x >= 0) ? gval(Gs, rw[u], cA) : 0.0;
+          vB[u] = (rw[u].x >= 0 && cB.x >= 0) ? gval(Gs, rw[u], cB) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (rw[u].x < 0) continue;
+          double* dst = fullG ? p.G + (rowbase + rw[u].x) * p.K + colbase : tile + (int64_t)rw[u].x * p.Ntil;
+          if (cA.x >= 0 && !(same_cls && rw[u].x > cA.x)) dst[cA.x] = vA[u];
+          if (cB.x >= 0 && !(same_cls && rw[u].x > cB.x)) dst[cB.x] = vB[u];
+        }
       }
     }
     if (fullG || diag_pair) {  // pass 1: mirror entries G[t][s], lanes along the rows s
       const int4 rA = lane < nr ? s_rt[lane] : none, rB = lane + 32 < nr ? s_rt[lane + 32] : none;
-      for (int c = warp; c < nc; c += NCW) {
-        const int4 cl = s_ct[c];
-        double* dst = fullG ? p.G + (colbase + cl.x) * p.K + rowbase : tile + (int64_t)cl.x * p.Ntil;
-        if (rA.x >= 0 && !(same_cls && rA.x > cl.x)) dst[rA.x] = gval(Gs, rA, cl);
-        if (rB.x >= 0 && !(same_cls && rB.x > cl.x)) dst[rB.x] = gval(Gs, rB, cl);
+      for (int c0 = warp; c0 < nc; c0 += 4 * NCW) {
+        int4 cl[4];
+        double vA[4], vB[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cl[u] = c0 + u * NCW < nc ? s_ct[c0 + u * NCW] : none;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          vA[u] = (cl[u].x >= 0 && rA.x >= 0) ? gval(Gs, rA, cl[u]) : 0.0;
+          vB[u] = (cl[u].x >= 0 && rB.x >= 0) ? gval(Gs, rB, cl[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (cl[u].x < 0) continue;
+          double* dst = fullG ? p.G + (colbase + cl[u].x) * p.K + rowbase : tile + (int64_t)cl[u].x * p.Ntil;
+          if (rA.x >= 0 && !(same_cls && rA.x > cl[u].x)) dst[rA.x] = vA[u];
+          if (rB.x >= 0 && !(same_cls && rB.x > cl[u].x)) dst[rB.x] = vB[u];
+        }
       }
     }
   }

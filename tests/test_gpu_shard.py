@@ -1,0 +1,103 @@
+"""GPU tests of the block-sharded Schur complement (SHARD_BLOCKS: the paper's decentralised
+scheme) and its NCCL combine (polya_reduce_G).
+
+On one GPU the N ranks are N contexts (rank r of N) on the same device; each assembles its
+partial G^(r) over its Polya blocks [b0, b1), and sum_r G^(r) must equal the single-rank G
+(to 1e-12 relative: multi-GPU vs 1) and the oracle's literal G (1e-10).  The NCCL
+collective itself is exercised with a one-rank communicator (ReduceScatter / AllReduce of one
+rank is the identity), since only one GPU is available; the N > 1 host logic is covered by
+tests/test_multirank_cpu.py over gloo."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import sdp as osdp
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_1411_3769_b200 as pb
+    pb.lib()
+    assert torch.cuda.is_available()
+    return pb
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _inputs(cfg, seed=0):
+    rng = np.random.default_rng(seed)
+    A = synth.vertex_matrices(cfg, rng)
+    from math import comb
+    nb = comb(cfg.l + cfg.dp + cfg.d1 - 1, cfg.l - 1) + comb(cfg.l + cfg.dp + cfg.d2, cfg.l - 1)
+    X, W = synth.spd_blocks(cfg.n, nb, rng)
+    return A, X, W
+
+
+CASES = [(synth.CONFIGS[2], 3), (synth.small_config(12, 3, 2, 1, 2), 2), (synth.small_config(20, 2, 2, 1, 1), 5),
+         (synth.CONFIGS[3], 4)]
+
+
+@pytest.mark.parametrize("cfg,world", CASES, ids=lambda v: getattr(v, "name", str(v)))
+def test_block_partials_sum_to_G(pb, cfg, world):
+    A, X, W = _inputs(cfg)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    ref = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A)
+    G_tiles = ref.schur(Xd, Wd, layout=pb.G_PAIR_TILES).cpu().numpy().ravel()
+    G_full = ref.schur(Xd, Wd, layout=pb.G_FULL).cpu().numpy()
+    ref.close()
+    acc_t = np.zeros_like(G_tiles)
+    acc_f = np.zeros_like(G_full)
+    flops = 0.0
+    for r in range(world):
+        ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=world, shard=pb.SHARD_BLOCKS)
+        part = ctx.schur(Xd, Wd, layout=pb.G_PAIR_TILES).cpu().numpy()
+        assert part.size == world * ctx.dims["reduce_count"]
+        assert not np.any(part[G_tiles.size:])          # padding stays zero
+        acc_t += part[:G_tiles.size]
+        acc_f += ctx.schur(Xd, Wd, layout=pb.G_FULL).cpu().numpy()
+        flops += ctx.dims["useful_flops_schur"]
+        ctx.close()
+    assert _rel(acc_t, G_tiles) <= 1e-12
+    assert _rel(acc_f, G_full) <= 1e-12
+    if cfg.n <= 12:
+        P = osdp.build_problem(A, cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)
+        assert _rel(acc_f, osdp.schur_literal(P, X, W)) <= 1e-10
+
+
+def test_nccl_one_rank_combine(pb):
+    cfg = synth.CONFIGS[2]
+    A, X, W = _inputs(cfg)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=0, nranks=1, shard=pb.SHARD_BLOCKS)
+    ctx.nccl_init(pb.nccl_unique_id())
+    part = ctx.schur(Xd, Wd, layout=pb.G_PAIR_TILES)
+    out = ctx.reduce_G(part, layout=pb.G_PAIR_TILES)
+    torch.cuda.synchronize()
+    assert torch.equal(out, part[:out.numel()])
+    Gf = ctx.schur(Xd, Wd, layout=pb.G_FULL)
+    before = Gf.clone()
+    ctx.reduce_G(Gf, layout=pb.G_FULL)           # in-place AllReduce over one rank
+    torch.cuda.synchronize()
+    assert torch.equal(Gf, before)
+    P = osdp.build_problem(A, cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)
+    assert _rel(Gf.cpu().numpy(), osdp.schur_literal(P, X, W)) <= 1e-10
+    ctx.close()
+
+
+def test_reduce_without_nccl_or_tiles_mode_fails_loudly(pb):
+    cfg = synth.CONFIGS[1]
+    A, X, W = _inputs(cfg)
+    G = torch.zeros(16, dtype=torch.float64, device="cuda")
+    t = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A)
+    with pytest.raises(pb.PolyaError):
+        t.reduce_G(G, out=G)                         # SHARD_TILES: no combine step
+    b = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, shard=pb.SHARD_BLOCKS)
+    with pytest.raises(pb.PolyaError):
+        b.reduce_G(G, out=G)                         # no communicator yet
+    t.close()
+    b.close()

@@ -8,7 +8,11 @@ algorithmic FLOPs.  These tests check, across real processes over gloo:
   * the ranks' algorithmic FLOPs sum to W_G = n^4 (sum nu^2 + 4 sum mu^2), with nu, mu
     counted from the ORACLE's beta and H (independent of the library);
   * the cost balance is within 1 % at cfg 4 (5 % on tiny shapes with ~170 items);
-  * bench.py's max / sum reductions over the process group.
+  * bench.py's max / sum reductions over the process group;
+  * the block-sharded alternative (SHARD_BLOCKS, the paper's decentralised scheme): the ranks'
+    block ranges [b0, b1) tile [0, L+M) contiguously, every rank assembles all items, and the
+    ranks' FLOPs (each its blocks' share) sum to W_G with the heaviest rank within one block's
+    cost of the mean.
 """
 import os
 import socket
@@ -45,7 +49,13 @@ def _worker(rank, world, port, q):
         dist.all_gather(parts, t)
         fl = bench.reduce_over_ranks(d["useful_flops_schur"], "sum", "cpu", world)
         mx = bench.reduce_over_ranks(d["useful_flops_schur"], "max", "cpu", world)
-        out.append(([p.tolist() for p in parts], fl, mx))
+        db = pb.plan(*shape, rank=rank, nranks=world, shard=pb.SHARD_BLOCKS)
+        tb = torch.tensor([db["b0"], db["b1"], db["item0"], db["item1"]], dtype=torch.int64)
+        bparts = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(bparts, tb)
+        bfl = bench.reduce_over_ranks(db["useful_flops_schur"], "sum", "cpu", world)
+        bmx = bench.reduce_over_ranks(db["useful_flops_schur"], "max", "cpu", world)
+        out.append(([p.tolist() for p in parts], fl, mx, [p.tolist() for p in bparts], bfl, bmx))
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
@@ -62,6 +72,16 @@ def _wg_from_oracle(n, l, dp, d1, d2):
     return float(n) ** 4 * (float((nu ** 2).sum()) + 4.0 * float((mu ** 2).sum()))
 
 
+def _max_block_cost(n, l, dp, d1, d2):
+    from oracle import polya
+    beta = polya.beta_table(l, dp, d1)
+    A = np.random.default_rng(0).normal(size=(l, 2, 2))
+    H = polya.H_table(A, l, dp, d2)
+    nu = (beta != 0).sum(axis=0)
+    mu = np.array([sum(np.any(H[h, m] != 0) for h in range(H.shape[0])) for m in range(H.shape[1])])
+    return float(n) ** 4 * max(float((nu ** 2).max()), 4.0 * float((mu ** 2).max()))
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_multirank_plan_and_reductions_gloo(world):
     import paper_1411_3769_b200 as pb
@@ -76,7 +96,7 @@ def test_multirank_plan_and_reductions_gloo(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for shape, (parts, fl, mx) in zip(SHAPES, res):
+    for shape, (parts, fl, mx, bparts, bfl, bmx) in zip(SHAPES, res):
         total = pb.plan(*shape)["item1"]
         assert parts[0][0] == 0 and parts[-1][1] == total
         assert all(parts[r][1] == parts[r + 1][0] for r in range(world - 1))
@@ -84,3 +104,10 @@ def test_multirank_plan_and_reductions_gloo(world):
         assert abs(fl - wg) <= 1e-9 * wg
         # balance: item-granular, so coarse for tiny shapes (171 items) and tight for cfg 4 (414k)
         assert mx <= (1.01 if total > 100000 else 1.05) * wg / world
+        # block sharding: contiguous block ranges covering all blocks, all items on every rank
+        nb = pb.plan(*shape)["b1"]
+        assert bparts[0][0] == 0 and bparts[-1][1] == nb
+        assert all(bparts[r][1] == bparts[r + 1][0] for r in range(world - 1))
+        assert all(bp[2] == 0 and bp[3] == total for bp in bparts)
+        assert abs(bfl - wg) <= 1e-9 * wg
+        assert bmx <= wg / world + _max_block_cost(*shape)   # within one block's cost of the mean
