@@ -92,9 +92,25 @@ __device__ __forceinline__ int Tc(int c) {
   return (c1 << 4) ^ ((c & 1) << 3) ^ (e1 | ((e0 ^ e1) << 1) | (e0 << 2));
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+// Operand tiles are re-read by every item of a pair: keep them in L2 (evict_last), while the
+// 11+ GB of G streamed out per call is stored evict-first (st.global.cs) so it does not flush them.
+#ifndef SCHUR_L2HINTS
+#define SCHUR_L2HINTS 0   // measured: no gain (v13), kept as an experiment switch
+#endif
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, uint64_t pol) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+  if (SCHUR_L2HINTS)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "l"(pol));
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+}
+__device__ __forceinline__ void st_g(double* p, double v) {
+  if (SCHUR_L2HINTS) __stcs(p, v); else *p = v;
 }
 __device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -114,7 +130,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory"); }
+// Consumer phases (each fold of an orientation, each item's epilogue) are ordered by one mbarrier
+// with one arrival per consumer warp: a warp arrives when its part of a phase is done and waits
+// for the previous phase only right before it touches Gs again, so a warp that finishes a fold
+// early streams on into the next orientation's DMMAs instead of idling at a CTA barrier.
+__device__ __forceinline__ void phase_arrive(uint64_t* bar, uint32_t& nph) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+  ++nph;
+}
+__device__ __forceinline__ void phase_wait_prev(uint64_t* bar, uint32_t nph) {
+  if (nph > 0) mbar_wait(bar, (nph - 1) & 1);
+}
 
 struct ItemInfo {
   int pl, h, h2, sc, tc, ci, cj, ck, cl, nstage;
@@ -206,7 +233,7 @@ __device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
 template <int MI, int NJ>
 __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
                                        uint64_t* empty, uint32_t& cnt, int nstage, int o, int cX, int cZ,
-                                       bool first) {
+                                       bool first, uint64_t* pbar, uint32_t& nph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int xw = 4 * (warp >> 1), zw = 4 * (warp & 1);
   const int n = p.n;
@@ -253,7 +280,7 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
     if (sum == 1.2345e-300) p.G[tid] = sum;
     return;
   }
-  consumer_sync();   // the previous fold / the previous item's epilogue is done with Gs
+  phase_wait_prev(pbar, nph);   // the previous fold / the previous item's epilogue is done with Gs
   // fold: acc[i][j][e] = Raw(x, y, z, w) -> Gs[(a,b,c,d)(o)], gs = Ta(a)^Tb(b)^Tc(c)^d split into
   // per-coordinate terms: x -> (o&2 ? Ta : Tb), w -> (o&2 ? Tb : Ta), y -> (o&1 ? id : Tc),
   // z -> (o&1 ? Tc : id)   (o0: (a,b,c,d) = (w,x,y,z), o1: (w,x,z,y), o2: (x,w,y,z), o3: (x,w,z,y))
@@ -293,6 +320,7 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
         for (int e = 0; e < 2; ++e) Gs[bx[i] ^ bz[j][e]] = old[j][e] + acc[i][j][e];
     }
   }
+  phase_arrive(pbar, nph);
 }
 
 __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
@@ -301,8 +329,9 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   uint64_t* full = reinterpret_cast<uint64_t*>(Gs + Q * Q * Q * Q);   // stage landed (32 producer arrivals)
   uint64_t* empty = full + NSTAGE;                                      // stage consumed (NCW arrivals)
   __shared__ unsigned char s_diag[64][2];  // (lc, ld) of local pairs ordered by (ld-lc, lc)
-  __shared__ int4 s_rt[64], s_ct[64];      // epilogue tables of the item's valid row / column pairs
-  __shared__ int s_nrc[2];                 // their counts
+  __shared__ int4 s_rt[2][64], s_ct[2][64];   // epilogue tables of the item's valid row / column pairs
+  __shared__ int s_nrc[2][2];                  // their counts (double-buffered by item parity)
+  __shared__ uint64_t s_pbar;                  // consumer phase barrier (NCW arrivals per phase)
   __shared__ SlotInfo s_info[NSTAGE];      // item of the stage held by each ring slot (first stages)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -317,6 +346,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
       mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
       mbar_init(empty + i, NCW);
     }
+    mbar_init(&s_pbar, NCW);
   }
   __syncthreads();
   const int n = p.n, np = p.np;
@@ -328,6 +358,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   if (warp == NCW) {
     // ===== producer warp: 16-byte cp.async chunks (row sr, column pair sc2) of all 16 tiles ====
     const int sr = lane >> 2, sc2 = lane & 3;
+    const uint64_t pol = l2_evict_last_policy();
     uint32_t cnt = 0;
     unsigned long long got = 0;
     if (lane == 0) got = atomicAdd(p.counter, 1ULL);
@@ -379,8 +410,8 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
             const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, kk);
             const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, kk);
             if (!(SCHUR_EXP & 4)) {   // experiment bit 4: no operand loads (timing of the DMMA side only)
-              cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL);
-              cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR);
+              cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL, pol);
+              cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR, pol);
             }
           }
           cp_async_mbar_arrive(full + slot);
@@ -405,7 +436,8 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   }
 
   // ===== consumer warps: DMMA on ring stages, fold into Gs, epilogue ==========================
-  uint32_t cnt = 0;
+  uint32_t cnt = 0, nph = 0;
+  int icount = 0;
   for (;;) {
     {  // the next ring stage is the first stage of the next item (or the end sentinel)
       const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
@@ -414,33 +446,18 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
     const SlotInfo it = s_info[cnt % NSTAGE];
     if (it.item >= p.item1) break;
     const bool dS = (it.ci == it.cj), dT = (it.ck == it.cl);
-    bool first = true;
-    for (int o = 0; o < 4; ++o) {
-      if ((o & 1) && dT) continue;
-      if ((o & 2) && dS) continue;
-      int cX, cY, cZ, cW;
-      roles(o, it, cX, cY, cZ, cW);
-      // ragged chunk (n not a multiple of 8) in an MMA dimension (y: M rows, w: N columns): with
-      // <= 4 valid indices, pack two x (or z) values into one 8-row MMA tile instead of
-      // multiplying 8-row tiles that are half zeros
-      const bool rY = (n - cY * Q) <= 4, rW = (n - cW * Q) <= 4;
-      if (!rY && !rW) orient<4, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
-      else if (rY && !rW) orient<2, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
-      else if (!rY && rW) orient<4, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
-      else orient<2, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first);
-      first = false;
-    }
-    if (SCHUR_EXP & 3) continue;   // timing experiment: no epilogue
-    consumer_sync();     // all folds of the item are in Gs
-    // ---- epilogue: fold diagonal classes and write G ----------------------------------------
-    // Tables of the item's valid local pairs, compacted in diagonal order (consecutive entries
-    // have consecutive svec indices, so a warp's stores form contiguous runs): warp 0 the rows
-    // (a,b) of class (ci,cj), warp 1 the columns (c,d) of class (ck,cl).
-    if (warp < 2) {
+    const int tb = icount & 1;
+    ++icount;
+    // Tables of the item's valid local pairs (buffer tb: its previous user, item i-2, finished
+    // its epilogue before item i-1's first fold), compacted in diagonal order (consecutive
+    // entries have consecutive svec indices, so a warp's stores form contiguous runs): warp 0
+    // the rows (a,b) of class (ci,cj), warp 1 the columns (c,d) of class (ck,cl).  Published to
+    // the other warps by the fold-phase arrivals.
+    if (warp < 2 && !(SCHUR_EXP & 3)) {
       const bool rows = (warp == 0);
       const int c1 = rows ? it.ci : it.ck, c2 = rows ? it.cj : it.cl;
       const bool dg = rows ? dS : dT;
-      int4* tab = rows ? s_rt : s_ct;
+      int4* tab = rows ? s_rt[tb] : s_ct[tb];
       int base = 0;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -456,10 +473,28 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         }
         base += __popc(bal);
       }
-      if (lane == 0) s_nrc[warp] = base;
+      if (lane == 0) s_nrc[tb][warp] = base;
     }
-    consumer_sync();
-    const int nr = s_nrc[0], nc = s_nrc[1];
+    bool first = true;
+    for (int o = 0; o < 4; ++o) {
+      if ((o & 1) && dT) continue;
+      if ((o & 2) && dS) continue;
+      int cX, cY, cZ, cW;
+      roles(o, it, cX, cY, cZ, cW);
+      // ragged chunk (n not a multiple of 8) in an MMA dimension (y: M rows, w: N columns): with
+      // <= 4 valid indices, pack two x (or z) values into one 8-row MMA tile instead of
+      // multiplying 8-row tiles that are half zeros
+      const bool rY = (n - cY * Q) <= 4, rW = (n - cW * Q) <= 4;
+      if (!rY && !rW) orient<4, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
+      else if (rY && !rW) orient<2, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
+      else if (!rY && rW) orient<4, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
+      else orient<2, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
+      first = false;
+    }
+    if (SCHUR_EXP & 3) continue;   // timing experiment: no epilogue
+    phase_wait_prev(&s_pbar, nph);   // all folds of the item are in Gs (and its tables are written)
+    // ---- epilogue: fold diagonal classes and write G ----------------------------------------
+    const int nr = s_nrc[tb][0], nc = s_nrc[tb][1];
     const bool diag_pair = (it.h == it.h2);
     const bool same_cls = diag_pair && (it.sc == it.tc);
     const bool fullG = (p.layout == POLYA_G_FULL);
@@ -467,12 +502,12 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
     double* tile = p.G + (int64_t)it.pl * p.Ntil * p.Ntil;
     const int4 none = make_int4(-1, 0, 0, 0);
     {  // pass 0: direct entries G[s][t], lanes along the columns t; 4 rows per warp in flight
-      const int4 cA = lane < nc ? s_ct[lane] : none, cB = lane + 32 < nc ? s_ct[lane + 32] : none;
+      const int4 cA = lane < nc ? s_ct[tb][lane] : none, cB = lane + 32 < nc ? s_ct[tb][lane + 32] : none;
       for (int r0 = warp; r0 < nr; r0 += 4 * NCW) {
         int4 rw[4];
         double vA[4], vB[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) rw[u] = r0 + u * NCW < nr ? s_rt[r0 + u * NCW] : none;
+        for (int u = 0; u < 4; ++u) rw[u] = r0 + u * NCW < nr ? s_rt[tb][r0 + u * NCW] : none;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           vA[u] = (rw[u].x >= 0 && cA.x >= 0) ? gval(Gs, rw[u], cA) : 0.0;
@@ -482,18 +517,18 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         for (int u = 0; u < 4; ++u) {
           if (rw[u].x < 0) continue;
           double* dst = fullG ? p.G + (rowbase + rw[u].x) * p.K + colbase : tile + (int64_t)rw[u].x * p.Ntil;
-          if (cA.x >= 0 && !(same_cls && rw[u].x > cA.x)) dst[cA.x] = vA[u];
-          if (cB.x >= 0 && !(same_cls && rw[u].x > cB.x)) dst[cB.x] = vB[u];
+          if (cA.x >= 0 && !(same_cls && rw[u].x > cA.x)) st_g(dst + cA.x, vA[u]);
+          if (cB.x >= 0 && !(same_cls && rw[u].x > cB.x)) st_g(dst + cB.x, vB[u]);
         }
       }
     }
     if (fullG || diag_pair) {  // pass 1: mirror entries G[t][s], lanes along the rows s
-      const int4 rA = lane < nr ? s_rt[lane] : none, rB = lane + 32 < nr ? s_rt[lane + 32] : none;
+      const int4 rA = lane < nr ? s_rt[tb][lane] : none, rB = lane + 32 < nr ? s_rt[tb][lane + 32] : none;
       for (int c0 = warp; c0 < nc; c0 += 4 * NCW) {
         int4 cl[4];
         double vA[4], vB[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cl[u] = c0 + u * NCW < nc ? s_ct[c0 + u * NCW] : none;
+        for (int u = 0; u < 4; ++u) cl[u] = c0 + u * NCW < nc ? s_ct[tb][c0 + u * NCW] : none;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           vA[u] = (cl[u].x >= 0 && rA.x >= 0) ? gval(Gs, rA, cl[u]) : 0.0;
@@ -503,11 +538,12 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         for (int u = 0; u < 4; ++u) {
           if (cl[u].x < 0) continue;
           double* dst = fullG ? p.G + (colbase + cl[u].x) * p.K + rowbase : tile + (int64_t)cl[u].x * p.Ntil;
-          if (rA.x >= 0 && !(same_cls && rA.x > cl[u].x)) dst[rA.x] = vA[u];
-          if (rB.x >= 0 && !(same_cls && rB.x > cl[u].x)) dst[rB.x] = vB[u];
+          if (rA.x >= 0 && !(same_cls && rA.x > cl[u].x)) st_g(dst + rA.x, vA[u]);
+          if (rB.x >= 0 && !(same_cls && rB.x > cl[u].x)) st_g(dst + rB.x, vB[u]);
         }
       }
     }
+    phase_arrive(&s_pbar, nph);   // this warp is done reading Gs for the item
   }
 }
 
