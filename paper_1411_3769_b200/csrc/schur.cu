@@ -94,6 +94,9 @@ __device__ __forceinline__ int Tc(int c) {
 
 // Operand tiles are re-read by every item of a pair: keep them in L2 (evict_last), while the
 // 11+ GB of G streamed out per call is stored evict-first (st.global.cs) so it does not flush them.
+#ifndef SCHUR_CA
+#define SCHUR_CA 0   // experiment: L1-allocating cp.async (.ca) instead of .cg
+#endif
 #ifndef SCHUR_L2HINTS
 #define SCHUR_L2HINTS 0   // measured: no gain (v13), kept as an experiment switch
 #endif
@@ -106,6 +109,8 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src,
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   if (SCHUR_L2HINTS)
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "l"(pol));
+  else if (SCHUR_CA)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
   else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
@@ -129,6 +134,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
           sptr(bar)),
       "r"(parity)
       : "memory");
+}
+#ifndef SCHUR_BULK
+#define SCHUR_BULK 0   // 1: operand rows by cp.async.bulk (measured: per-lane bulk copies serialise in the producer)
+#endif
+// 64-byte row copy global -> shared by the bulk-copy (TMA) engine, completing `bytes` of the
+// mbarrier's transaction count.
+__device__ __forceinline__ void bulk_row(void* smem_dst, const void* gmem_src, uint64_t* bar, unsigned bytes) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   sptr(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(sptr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(sptr(bar)),
+               "r"(bytes)
+               : "memory");
 }
 // Consumer phases (each fold of an orientation, each item's epilogue) are ordered by one mbarrier
 // with one arrival per consumer warp: a warp arrives when its part of a phase is done and waits
@@ -343,7 +364,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   }
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
+      mbar_init(full + i, SCHUR_BULK ? 1 : 33);   // lane 0's arrive(.expect_tx) (+ 32 cp.async completions)
       mbar_init(empty + i, NCW);
     }
     mbar_init(&s_pbar, NCW);
@@ -389,6 +410,10 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         roles(o, it, cX, cY, cZ, cW);
         const int offL = (cX * Q + sr) * np + cY * Q + 2 * sc2;
         const int offR = (cZ * Q + sr) * np + cW * Q + 2 * sc2;
+        // bulk mode: lane copies rows 4(lane&1) .. +3 of tile lane>>1 (tiles 0-7: L_k, 8-15: R_k)
+        const int btile = lane >> 1, brow = 4 * (lane & 1);
+        const int boff = btile < KB ? (cX * Q + brow) * np + cY * Q : (cZ * Q + brow) * np + cW * Q;
+        double* bdst0 = smem + (btile < KB ? btile * KS : KB * KS + (btile - KB) * KS) + brow * Q;
         int2 dcur = dfirst;
         for (int s = 0; s < it.nstage; ++s) {
           // descriptors of the next stage: the next k-block, or the first one again (the next
@@ -404,6 +429,21 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
             s_info[slot] = si;
           }
           first_stage = false;
+          if (SCHUR_BULK) {
+            const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, btile & (KB - 1));
+            const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, btile & (KB - 1));
+            if (lane == 0) mbar_arrive_expect_tx(full + slot, (SCHUR_EXP & 4) ? 0u : 2u * KB * Q * Q * 8u);   // releases s_info
+            __syncwarp();
+            if (!(SCHUR_EXP & 4)) {
+              const double* src = p.arena + (uint64_t)(btile < KB ? idL : idR) * p.ms32 + boff;
+              double* dst = bdst0 + slot * STAGE;
+#pragma unroll
+              for (int r = 0; r < 4; ++r) bulk_row(dst + r * Q, src + r * np, full + slot, Q * 8);
+            }
+            dcur = dnext;
+            ++cnt;
+            continue;
+          }
           double* T = smem + slot * STAGE + sr * Q + 2 * sc2;
 #pragma unroll
           for (int kk = 0; kk < KB; ++kk) {
@@ -428,7 +468,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
       const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
       mbar_wait(empty + slot, ph ^ 1);
       if (lane == 0) s_info[slot].item = p.item1;
-      cp_async_mbar_arrive(full + slot);
+      if (!SCHUR_BULK) cp_async_mbar_arrive(full + slot);
       if (lane == 0) mbar_arrive(full + slot);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
