@@ -15,12 +15,16 @@ DESIGN.md "Readings of the paper"):
                     (sum alpha)^d * P(alpha) and (sum alpha)^d * A(alpha) P(alpha)
                     (Eqs. LMI_1-LMI_4) plus the literal
                     recursions Eqs. (19)-(22) (PAPER.md:218-235), C by Eq. (27);
+                    homogenisation and the simplex maps g of
+                    Examples 1-2 (PAPER.md:1054-1057, reading R17);
 * ``sdp``        -- the basis E_k (Eqs. 4-5, reading R2), the V-map (Eq. 30),
                     dense F_i blocks (Eq. 31), B(X) and B^T(y) (Eqs. 14, 16),
                     and the Schur complement lambda_{k,l} = sum_b tr(B_k Z^-1 B_l X)
                     (Eq. T2, PAPER.md:743-747) by literal traces;
 * ``ipm``        -- one predictor-corrector iteration of Algorithm 2 on dense
-                    block matrices, readings R3-R6.
+                    block matrices (PAPER.md:565-597, 705-872), readings R3-R6;
+                    the iteration to the stopping rule and the
+                    grid-checked verdict (O8).
 
 Every function is pinned by ``tests/test_oracle_*.py`` against values the paper
 prints, closed forms, invariants and brute force.

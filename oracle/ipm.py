@@ -33,7 +33,7 @@ import numpy as np
 from . import sdp
 from .monomials import enumerate_W
 
-__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "grid_check"]
+__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "grid_check", "solve", "verdict"]
 
 
 def C_blocks(P):
@@ -117,9 +117,36 @@ def grid_check(P, y, samples=1000, seed=0):
     pts = [np.eye(P.l)[i] for i in range(P.l)]
     pts += [0.5 * (np.eye(P.l)[i] + np.eye(P.l)[j]) for i in range(P.l) for j in range(i + 1, P.l)]
     pts += list(rng.dirichlet(np.ones(P.l), size=samples))
+    Wa = enumerate_W(P.l, P.da)
     for al in pts:
         Pa = sum(math.prod(a ** e for a, e in zip(al, h)) * Ph[i] for i, h in enumerate(Wp))
-        Aa = sum(al[i] * P.A[i] for i in range(P.l))
+        Aa = sum(math.prod(a ** e for a, e in zip(al, lam)) * P.A[i] for i, lam in enumerate(Wa))
         if np.linalg.eigvalsh(Pa).min() <= 0 or np.linalg.eigvalsh(Aa.T @ Pa + Pa @ Aa).max() >= 0:
             return False
     return True
+
+
+def solve(P, eps=1e-8, tol=1e-8, maxit=60):
+    """Algorithm 2 iterated from its initial point until the duality gap is below eps
+    (stopping rule) and the primal residual ||B(X) - a|| below tol.  Returns
+    (converged, X, Z, y, iterations); converged requires every Z block PD (reading R10)."""
+    X, Z, y, mu = initial_state(P)
+    for it in range(1, maxit + 1):
+        try:
+            X, Z, y, st = ipm_step(P, X, Z, y, mu)
+        except np.linalg.LinAlgError:
+            return False, X, Z, y, it
+        mu = st["mu"]
+        if not np.all(np.isfinite(y)):
+            return False, X, Z, y, it
+        pinf = np.linalg.norm(sdp.adjoint_trace(P, X) - 1.0)
+        if st["gap"] <= eps and pinf <= tol:
+            return all(np.linalg.eigvalsh(z).min() > 0 for z in Z), X, Z, y, it
+    return False, X, Z, y, maxit
+
+
+def verdict(P, eps=1e-8, tol=1e-8, maxit=60, samples=1000, seed=0):
+    """Robust-stability certificate (Theorem 1 via Polya): converged SDP and the
+    reconstructed P(alpha) (reading R7) passing the grid check (O8)."""
+    ok, _, _, y, _ = solve(P, eps, tol, maxit)
+    return bool(ok and grid_check(P, y, samples, seed))

@@ -24,7 +24,7 @@ import numpy as np
 from .monomials import enumerate_W, index_map
 
 __all__ = ["poly_mul", "simplex_power", "beta_table", "H_table", "beta_recursion",
-           "H_recursion", "C_scalars", "counts", "H_row"]
+           "H_recursion", "C_scalars", "counts", "H_row", "homogenize", "simplex_map", "evaluate"]
 
 
 def poly_mul(p: dict, q: dict) -> dict:
@@ -155,3 +155,48 @@ def H_row(A: np.ndarray, l: int, dp: int, d2: int, h_index: int, da: int = 1) ->
     for e, c in prod.items():
         out[idx[e]] += c
     return out
+
+
+def homogenize(terms: dict, l: int):
+    """The homogenisation procedure of PAPER.md:113-132: with d_a the degree of A(alpha), the
+    i-th monomial of A is multiplied by (sum_j alpha_j)^{d_a - d_{a_i}} (so B = A on Delta_l).
+    terms: {exponent tuple: coefficient (scalar or n x n array)}.  Returns (d_a, coefficient array
+    of B in W_{d_a} order), expanded by explicit polynomial multiplication."""
+    da = max(sum(e) for e in terms)
+    idx = index_map(l, da)
+    c0 = np.asarray(next(iter(terms.values())), dtype=float)
+    out = np.zeros((len(idx),) + c0.shape)
+    for e, c in terms.items():
+        for e2, k in poly_mul(simplex_power(l, da - sum(e)), {tuple(e): 1}).items():
+            out[idx[e2]] += k * np.asarray(c, dtype=float)
+    return da, out
+
+
+def simplex_map(A: np.ndarray, l: int, d: int, scale, shift) -> np.ndarray:
+    """Coefficients (W_d order) of A'(alpha) = A(g(alpha)) for a homogeneous A of degree d given in
+    W_d order and the affine simplex map g_i(alpha) = scale_i alpha_i + shift_i, homogenised on
+    Delta_l as g_i = scale_i alpha_i + shift_i (sum_j alpha_j).  Example 1's map is
+    scale = 2|rho|, shift = -|rho|; Example 2 "defines g as in Example 1" for
+    S_L, read as scale = 1 - L, shift = L (reading R17)."""
+    Wd = enumerate_W(l, d)
+    idx = index_map(l, d)
+    unit = lambda i: tuple(1 if j == i else 0 for j in range(l))  # noqa: E731
+    g = []
+    for i in range(l):
+        gi = {unit(j): float(shift[i]) for j in range(l)}
+        gi[unit(i)] = gi[unit(i)] + float(scale[i])
+        g.append(gi)
+    out = np.zeros_like(np.asarray(A, dtype=float))
+    for k, lam in enumerate(Wd):
+        prod = {tuple([0] * l): 1.0}
+        for i in range(l):
+            for _ in range(lam[i]):
+                prod = poly_mul(prod, g[i])
+        for e, c in prod.items():
+            out[idx[e]] += c * A[k]
+    return out
+
+
+def evaluate(A: np.ndarray, l: int, d: int, alpha) -> np.ndarray:
+    """sum_{lambda in W_d} A[<lambda>] alpha^lambda (Eq. A_alpha, PAPER.md:178-181)."""
+    return sum(math.prod(a ** e for a, e in zip(alpha, lam)) * A[i] for i, lam in enumerate(enumerate_W(l, d)))
