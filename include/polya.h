@@ -204,6 +204,48 @@ polya_status polya_nccl_unique_id(char out_id[128]);
 polya_status polya_nccl_init(polya_ctx* ctx, const char id[128]);
 polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart_dev, double* Grecv_dev, int layout, void* stream);
 
+/* ---- beyond one iteration: non-homogeneous systems, parameter boxes, solve, verdict ------------
+ * (used by the bisection drivers of the paper's Examples 1-2.)
+ *
+ * polya_homogenize: the procedure of PAPER.md:113-132.  A(alpha) = sum_t coeffs_t alpha^{exps_t}
+ * (exps: int32[nterms][l], coeffs: double[nterms][n][n], host) of degree d_a = max_t |exps_t| is
+ * replaced by B(alpha) = sum_t coeffs_t (sum_j alpha_j)^{d_a - |exps_t|} alpha^{exps_t}, equal to A on
+ * the simplex and homogeneous; out = B's coefficients double[f(l,d_a)][n][n] in W_{d_a} order (R1).
+ * With out == NULL only *da_out is written (size query).  Host-only, synchronous.
+ *
+ * polya_simplex_map: A'(alpha) = A(g(alpha)) for the affine simplex maps of Examples 1-2
+ * (reading R17): g_i(alpha) = scale_i alpha_i + shift_i (sum_j alpha_j), which
+ * maps Delta_l affinely onto a box-constrained simplex (Example 1: scale = 2|rho|, shift = -|rho|; Example 2: scale = 1 - L, shift = L).  A_in, A_out: double[f(l,d)][n][n] in W_d
+ * order (homogeneous of degree d).  Host-only, synchronous.  Errors: EINVAL, EOVERFLOW.      */
+polya_status polya_homogenize(int32_t l, int32_t n, int32_t nterms, const int32_t* exps, const double* coeffs,
+                              int32_t* da_out, double* out);
+polya_status polya_simplex_map(int32_t l, int32_t d, int32_t n, const double* scale, const double* shift,
+                               const double* A_in, double* A_out);
+
+/* polya_ipm_solve: Algorithm 2 iterated (polya_ipm_step) until the stopping rule gap <= eps
+ * with primal residual ||B(X) - a||_2 <= tol, or maxit iterations.  init != 0
+ * starts from Algorithm 2's initial point X = Z = I, y = 0.  The outcome is a
+ * result, not an error: res->converged = 1 iff the rule was met with every Z block positive
+ * definite (reading R10); otherwise res->status says why (ENOTPD: a block or G lost definiteness,
+ * ESTEP: no admissible step, EMAXIT).  The return value reports only misuse / CUDA failures.
+ * Single rank (nranks = 1).  Synchronous.                                                   */
+typedef struct { double eps, tol; int32_t maxit, init; } polya_solve_opts;
+typedef struct {
+  int32_t converged, iterations, status;
+  double gap, pinf, mu;
+  float ms_schur, ms_factor, ms_other;   /* summed over the iterations */
+} polya_solve_result;
+polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, const polya_solve_opts* opt,
+                             polya_solve_result* res, void* stream);
+
+/* polya_verdict: the grid check of the certificate (Theorem 1):
+ * with P(alpha) = sum_h alpha^h V_h(y) (reading R7; y_dev: double[K] on the device) and A(alpha) the
+ * set-up's A, counts the points alpha = pts_host[p] (double[npts][l], host, points of the simplex)
+ * where P(alpha) > 0 or -(A^T P + P A)(alpha) > 0 fails a Cholesky test, into *nfail_out.
+ * One CTA per point on the device; n <= 64.  Synchronous.                                     */
+polya_status polya_verdict(polya_ctx* ctx, const double* y_dev, int32_t npts, const double* pts_host,
+                           int32_t* nfail_out, void* stream);
+
 /* Surfaces asynchronous errors (device synchronise + last-error check). */
 polya_status polya_sync(polya_ctx* ctx);
 const char* polya_strerror(polya_status s);

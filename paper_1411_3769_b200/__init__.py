@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 __all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "SHARD_TILES", "SHARD_BLOCKS", "EXPORTS",
-           "LIB_PATH", "plan", "nccl_unique_id"]
+           "LIB_PATH", "plan", "nccl_unique_id", "homogenize", "simplex_map"]
 
 # POLYA_LIB overrides the library path (timing-experiment variants built by tools/schur_exp.py)
 LIB_PATH = os.environ.get("POLYA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
@@ -21,7 +21,8 @@ SHARD_TILES, SHARD_BLOCKS = 0, 1
 EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents", "polya_get_beta", "polya_get_H",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
-           "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G"]
+           "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
+           "polya_simplex_map", "polya_ipm_solve", "polya_verdict"]
 
 
 class PolyaError(RuntimeError):
@@ -44,6 +45,16 @@ class _Dims(ctypes.Structure):
 class _IpmState(ctypes.Structure):
     _fields_ = [("X", ctypes.c_void_p), ("Z", ctypes.c_void_p), ("y", ctypes.c_void_p),
                 ("mu", ctypes.c_double), ("iter", ctypes.c_int32)]
+
+
+class _SolveOpts(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("init", ctypes.c_int32)]
+
+
+class _SolveResult(ctypes.Structure):
+    _fields_ = [("converged", ctypes.c_int32), ("iterations", ctypes.c_int32), ("status", ctypes.c_int32),
+                ("gap", ctypes.c_double), ("pinf", ctypes.c_double), ("mu", ctypes.c_double),
+                ("ms_schur", ctypes.c_float), ("ms_factor", ctypes.c_float), ("ms_other", ctypes.c_float)]
 
 
 class _IpmStats(ctypes.Structure):
@@ -81,6 +92,11 @@ def lib():
     L.polya_nccl_unique_id.argtypes = [vp]
     L.polya_nccl_init.argtypes = [vp, vp]
     L.polya_reduce_G.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+    L.polya_homogenize.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+    L.polya_simplex_map.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+    L.polya_ipm_solve.argtypes = [vp, ctypes.POINTER(_IpmState), ctypes.POINTER(_SolveOpts), ctypes.POINTER(_SolveResult),
+                                  vp]
+    L.polya_verdict.argtypes = [vp, vp, i32, vp, vp, vp]
     L.polya_strerror.argtypes = [ctypes.c_int]
     L.polya_strerror.restype = ctypes.c_char_p
     L.polya_last_error.argtypes = [vp]
@@ -114,6 +130,41 @@ def nccl_unique_id():
     if st != 0:
         raise PolyaError(f"polya_nccl_unique_id: {lib().polya_strerror(st).decode()}")
     return bytes(buf.raw)
+
+
+def homogenize(terms, l):
+    """polya_homogenize: terms = {exponent tuple: n x n array}; returns
+    (d_a, coefficients double[f(l,d_a)][n][n] in W_{d_a} order)."""
+    exps = np.ascontiguousarray(np.array([list(e) for e in terms], dtype=np.int32))
+    coeffs = np.ascontiguousarray(np.array([np.asarray(c, dtype=np.float64) for c in terms.values()]))
+    n = coeffs.shape[-1]
+    da = ctypes.c_int32()
+    vp = ctypes.c_void_p
+    st = lib().polya_homogenize(l, n, len(exps), exps.ctypes.data_as(vp), coeffs.ctypes.data_as(vp), ctypes.byref(da),
+                                None)
+    if st != 0:
+        raise PolyaError(f"polya_homogenize: {lib().polya_strerror(st).decode()}")
+    from math import comb
+    out = np.zeros((comb(l + da.value - 1, l - 1), n, n))
+    st = lib().polya_homogenize(l, n, len(exps), exps.ctypes.data_as(vp), coeffs.ctypes.data_as(vp), ctypes.byref(da),
+                                out.ctypes.data_as(vp))
+    if st != 0:
+        raise PolyaError(f"polya_homogenize: {lib().polya_strerror(st).decode()}")
+    return da.value, out
+
+
+def simplex_map(A, l, d, scale, shift):
+    """polya_simplex_map: coefficients of A(g(alpha)), g_i = scale_i alpha_i + shift_i sum_j alpha_j."""
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+    sc = np.ascontiguousarray(np.asarray(scale, dtype=np.float64))
+    sh = np.ascontiguousarray(np.asarray(shift, dtype=np.float64))
+    out = np.zeros_like(A)
+    vp = ctypes.c_void_p
+    st = lib().polya_simplex_map(l, d, A.shape[-1], sc.ctypes.data_as(vp), sh.ctypes.data_as(vp), A.ctypes.data_as(vp),
+                                 out.ctypes.data_as(vp))
+    if st != 0:
+        raise PolyaError(f"polya_simplex_map: {lib().polya_strerror(st).decode()}")
+    return out
 
 
 def _stream_ptr(stream=None):
@@ -241,6 +292,31 @@ class Polya:
         self._check(lib().polya_reduce_G(self._h, _dev_ptr(Gpart, None, "Gpart"), _dev_ptr(out, None, "Grecv"), layout,
                                          _stream_ptr(stream)), "polya_reduce_G")
         return out
+
+    def ipm_solve(self, X=None, Z=None, y=None, eps=1e-8, tol=1e-8, maxit=60, init=True, stream=None):
+        """polya_ipm_solve: Algorithm 2 to its stopping rule (state on the device, updated in place)."""
+        import torch
+        nbn = (self.nblocks, self.n, self.n)
+        X = torch.empty(nbn, dtype=torch.float64, device="cuda") if X is None else X
+        Z = torch.empty(nbn, dtype=torch.float64, device="cuda") if Z is None else Z
+        y = torch.empty(self.K, dtype=torch.float64, device="cuda") if y is None else y
+        st = _IpmState(_dev_ptr(X, None, "X").value, _dev_ptr(Z, None, "Z").value, _dev_ptr(y, self.K, "y").value,
+                       1.0 / 3.0, 0)
+        opt = _SolveOpts(float(eps), float(tol), int(maxit), int(bool(init)))
+        res = _SolveResult()
+        self._check(lib().polya_ipm_solve(self._h, ctypes.byref(st), ctypes.byref(opt), ctypes.byref(res),
+                                          _stream_ptr(stream)), "polya_ipm_solve")
+        out = {k: getattr(res, k) for k, _ in _SolveResult._fields_}
+        out.update(X=X, Z=Z, y=y)
+        return out
+
+    def verdict(self, y, pts, stream=None):
+        """polya_verdict: number of points of the simplex where the certificate fails the grid check."""
+        pts = np.ascontiguousarray(np.asarray(pts, dtype=np.float64).reshape(-1, self.l))
+        nf = ctypes.c_int32()
+        self._check(lib().polya_verdict(self._h, _dev_ptr(y, self.K, "y"), len(pts), pts.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.byref(nf), _stream_ptr(stream)), "polya_verdict")
+        return int(nf.value)
 
     def set_timing(self, on=True):
         self._check(lib().polya_set_timing(self._h, int(bool(on))), "polya_set_timing")

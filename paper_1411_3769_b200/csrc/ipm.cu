@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -227,6 +228,76 @@ __global__ void k_vec_axpby(int64_t K, double a, const double* __restrict__ x, d
 __global__ void k_vec_shift(int64_t K, double cst, double* __restrict__ x) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x)
     x[e] += cst;
+}
+
+// part[blk] = partial sum of (v_e - 1)^2 (primal residual ||B(X) - a||^2, a = 1)
+__global__ void k_resid(int64_t K, const double* __restrict__ v, double* __restrict__ part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x) {
+    const double d = v[e] - 1.0;
+    s += d * d;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// X_b = Z_b = I (Algorithm 2's initial point)
+__global__ void k_identity(int64_t total, int n, double* __restrict__ X, double* __restrict__ Z) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % ((int64_t)n * n);
+    const double v = (r / n == r % n) ? 1.0 : 0.0;
+    X[e] = v;
+    Z[e] = v;
+  }
+}
+
+// Verdict grid check (O8, Theorem 1): at the point alpha = pts[blockIdx.x] of the simplex,
+//   P(alpha) = sum_h alpha^h V_h(y)   (reading R7; V_h in the arena after k_vmap)
+//   A(alpha) = sum_lambda alpha^lambda A_lambda
+// and the test P(alpha) > 0, -(A^T P + P A)(alpha) > 0 by in-shared-memory Cholesky.
+__global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__ Wp, const int32_t* __restrict__ Wa,
+                       const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
+                       const double* __restrict__ A, const double* __restrict__ pts, int* __restrict__ nfail) {
+  extern __shared__ double sm[];
+  double* P = sm;
+  double* Aa = sm + n * n;
+  double* M = sm + 2 * n * n;
+  double* mono = sm + 3 * n * n;   // [L0 + nA]
+  const double* al = pts + (int64_t)blockIdx.x * l;
+  for (int q = threadIdx.x; q < L0 + nA; q += blockDim.x) {
+    const int32_t* e = q < L0 ? Wp + (int64_t)q * l : Wa + (int64_t)(q - L0) * l;
+    double m = 1.0;
+    for (int i = 0; i < l; ++i)
+      for (int k = 0; k < e[i]; ++k) m *= al[i];
+    mono[q] = m;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    double p = 0.0, a = 0.0;
+    for (int h = 0; h < L0; ++h) p += mono[h] * arena[(id_Vy + h) * ms + (int64_t)i * np + j];
+    for (int q = 0; q < nA; ++q) a += mono[L0 + q] * A[(int64_t)q * n * n + e];
+    P[e] = p;
+    Aa[e] = a;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    double v = 0.0;
+    for (int k = 0; k < n; ++k) v += Aa[k * n + i] * P[k * n + j] + P[i * n + k] * Aa[k * n + j];
+    M[e] = -v;
+  }
+  __syncthreads();
+  const bool lyap = smem_chol(M, n);
+  __syncthreads();
+  const bool pos = smem_chol(P, n);
+  if (threadIdx.x == 0 && !(lyap && pos)) atomicAdd(nfail, 1);
 }
 
 struct Ipm {
@@ -479,4 +550,121 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     return f.s;
   }
   return POLYA_OK;
+}
+
+// ---- Algorithm 2 to its stopping rule, and the verdict ---------------------
+
+extern "C" polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, const polya_solve_opts* opt,
+                                        polya_solve_result* res, void* stream) {
+  if (!ctx || !st || !st->X || !st->Z || !st->y || !opt || !res) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::memset(res, 0, sizeof(*res));
+  res->status = POLYA_EMAXIT;
+  try {
+    if (opt->init) {   // X = Z = I, y = 0, mu = tr(ZX) / (3 (L+M) n) = 1/3 (R4)
+      const int64_t total = c.nb * c.n * c.n;
+      k_identity<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(total, (int)c.n, st->X, st->Z);
+      ++c.launches;
+      CK(cudaGetLastError());
+      CK(cudaMemsetAsync(st->y, 0, (size_t)c.K * sizeof(double), s));
+      st->mu = 1.0 / 3.0;
+      st->iter = 0;
+    }
+    std::vector<double> part(kScalarBlocks);
+    for (int it = 0; it < opt->maxit; ++it) {
+      polya_ipm_stats ps;
+      const polya_status r = polya_ipm_step(ctx, st, &ps, stream);
+      res->iterations = it + 1;
+      if (r != POLYA_OK) {   // an outcome, not an exception: Z or G lost definiteness, no step
+        res->status = r;
+        return POLYA_OK;
+      }
+      res->gap = ps.gap;
+      res->mu = ps.mu;
+      res->ms_schur += ps.ms_schur;
+      res->ms_factor += ps.ms_factor;
+      res->ms_other += ps.ms_other;
+      // primal residual ||B(X) - a||_2
+      Ipm* w = ipm_ws(c);
+      call(polya_adjoint(ctx, st->X, w->tmpK, s), c);
+      k_resid<<<kScalarBlocks, 256, 0, s>>>(c.K, w->tmpK, w->part);
+      ++c.launches;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(part.data(), w->part, kScalarBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double r2 = 0.0;
+      for (double v : part) r2 += v;
+      res->pinf = std::sqrt(r2);
+      if (!std::isfinite(res->gap) || !std::isfinite(res->pinf)) {
+        res->status = POLYA_ENOTPD;
+        return POLYA_OK;
+      }
+      if (res->gap <= opt->eps && res->pinf <= opt->tol) {   // stopping rule
+        // every Z block positive definite (reading R10): the blockwise Cholesky of k_block_inv
+        CK(cudaMemsetAsync(w->fail, 0, sizeof(int), s));
+        CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(2 * (size_t)c.n * c.n * sizeof(double))));
+        k_block_inv<<<(unsigned)c.nb, 128, 2 * (size_t)c.n * c.n * sizeof(double), s>>>((int)c.n, st->Z, w->W, w->fail);
+        ++c.launches;
+        CK(cudaGetLastError());
+        int hfail = 0;
+        CK(cudaMemcpyAsync(&hfail, w->fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        res->converged = hfail ? 0 : 1;
+        res->status = hfail ? POLYA_ENOTPD : POLYA_OK;
+        return POLYA_OK;
+      }
+    }
+  } catch (const IpmFail& f) {
+    c.last_error = f.msg;
+    return f.s;
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t npts, const double* pts_host,
+                                      int32_t* nfail_out, void* stream) {
+  if (!ctx || !y || npts < 0 || (npts > 0 && !pts_host) || !nfail_out) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (c.n > 64) {
+    c.last_error = "polya_verdict: n <= 64 (three n x n matrices per point in shared memory)";
+    return POLYA_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  *nfail_out = 0;
+  if (npts == 0) return POLYA_OK;
+  int32_t *dWp = nullptr, *dWa = nullptr;
+  double* dpts = nullptr;
+  int* dfail = nullptr;
+  polya_status ret = POLYA_OK;
+  try {
+    CK(cudaMalloc(&dWp, c.Wp.size() * sizeof(int32_t)));
+    CK(cudaMalloc(&dWa, c.Wa.size() * sizeof(int32_t)));
+    CK(cudaMalloc(&dpts, (size_t)npts * c.l * sizeof(double)));
+    CK(cudaMalloc(&dfail, sizeof(int)));
+    CK(cudaMemcpyAsync(dWp, c.Wp.data(), c.Wp.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dWa, c.Wa.data(), c.Wa.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dpts, pts_host, (size_t)npts * c.l * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(dfail, 0, sizeof(int), s));
+    CK(launch_vmap(c, y, s));   // V_h(y) -> arena slots id_Vy + h
+    const size_t sm = (3 * (size_t)c.n * c.n + c.L0 + c.nA) * sizeof(double);
+    CK(cudaFuncSetAttribute(k_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_grid<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, (int)c.nA, dWp, dWa, c.arena, c.mstride,
+                                          (int)c.np, c.id_Vy, c.dA, dpts, dfail);
+    ++c.launches;
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *nfail_out = h;
+  } catch (const IpmFail& f) {
+    c.last_error = f.msg;
+    ret = f.s;
+  }
+  cudaFree(dWp);
+  cudaFree(dWa);
+  cudaFree(dpts);
+  cudaFree(dfail);
+  return ret;
 }

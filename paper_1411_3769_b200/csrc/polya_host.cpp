@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <new>
 
 #include "polya_internal.h"
@@ -532,6 +533,92 @@ extern "C" polya_status polya_plan(const polya_config* cfg, polya_dims* out) {
     c.cfg = g;
     build(c, nullptr, false);
     fill_dims(c, out);
+  } catch (const Fail& f) {
+    return f.s;
+  } catch (const std::bad_alloc&) {
+    return POLYA_ENOMEM;
+  }
+  return POLYA_OK;
+}
+
+// ---- homogenisation and simplex maps (set-up of non-homogeneous / non-simplex problems) ----------
+
+extern "C" polya_status polya_homogenize(int32_t l, int32_t n, int32_t nterms, const int32_t* exps,
+                                         const double* coeffs, int32_t* da_out, double* out) {
+  if (l < 1 || n < 1 || nterms < 1 || !exps || !da_out || (out && !coeffs)) return POLYA_EINVAL;
+  int32_t da = 0;
+  for (int32_t t = 0; t < nterms; ++t) {
+    int32_t d = 0;
+    for (int32_t i = 0; i < l; ++i) {
+      if (exps[(int64_t)t * l + i] < 0) return POLYA_EINVAL;
+      d += exps[(int64_t)t * l + i];
+    }
+    da = std::max(da, d);
+  }
+  *da_out = da;
+  if (!out) return POLYA_OK;   // size query
+  try {
+    std::vector<int32_t> W;
+    enumerate(l, da, W);
+    const int64_t cnt = (int64_t)W.size() / l, nn = (int64_t)n * n;
+    std::fill(out, out + cnt * nn, 0.0);
+    std::vector<int32_t> diff(l);
+    for (int32_t t = 0; t < nterms; ++t) {
+      int32_t d = 0;
+      for (int32_t i = 0; i < l; ++i) d += exps[(int64_t)t * l + i];
+      // (sum_j alpha_j)^{da - d} alpha^{e_t} = sum_gamma multinomial(da - d; gamma - e_t) alpha^gamma
+      for (int64_t g = 0; g < cnt; ++g) {
+        for (int32_t i = 0; i < l; ++i) diff[i] = W[g * l + i] - exps[(int64_t)t * l + i];
+        const int64_t w = multinomial(da - d, diff.data(), l);
+        if (!w) continue;
+        for (int64_t e = 0; e < nn; ++e) out[g * nn + e] += (double)w * coeffs[(int64_t)t * nn + e];
+      }
+    }
+  } catch (const Fail& f) {
+    return f.s;
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_simplex_map(int32_t l, int32_t d, int32_t n, const double* scale, const double* shift,
+                                          const double* A_in, double* A_out) {
+  if (l < 1 || d < 0 || n < 1 || !scale || !shift || !A_in || !A_out) return POLYA_EINVAL;
+  try {
+    // exponent -> position in W_k, for k = 0..d
+    std::vector<std::vector<int32_t>> W(d + 1);
+    std::vector<std::map<std::vector<int32_t>, int64_t>> pos(d + 1);
+    for (int32_t k = 0; k <= d; ++k) {
+      enumerate(l, k, W[k]);
+      for (int64_t q = 0; q < (int64_t)W[k].size() / l; ++q)
+        pos[k][std::vector<int32_t>(W[k].begin() + q * l, W[k].begin() + (q + 1) * l)] = q;
+    }
+    const int64_t cnt = (int64_t)W[d].size() / l, nn = (int64_t)n * n;
+    std::fill(A_out, A_out + cnt * nn, 0.0);
+    for (int64_t q = 0; q < cnt; ++q) {
+      // prod_i g_i(alpha)^{lambda_i}, g_i = scale_i alpha_i + shift_i sum_j alpha_j, by explicit
+      // polynomial multiplication (dense coefficient vectors over W_k)
+      std::vector<double> poly(1, 1.0);
+      int32_t deg = 0;
+      for (int32_t i = 0; i < l; ++i)
+        for (int32_t r = 0; r < W[d][q * l + i]; ++r) {
+          std::vector<double> next(W[deg + 1].size() / l, 0.0);
+          std::vector<int32_t> e(l);
+          for (int64_t u = 0; u < (int64_t)poly.size(); ++u) {
+            if (poly[u] == 0.0) continue;
+            for (int32_t j = 0; j < l; ++j) {
+              const double cij = shift[i] + (j == i ? scale[i] : 0.0);
+              if (cij == 0.0) continue;
+              for (int32_t v = 0; v < l; ++v) e[v] = W[deg][u * l + v] + (v == j ? 1 : 0);
+              next[pos[deg + 1][e]] += poly[u] * cij;
+            }
+          }
+          poly.swap(next);
+          ++deg;
+        }
+      for (int64_t g = 0; g < cnt; ++g)
+        if (poly[g] != 0.0)
+          for (int64_t e = 0; e < nn; ++e) A_out[g * nn + e] += poly[g] * A_in[q * nn + e];
+    }
   } catch (const Fail& f) {
     return f.s;
   } catch (const std::bad_alloc&) {

@@ -1,0 +1,119 @@
+"""GPU tests of the full method beyond one iteration: Algorithm 2
+to its stopping rule (polya_ipm_solve), the certificate's grid check on the device
+(polya_verdict), and bisection on the paper's Example 2.
+
+Bars: the verdicts (certified or not) equal the oracle's on the same problems (reading R15: the
+certificate itself is not unique, the verdict is); a bisection whose every verdict agrees returns
+the oracle's bound exactly; every certified bound lies above the brute-force stability boundary
+(-0.1115, see tests/test_oracle_examples.py: Theorem 1 makes a certificate impossible below it)
+and tightens as (d_p, d1, d2) grow."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ipm as oipm
+from oracle import polya as opolya
+from oracle import sdp as osdp
+
+from test_oracle_examples import example2_A
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+BOUNDARY = -0.1115   # brute-force stability boundary of Example 2 (stable at -0.1115, unstable at -0.112)
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_1411_3769_b200 as pb
+    pb.lib()
+    assert torch.cuda.is_available()
+    return pb
+
+
+@pytest.mark.parametrize("key,stable", [(1, True), ("1u", False), (2, True)])
+def test_solve_and_verdict_on_constructed_systems(pb, key, stable):
+    from paper_1411_3769_b200 import robust
+    c = synth.CONFIGS[key]
+    A = synth.vertex_matrices(c, np.random.default_rng(0))
+    r = robust.certify(A, c.n, c.l, c.dp, c.d1, c.d2, samples=300)
+    assert r["certified"] == stable, r
+    if stable:
+        assert r["gap"] <= 1e-8 and r["pinf"] <= 1e-8 and r["nfail"] == 0
+
+
+def test_solve_matches_oracle_solution_config1(pb):
+    """Same stopping iteration and the same certificate y to 1e-6 on config 1 (the GPU steps match
+    the oracle's to ~1e-15 each, tests/test_gpu_ipm.py)."""
+    c = synth.CONFIGS[1]
+    A = synth.vertex_matrices(c, np.random.default_rng(0))
+    P = osdp.build_problem(A, c.n, c.l, c.dp, c.d1, c.d2)
+    ok, X, Z, y, it = oipm.solve(P)
+    ctx = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
+    r = ctx.ipm_solve()
+    assert bool(r["converged"]) == ok and r["iterations"] == it
+    yg = r["y"].cpu().numpy()
+    assert np.linalg.norm(yg - y) <= 1e-6 * np.linalg.norm(y)
+    ctx.close()
+
+
+def test_verdict_kernel_matches_oracle_grid_check(pb):
+    """polya_verdict on a converged certificate and on a perturbed (invalid) one, vs oracle.grid_check."""
+    from paper_1411_3769_b200 import robust
+    P = osdp.build_problem(example2_A(0.4), 3, 3, 1, 1, 1, da=3)
+    ok, X, Z, y, it = oipm.solve(P)
+    assert ok
+    ctx = pb.Polya(3, 3, 1, 1, 1, example2_A(0.4), da=3)
+    pts = robust.simplex_points(3, 300, 0)
+    yd = torch.from_numpy(y).cuda()
+    assert ctx.verdict(yd, pts) == 0 and oipm.grid_check(P, y, 300, 0)
+    bad = y.copy()
+    bad[:6] *= -1.0                         # P_0 -> -P_0: not positive at the first vertex
+    assert ctx.verdict(torch.from_numpy(bad).cuda(), pts) > 0 and not oipm.grid_check(P, bad, 300, 0)
+    ctx.close()
+
+
+@pytest.mark.parametrize("L,deg,certified", [(0.4, (1, 1, 1), True), (0.1, (1, 2, 2), True),
+                                               (0.0, (1, 1, 1), False), (-0.2, (2, 2, 2), False)])
+def test_example2_verdicts_match_oracle(pb, L, deg, certified):
+    from paper_1411_3769_b200 import robust
+    r = robust.certify(example2_A(L), 3, 3, *deg, da=3, samples=300)
+    assert r["certified"] == certified == oipm.verdict(osdp.build_problem(example2_A(L), 3, 3, *deg, da=3), samples=300)
+
+
+def test_example2_bisection_equals_oracle(pb):
+    from paper_1411_3769_b200 import robust
+    deg = (1, 2, 2)
+
+    def gpu(L):
+        Ap = robust_A(pb, L)
+        return robust.certify(Ap, 3, 3, *deg, da=3, samples=300)["certified"]
+
+    def cpu(L):
+        return oipm.verdict(osdp.build_problem(example2_A(L), 3, 3, *deg, da=3), samples=300)
+
+    hg, lg, tg = robust.bisect(gpu, -0.2, 0.4, steps=8)
+    hc, lc, tc = robust.bisect(cpu, -0.2, 0.4, steps=8)
+    assert tg == tc and hg == hc
+    assert BOUNDARY < hg < 0.4
+
+
+def robust_A(pb, L):
+    """Example 2's A(g(alpha)) through the library's own set-up (polya_homogenize + polya_simplex_map)."""
+    from test_oracle_examples import example2_terms
+    da, A = pb.homogenize(example2_terms(), 3)
+    return pb.simplex_map(A, 3, da, [1 - L] * 3, [L] * 3)
+
+
+def test_example2_bounds_tighten_with_degree(pb):
+    """Upper bounds on L_opt = -0.111 from bisection at growing (d_p, d1 = d2): never below
+    the stability boundary (Theorem 1) and non-increasing in the degrees."""
+    from paper_1411_3769_b200 import robust
+    bounds = []
+    for deg in [(1, 1, 1), (2, 2, 2), (2, 4, 4), (3, 6, 6)]:
+        hi, lo, _ = robust.bisect(lambda L: robust.certify(robust_A(pb, L), 3, 3, *deg, da=3, samples=300)["certified"],
+                                  -0.2, 0.6, steps=9)
+        bounds.append(hi)
+    assert all(b > BOUNDARY for b in bounds)
+    assert all(bounds[i + 1] <= bounds[i] + 1e-12 for i in range(len(bounds) - 1)), bounds
+    assert bounds[-1] < bounds[0]
