@@ -49,3 +49,13 @@ def test_invalid_arguments_are_rejected_without_a_gpu():
     cfg = pb._Config(4, 2, 1, 1, 1, 1, 1e-3, 2, 2)                    # rank outside [0, nranks)
     assert L.polya_setup(ctypes.byref(cfg), ctypes.c_void_p(1), ctypes.byref(h)) == 1
     assert L.polya_strerror(2) == b"integer overflow in problem size"
+
+
+def test_library_then_torch_import_order():
+    """libpolya.so links the NCCL that PyTorch loads (rpath to the pip wheel), so loading the
+    library BEFORE torch must not shadow torch's libnccl.so.2 with an older system copy."""
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_1411_3769_b200 as pb; pb.lib(); "
+            "import torch; import torch.distributed; print('ok')") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
