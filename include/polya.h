@@ -181,6 +181,14 @@ typedef struct {
 } polya_ipm_stats;
 polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, polya_ipm_stats* stats, void* stream);
 
+/* Factorisation of the K x K Schur complement inside polya_ipm_step (the root's Cholesky, Case 2,
+ * PAPER.md:913-916): mode 0 = automatic (dense when K^2 doubles fit in 45 % of device memory,
+ * else tiled), 1 = dense (G in POLYA_G_FULL layout, cuSOLVER dpotrf/dpotrs), 2 = tiled (G in
+ * POLYA_G_PAIR_TILES layout -- half the memory -- right-looking block Cholesky: cuSOLVER dpotrf on
+ * the diagonal tiles, cuBLAS dtrsm/dsyrk/dgemm on the others, blocked triangular solves).
+ * Applies from the next polya_ipm_step.  Errors: EINVAL.                                     */
+polya_status polya_set_factorization(polya_ctx* ctx, int mode);
+
 /* Phase timing of polya_schur with CUDA events recorded on the call's stream:
  * enable != 0 turns the events on for subsequent calls; polya_get_timing waits for the
  * last call's events and returns the milliseconds of the SCM precompute (padding, U, V,

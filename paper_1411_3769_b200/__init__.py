@@ -22,7 +22,7 @@ EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
            "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
-           "polya_simplex_map", "polya_ipm_solve", "polya_verdict"]
+           "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization"]
 
 
 class PolyaError(RuntimeError):
@@ -97,6 +97,7 @@ def lib():
     L.polya_ipm_solve.argtypes = [vp, ctypes.POINTER(_IpmState), ctypes.POINTER(_SolveOpts), ctypes.POINTER(_SolveResult),
                                   vp]
     L.polya_verdict.argtypes = [vp, vp, i32, vp, vp, vp]
+    L.polya_set_factorization.argtypes = [vp, ctypes.c_int]
     L.polya_strerror.argtypes = [ctypes.c_int]
     L.polya_strerror.restype = ctypes.c_char_p
     L.polya_last_error.argtypes = [vp]
@@ -317,6 +318,10 @@ class Polya:
         self._check(lib().polya_verdict(self._h, _dev_ptr(y, self.K, "y"), len(pts), pts.ctypes.data_as(ctypes.c_void_p),
                                         ctypes.byref(nf), _stream_ptr(stream)), "polya_verdict")
         return int(nf.value)
+
+    def set_factorization(self, mode):
+        """polya_set_factorization: 0 auto, 1 dense K x K, 2 tiled (pair tiles)."""
+        self._check(lib().polya_set_factorization(self._h, int(mode)), "polya_set_factorization")
 
     def set_timing(self, on=True):
         self._check(lib().polya_set_timing(self._h, int(bool(on))), "polya_set_timing")

@@ -7,12 +7,17 @@
 //   O1  = B(W Rd X) - 1                                     (Processors step 1, Eq. T1)
 //   G   = SCM (polya_schur, POLYA_G_FULL)                   (Eq. T2)
 //   potrf(G); dy^ = G^-1 O1                                 (Root step 1, Eq. SAE1; cuSOLVER)
+//     -- or, when the K x K matrix does not fit (config 5: 186 GB), a right-looking block Cholesky
+//        over the PAIR_TILES layout of polya_schur (cuSOLVER potrf on diagonal tiles, cuBLAS
+//        trsm / syrk / gemm on the rest) and blocked triangular solves: the root's factorisation
+//        (Case 2) on one GPU with half the memory
 //   dZ^ = -Rd + B^T(dy^);  dX^ = sym(-X + W (Rd - B^T(dy^)) X)          (R3)
 //   O2  = mu B(W) - B(W dZ^ dX^);  dy- = G^-1 O2            (Processors/Root step 2, Eq. SAE2)
 //   dZ- = B^T(dy-);  dX- = sym(mu W - W dZ^ dX^ - W dZ- X)  (Processors step 3)
 //   t_p, t_d = min(1, 0.98 t_max), t_max by per-block bisection on positive definiteness (R5)
 //   X += t_p dX, Z += t_d dZ, y += t_d dy                   (Eqs. 33-35, R6)
 //   mu = tr(ZX) / (3 (L+M) n) (R4), phi = tr(CX), psi = sum y, gap = |phi - psi|   (Step 4)
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -308,7 +313,9 @@ struct Ipm {
   int* info = nullptr;
   int* fail = nullptr;
   int lwork = 0;
+  bool tiled = false;          // G held as pair tiles (lower block triangle in column-major view)
   cusolverDnHandle_t sol = nullptr;
+  cublasHandle_t blas = nullptr;
   cudaEvent_t ev[6] = {};
 };
 
@@ -329,6 +336,7 @@ void polya_ipm_free(polya::Ctx& c) {
   if (w->info) cudaFree(w->info);
   if (w->fail) cudaFree(w->fail);
   if (w->sol) cusolverDnDestroy(w->sol);
+  if (w->blas) cublasDestroy(w->blas);
   for (auto& e : w->ev)
     if (e) cudaEventDestroy(e);
   delete w;
@@ -347,23 +355,38 @@ struct IpmFail {
     if (e_ != cudaSuccess) throw IpmFail{e_ == cudaErrorMemoryAllocation ? POLYA_ENOMEM : POLYA_ECUDA, \
                                          std::string(#x) + ": " + cudaGetErrorString(e_)};         \
   } while (0)
+#define CB(x)                                                                                      \
+  do {                                                                                             \
+    cublasStatus_t e_ = (x);                                                                       \
+    if (e_ != CUBLAS_STATUS_SUCCESS) throw IpmFail{POLYA_ECUDA, std::string(#x) + " failed"};      \
+  } while (0)
 #define CS(x)                                                                                      \
   do {                                                                                             \
     cusolverStatus_t e_ = (x);                                                                     \
     if (e_ != CUSOLVER_STATUS_SUCCESS) throw IpmFail{POLYA_ECUDA, std::string(#x) + " failed"};    \
   } while (0)
 
+bool want_tiled(const Ctx& c) {
+  if (c.fact_mode == 1) return false;
+  if (c.fact_mode == 2) return true;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+  return (double)c.K * (double)c.K * 8.0 > 0.45 * (double)tot;   // the dense K x K G would not fit comfortably
+}
+
 Ipm* ipm_ws(Ctx& c) {
+  if (c.ipm && ((Ipm*)c.ipm)->tiled != want_tiled(c)) polya_ipm_free(c);   // factorisation mode changed
   if (c.ipm) return (Ipm*)c.ipm;
   Ipm* w = new Ipm();
   c.ipm = w;
   w->nb = c.nb; w->n = c.n; w->K = c.K;
+  w->tiled = want_tiled(c);
   const size_t st = (size_t)c.nb * c.n * c.n * sizeof(double), kv = (size_t)c.K * sizeof(double);
   double** stacks[] = {&w->W, &w->Rd, &w->T1, &w->T2, &w->dX1, &w->dZ1, &w->dX2, &w->dZ2};
   for (double** p : stacks) CK(cudaMalloc(p, st));
   double** vecs[] = {&w->O1, &w->O2, &w->dy1, &w->dy2, &w->tmpK};
   for (double** p : vecs) CK(cudaMalloc(p, kv));
-  CK(cudaMalloc(&w->G, (size_t)c.K * c.K * sizeof(double)));
+  CK(cudaMalloc(&w->G, (w->tiled ? (size_t)c.npairs * c.Ntil * c.Ntil : (size_t)c.K * c.K) * sizeof(double)));
   CK(cudaMalloc(&w->tb, (size_t)c.nb * sizeof(double)));
   CK(cudaMalloc(&w->part, (size_t)kScalarBlocks * 3 * sizeof(double)));
   CK(cudaMalloc(&w->dc, (size_t)std::max<int64_t>(c.L, 1) * sizeof(double)));
@@ -371,7 +394,9 @@ Ipm* ipm_ws(Ctx& c) {
   CK(cudaMalloc(&w->info, sizeof(int)));
   CK(cudaMalloc(&w->fail, sizeof(int)));
   CS(cusolverDnCreate(&w->sol));
-  CS(cusolverDnDpotrf_bufferSize(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, &w->lwork));
+  const int fdim = (int)(w->tiled ? c.Ntil : c.K);
+  CS(cusolverDnDpotrf_bufferSize(w->sol, CUBLAS_FILL_MODE_LOWER, fdim, w->G, fdim, &w->lwork));
+  CB(cublasCreate(&w->blas));
   CK(cudaMalloc(&w->work, (size_t)std::max(w->lwork, 1) * sizeof(double)));
   for (auto& e : w->ev) CK(cudaEventCreate(&e));
   return w;
@@ -422,6 +447,64 @@ double step_len(Ctx& c, Ipm* w, const double* S, const double* dS, cudaStream_t 
   return std::min(1.0, frac * t);
 }
 
+// ---- blocked Cholesky on the pair tiles --------------------------------------------------------
+// Tile of pair (h <= h') holds G[h-block][h'-block] row-major = the block B_{h'h} of the LOWER block
+// triangle in column-major view (N = Ntil).  G = L L^T, right-looking, L overwriting B.
+inline double* tile(const Ctx& c, Ipm* w, int64_t h, int64_t h2) {
+  const int64_t p = h * c.L0 - h * (h - 1) / 2 + (h2 - h);
+  return w->G + p * c.Ntil * c.Ntil;
+}
+
+void tiled_potrf(Ctx& c, Ipm* w, cudaStream_t s) {
+  const int N = (int)c.Ntil;
+  const int64_t T = c.L0;
+  const double one = 1.0, mone = -1.0;
+  CB(cublasSetStream(w->blas, s));
+  CK(cudaMemsetAsync(w->info, 0, sizeof(int), s));
+  for (int64_t k = 0; k < T; ++k) {
+    double* Lkk = tile(c, w, k, k);
+    CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, N, Lkk, N, w->work, w->lwork, w->info));
+    int hinfo = 0;
+    CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hinfo != 0)
+      throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite (tile " + std::to_string(k) + ", info " +
+                                      std::to_string(hinfo) + ")"};
+    for (int64_t i = k + 1; i < T; ++i)   // B_ik <- B_ik L_kk^{-T}
+      CB(cublasDtrsm(w->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, N, N, &one,
+                     Lkk, N, tile(c, w, k, i), N));
+    for (int64_t i = k + 1; i < T; ++i) {  // trailing update B_ij -= B_ik B_jk^T, k < j <= i
+      const double* Bik = tile(c, w, k, i);
+      CB(cublasDsyrk(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, N, N, &mone, Bik, N, &one, tile(c, w, i, i), N));
+      for (int64_t j = k + 1; j < i; ++j)
+        CB(cublasDgemm(w->blas, CUBLAS_OP_N, CUBLAS_OP_T, N, N, N, &mone, Bik, N, tile(c, w, k, j), N, &one,
+                       tile(c, w, j, i), N));
+    }
+  }
+  c.launches += T * (T + 1) * (T + 2) / 6 + T * (T + 1) / 2;
+}
+
+// x <- G^{-1} x with the tiled factor: L z = x (forward), L^T x = z (backward).
+void tiled_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
+  const int N = (int)c.Ntil;
+  const int64_t T = c.L0;
+  const double one = 1.0, mone = -1.0;
+  CB(cublasSetStream(w->blas, s));
+  for (int64_t k = 0; k < T; ++k) {
+    double* xk = x + k * N;
+    CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, N, tile(c, w, k, k), N, xk, 1));
+    for (int64_t i = k + 1; i < T; ++i)
+      CB(cublasDgemv(w->blas, CUBLAS_OP_N, N, N, &mone, tile(c, w, k, i), N, xk, 1, &one, x + i * N, 1));
+  }
+  for (int64_t k = T - 1; k >= 0; --k) {
+    double* xk = x + k * N;
+    for (int64_t i = k + 1; i < T; ++i)
+      CB(cublasDgemv(w->blas, CUBLAS_OP_T, N, N, &mone, tile(c, w, k, i), N, x + i * N, 1, &one, xk, 1));
+    CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, N, tile(c, w, k, k), N, xk, 1));
+  }
+  c.launches += 2 * T * (T + 1) / 2 + 2 * T;
+}
+
 polya_status call(polya_status st, Ctx& c) {
   if (st != POLYA_OK) throw IpmFail{st, c.last_error};
   return st;
@@ -470,9 +553,14 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     CK(cudaGetLastError());
     // G (FULL layout), then its Cholesky factor (timed separately)
     CK(cudaEventRecord(w->ev[1], s));
-    call(polya_schur(ctx, X, w->W, w->G, POLYA_G_FULL, s), c);
+    call(polya_schur(ctx, X, w->W, w->G, w->tiled ? POLYA_G_PAIR_TILES : POLYA_G_FULL, s), c);
     CK(cudaEventRecord(w->ev[2], s));
-    CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, w->work, w->lwork, w->info));
+    if (w->tiled) {
+      CK(cudaMemsetAsync(w->info, 0, sizeof(int), s));
+      tiled_potrf(c, w, s);
+    } else {
+      CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, w->work, w->lwork, w->info));
+    }
     CK(cudaEventRecord(w->ev[3], s));
     int hinfo = 0, hfail = 0;
     CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -482,7 +570,8 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     if (hinfo != 0) throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite (potrf info " + std::to_string(hinfo) + ")"};
     // dy^ = G^-1 O1
     CK(cudaMemcpyAsync(w->dy1, w->O1, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy1, (int)c.K, w->info));
+    if (w->tiled) tiled_potrs(c, w, w->dy1, s);
+    else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy1, (int)c.K, w->info));
     // dZ^ = -Rd + B^T(dy^);  dX^ = sym(-X + W (Rd - B^T(dy^)) X)
     call(polya_apply(ctx, w->dy1, w->T1, s), c);
     axpby(c, -1.0, w->Rd, 1.0, w->T1, w->dZ1, nullptr, 0.0, s);          // dZ^
@@ -498,7 +587,8 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     call(polya_adjoint(ctx, w->T2, w->O2, s), c);
     vaxpby(c, mu, w->tmpK, -1.0, w->O2, w->O2, s);
     CK(cudaMemcpyAsync(w->dy2, w->O2, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy2, (int)c.K, w->info));
+    if (w->tiled) tiled_potrs(c, w, w->dy2, s);
+    else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy2, (int)c.K, w->info));
     // dZ- = B^T(dy-);  dX- = sym(mu W - W dZ^ dX^ - W dZ- X)
     call(polya_apply(ctx, w->dy2, w->dZ2, s), c);
     bgemm(c, w->dZ2, 0, X, 0, w->T1, 1.0, 0.0, s);                         // dZ- X
@@ -667,4 +757,10 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
   cudaFree(dpts);
   cudaFree(dfail);
   return ret;
+}
+
+extern "C" polya_status polya_set_factorization(polya_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 2) return POLYA_EINVAL;
+  ctx->c.fact_mode = mode;
+  return POLYA_OK;
 }

@@ -95,6 +95,7 @@ struct Ctx {
   // IPM workspace (allocated lazily)
   void* ipm = nullptr;
   bool timing = false;
+  int fact_mode = 0;     // polya_set_factorization: 0 auto, 1 dense K x K, 2 tiled (pair tiles)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   std::string last_error;
   int64_t launches = 0;

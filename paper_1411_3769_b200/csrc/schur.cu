@@ -227,7 +227,7 @@ __device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int&
 
 #ifndef SCHUR_EXP
 #define SCHUR_EXP 0   // timing experiments only (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either,
-                      // 4 = no operand loads, 8 = no ragged-warp skip
+                      // 4 = no operand loads, 8 = no ragged-warp skip, 16 = no fragment LDS
 #endif
 #ifndef SCHUR_MINB
 #define SCHUR_MINB 3
@@ -244,26 +244,26 @@ __device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
   return v;
 }
 
-// One orientation of an item on the consumer warps: the raw 64x64 sub-block
+// One orientation of an item on the consumer warps: the raw sub-block
 // Raw[(x,y),(z,w)] = sum_k L_k[x,y] R_k[z,w] (x in cX, y in cY, z in cZ, w in cW) over the
-// item's nstage ring stages, then folded into Gs.  Warp (xw, zw) owns x in xw..xw+3 and
-// z in zw..zw+3.  MI = 4: M-tile i is x = xw+i with rows y = 0..7; MI = 2 (ragged y chunk,
-// <= 4 valid rows): M-tile i packs x = xw+2i+(g>>2) with y = g&3.  NJ likewise for (z, w) on the
-// N side, where the accumulator column 2t+e is w = 2t+e (NJ = 4) or z = zw+2j+(t>>1),
-// w = 2(t&1)+e (NJ = 2).
-template <int MI, int NJ>
+// item's nstage ring stages, then folded into Gs.  The valid (x, y) rows form MT M-tiles of 8
+// and the valid (z, w) columns NT N-tiles; the 4 warps split both in halves (2 x 2), so each warp
+// owns MI = MT/2 M-tiles and NJ = NT/2 N-tiles whatever the raggedness:
+//   PY = 0: M-tile m is x = m with rows y = 0..7 (MT = 8, or 4 when cX is a ragged chunk with <= 4
+//           valid x -- the 4 invalid x are not computed at all);
+//   PY = 1: cY is ragged (<= 4 valid y): M-tile m packs x = 2m + (g>>2) with y = g&3 (MT = 4 or 2);
+// and likewise on the N side (z, w) with PW, where the accumulator column 2t+e is w = 2t+e
+// (PW = 0) or z = 2n+(t>>1), w = 2(t&1)+e (PW = 1).
+template <int MI, int NJ, int PY, int PW>
 __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
-                                       uint64_t* empty, uint32_t& cnt, int nstage, int o, int cX, int cZ,
-                                       bool first, uint64_t* pbar, uint32_t& nph) {
+                                       uint64_t* empty, uint32_t& cnt, int nstage, int o, bool first,
+                                       uint64_t* pbar, uint32_t& nph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int xw = 4 * (warp >> 1), zw = 4 * (warp & 1);
-  const int n = p.n;
-  const int nvx = min(Q, n - cX * Q), nvz = min(Q, n - cZ * Q);
-  // a warp whose x- or z-tiles all lie past a ragged chunk's end only multiplies zeros: skip
-  const bool active = ((SCHUR_EXP & 8) != 0) || ((xw < nvx) && (zw < nvz));   // bit 8: no ragged skip
-  constexpr int AST = MI == 4 ? Q : 2 * Q, BST = NJ == 4 ? Q : 2 * Q;   // fragment strides per tile
-  const int aoff = xw * Q + (MI == 4 ? g : (g >> 2) * Q + (g & 3));
-  const int boff = zw * Q + (NJ == 4 ? g : (g >> 2) * Q + (g & 3));
+  const int m0 = MI * (warp >> 1), n0 = NJ * (warp & 1);   // the warp's first M-tile and N-tile
+  constexpr bool active = true;
+  constexpr int AST = PY ? 2 * Q : Q, BST = PW ? 2 * Q : Q;   // fragment strides per tile
+  const int aoff = PY ? (2 * m0 + (g >> 2)) * Q + (g & 3) : m0 * Q + g;
+  const int boff = PW ? (2 * n0 + (g >> 2)) * Q + (g & 3) : n0 * Q + g;
   double acc[MI][NJ][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
@@ -279,9 +279,9 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
       for (int k4 = 0; k4 < 2; ++k4) {
         double a[MI], b[NJ];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[i] = fA[k4 * 4 * KS + i * AST];
+        for (int i = 0; i < MI; ++i) a[i] = (SCHUR_EXP & 16) ? 1e-3 * (lane + i + k4) : fA[k4 * 4 * KS + i * AST];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) b[j] = fB[k4 * 4 * KS + j * BST];
+        for (int j = 0; j < NJ; ++j) b[j] = (SCHUR_EXP & 16) ? 1e-3 * (lane - j + s) : fB[k4 * 4 * KS + j * BST];
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -308,16 +308,16 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
   int bx[MI], bz[NJ][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
-    const int x = MI == 4 ? xw + i : xw + 2 * i + (g >> 2);
-    const int y = MI == 4 ? g : (g & 3);
+    const int x = PY ? 2 * (m0 + i) + (g >> 2) : m0 + i;
+    const int y = PY ? (g & 3) : g;
     bx[i] = ((o & 2) ? Ta(x) : Tb(x)) ^ ((o & 1) ? y : Tc(y));
   }
 #pragma unroll
   for (int j = 0; j < NJ; ++j)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int z = NJ == 4 ? zw + j : zw + 2 * j + (t >> 1);
-      const int w = NJ == 4 ? 2 * t + e : 2 * (t & 1) + e;
+      const int z = PW ? 2 * (n0 + j) + (t >> 1) : n0 + j;
+      const int w = PW ? 2 * (t & 1) + e : 2 * t + e;
       bz[j][e] = ((o & 1) ? Tc(z) : z) ^ ((o & 2) ? Tb(w) : Ta(w));
     }
   if (first) {
@@ -344,6 +344,25 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
   phase_arrive(pbar, nph);
 }
 
+// (M side, N side) code -> instantiation: code 0: 8 full tiles (4 per warp), 1: 4 unpacked tiles
+// (ragged x / z), 2: 4 packed tiles (ragged y / w), 3: 2 packed tiles (both ragged).
+#define ORIENT_M(MC, MI, PY)                                                                          \
+  case MC * 4 + 0: orient<MI, 4, PY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 4 + 1: orient<MI, 2, PY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 4 + 2: orient<MI, 2, PY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 4 + 3: orient<MI, 1, PY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break;
+__device__ __noinline__ void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
+                                             uint64_t* empty, uint32_t& cnt, int nstage, int o, bool first,
+                                             uint64_t* pbar, uint32_t& nph) {
+  switch (code) {
+    ORIENT_M(0, 4, 0)
+    ORIENT_M(1, 2, 0)
+    ORIENT_M(2, 2, 1)
+    ORIENT_M(3, 1, 1)
+  }
+}
+#undef ORIENT_M
+
 __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   extern __shared__ __align__(16) double smem[];
   double* Gs = smem + NSTAGE * STAGE;
@@ -355,7 +374,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   __shared__ uint64_t s_pbar;                  // consumer phase barrier (NCW arrivals per phase)
   __shared__ SlotInfo s_info[NSTAGE];      // item of the stage held by each ring slot (first stages)
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < 64) {  // diagonal order: consecutive entries have consecutive svec indices
     int idx = 0;
     for (int dlt = -(Q - 1); dlt <= Q - 1; ++dlt)
@@ -524,11 +543,10 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
       // ragged chunk (n not a multiple of 8) in an MMA dimension (y: M rows, w: N columns): with
       // <= 4 valid indices, pack two x (or z) values into one 8-row MMA tile instead of
       // multiplying 8-row tiles that are half zeros
-      const bool rY = (n - cY * Q) <= 4, rW = (n - cW * Q) <= 4;
-      if (!rY && !rW) orient<4, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
-      else if (rY && !rW) orient<2, 4>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
-      else if (!rY && rW) orient<4, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
-      else orient<2, 2>(p, smem, Gs, full, empty, cnt, it.nstage, o, cX, cZ, first, &s_pbar, nph);
+      const bool rY = (n - cY * Q) <= 4, rW = (n - cW * Q) <= 4;   // packed MMA rows / columns
+      const bool rX = (n - cX * Q) <= 4, rZ = (n - cZ * Q) <= 4;   // only 4 x (z) values exist
+      const int mcode = rY ? (rX ? 3 : 2) : (rX ? 1 : 0), ncode = rW ? (rZ ? 3 : 2) : (rZ ? 1 : 0);
+      orient_dispatch(mcode * 4 + ncode, p, smem, Gs, full, empty, cnt, it.nstage, o, first, &s_pbar, nph);
       first = false;
     }
     if (SCHUR_EXP & 3) continue;   // timing experiment: no epilogue

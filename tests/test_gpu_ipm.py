@@ -94,3 +94,24 @@ def test_ipm_step_config3_runs(pb):
     if s["tp"] == 1.0:
         assert np.linalg.norm(ctx.adjoint(Xd).cpu().numpy() - 1.0) <= 1e-6 * np.sqrt(P.K)
     ctx.close()
+
+
+@pytest.mark.parametrize("key", [2, 3, synth.small_config(9, 2, 1, 2, 1)],
+                         ids=lambda k: str(k) if not isinstance(k, synth.Config) else k.name)
+def test_tiled_factorisation_matches_dense(pb, key):
+    """polya_set_factorization(2): G as pair tiles + blocked Cholesky / solves (the path config 5
+    needs) gives the same iterates as the dense K x K dpotrf path, to 1e-10."""
+    c, A, P = _case(key)
+    X, Z, y, mu = oipm.initial_state(P)
+    runs = []
+    for mode in (1, 2):
+        ctx = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
+        ctx.set_factorization(mode)
+        Xd, Zd, yd = (torch.from_numpy(v.copy()).cuda() for v in (X, Z, y))
+        m = mu
+        for it in range(3):
+            m = ctx.ipm_step(Xd, Zd, yd, m, it)["mu"]
+        runs.append((Xd.cpu().numpy(), Zd.cpu().numpy(), yd.cpu().numpy()))
+        ctx.close()
+    for a, b in zip(runs[0], runs[1]):
+        assert _rel(b, a) <= 1e-10
