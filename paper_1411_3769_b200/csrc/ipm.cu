@@ -143,11 +143,13 @@ __device__ bool smem_chol(double* S, int n) {
   return true;
 }
 
-// W_b = Z_b^{-1} via Cholesky: L^{-1} by columns, then W = L^{-T} L^{-1}; exactly symmetric.
+// W_b = Z_b^{-1} via Cholesky Z = L L^T, X = L^{-1} in place (from X L = I, column by column from
+// the last: X_ij = -(sum_{k=j+1..i} X_ik L_kj) / L_jj), then W = X^T X; exactly symmetric.
+// Shared memory: n^2 + n doubles (n <= 168).
 __global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restrict__ W, int* __restrict__ fail) {
   extern __shared__ double sm[];
-  double* S = sm;           // n*n: Cholesky factor
-  double* Li = sm + n * n;  // n*n: L^{-1} (lower)
+  double* S = sm;           // n*n: L, then X = L^{-1} (lower)
+  double* col = sm + n * n; // n: the column of X being formed
   const int64_t nn = (int64_t)n * n, b = blockIdx.x;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[e] = Z[b * nn + e];
   __syncthreads();
@@ -155,20 +157,22 @@ __global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restr
     if (threadIdx.x == 0) atomicExch(fail, 1);
     return;
   }
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {  // column j of L^{-1}
-    for (int i = 0; i < n; ++i) {
-      if (i < j) { Li[i * n + j] = 0.0; continue; }
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) s -= S[i * n + k] * Li[k * n + j];
-      Li[i * n + j] = s / S[i * n + i];
+  for (int j = n - 1; j >= 0; --j) {
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = j + 1; k <= i; ++k) acc += S[i * n + k] * S[k * n + j];   // X_ik (k > j) * L_kj
+      col[i] = -acc / S[j * n + j];
     }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) S[i * n + j] = col[i];
+    if (threadIdx.x == 0) S[j * n + j] = 1.0 / S[j * n + j];
+    __syncthreads();
   }
-  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
     if (i > j) continue;
     double s = 0.0;
-    for (int k = j; k < n; ++k) s += Li[k * n + i] * Li[k * n + j];  // (L^-T L^-1)_{ij}, k >= max(i,j)
+    for (int k = j; k < n; ++k) s += S[k * n + i] * S[k * n + j];  // (X^T X)_{ij}, k >= max(i,j)
     W[b * nn + (int64_t)i * n + j] = s;
     W[b * nn + (int64_t)j * n + i] = s;
   }
@@ -519,8 +523,8 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     c.last_error = "polya_ipm_step runs on a single rank (distributed factorisation is out of scope)";
     return POLYA_EINVAL;
   }
-  if (c.n * c.n * 2 * (int64_t)sizeof(double) > 220 * 1024) {
-    c.last_error = "polya_ipm_step: block too large for the shared-memory Cholesky (n <= 120)";
+  if ((c.n * c.n + c.n) * (int64_t)sizeof(double) > 227 * 1024) {
+    c.last_error = "polya_ipm_step: block too large for the shared-memory Cholesky (n <= 168)";
     return POLYA_EINVAL;
   }
   cudaStream_t s = (cudaStream_t)stream;
@@ -535,9 +539,9 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     // W = Z^-1
     CK(cudaMemsetAsync(w->fail, 0, sizeof(int), s));
     {
-      CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(2 * (size_t)c.n * c.n * sizeof(double))));
-      k_block_inv<<<(unsigned)c.nb, 128, 2 * (size_t)c.n * c.n * sizeof(double), s>>>((int)c.n, Z, w->W, w->fail);
+      const size_t smi = ((size_t)c.n * c.n + c.n) * sizeof(double);
+      CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
+      k_block_inv<<<(unsigned)c.nb, 128, smi, s>>>((int)c.n, Z, w->W, w->fail);
       ++c.launches;
       CK(cudaGetLastError());
     }
@@ -693,9 +697,9 @@ extern "C" polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, con
       if (res->gap <= opt->eps && res->pinf <= opt->tol) {   // stopping rule
         // every Z block positive definite (reading R10): the blockwise Cholesky of k_block_inv
         CK(cudaMemsetAsync(w->fail, 0, sizeof(int), s));
-        CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(2 * (size_t)c.n * c.n * sizeof(double))));
-        k_block_inv<<<(unsigned)c.nb, 128, 2 * (size_t)c.n * c.n * sizeof(double), s>>>((int)c.n, st->Z, w->W, w->fail);
+        const size_t smi = ((size_t)c.n * c.n + c.n) * sizeof(double);
+        CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
+        k_block_inv<<<(unsigned)c.nb, 128, smi, s>>>((int)c.n, st->Z, w->W, w->fail);
         ++c.launches;
         CK(cudaGetLastError());
         int hfail = 0;
