@@ -24,6 +24,7 @@
 // share a pair's operands in L2.  Every G entry is produced by one CTA in a fixed k order:
 // deterministic, and FULL layouts are bitwise symmetric.
 #include <algorithm>
+#include <type_traits>
 
 #include "polya_internal.h"
 
@@ -38,7 +39,10 @@ constexpr int NT = NT_OVERRIDE;
 #else
 constexpr int NT = (NCW + 1) * 32;  // + one producer warp (cp.async into an mbarrier ring)
 #endif
-constexpr int NSTAGE = 4;  // ring depth
+#ifndef SCHUR_NSTAGE
+#define SCHUR_NSTAGE 4
+#endif
+constexpr int NSTAGE = SCHUR_NSTAGE;  // ring depth
 constexpr int KS = 68;     // doubles per staged 8x8 tile: 64 + 4 pad (conflict-free LDS.64 fragments)
 constexpr int STAGE = 2 * KB * KS;  // doubles per stage: L[8 k][8 x][8 y] + R[8 k][8 z][8 w]
 constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 2 * NSTAGE * sizeof(uint64_t);
@@ -236,11 +240,14 @@ __device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int&
 // One G entry of the item from the folded block: canonical summation order (direct, s-swap,
 // t-swap, both) so that an entry and its mirror image are bitwise equal.  Table entries are
 // {svec index, Gs term direct, Gs term swapped, has swap}.
+template <bool DIAG>
 __device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
   double v = Gs[r.y ^ c.y];
-  if (r.w) v += Gs[r.z ^ c.y];
-  if (c.w) v += Gs[r.y ^ c.z];
-  if (r.w && c.w) v += Gs[r.z ^ c.z];
+  if (DIAG) {   // only items with a diagonal class have swapped terms (no FP64 adds otherwise)
+    if (r.w) v += Gs[r.z ^ c.y];
+    if (c.w) v += Gs[r.y ^ c.z];
+    if (r.w && c.w) v += Gs[r.z ^ c.z];
+  }
   return v;
 }
 
@@ -559,6 +566,8 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
     const int64_t rowbase = (int64_t)it.h * p.Ntil, colbase = (int64_t)it.h2 * p.Ntil;
     double* tile = p.G + (int64_t)it.pl * p.Ntil * p.Ntil;
     const int4 none = make_int4(-1, 0, 0, 0);
+    auto passes = [&](auto diag_tag) {
+      constexpr bool DIAG = decltype(diag_tag)::value;
     {  // pass 0: direct entries G[s][t], lanes along the columns t; 4 rows per warp in flight
       const int4 cA = lane < nc ? s_ct[tb][lane] : none, cB = lane + 32 < nc ? s_ct[tb][lane + 32] : none;
       for (int r0 = warp; r0 < nr; r0 += 4 * NCW) {
@@ -568,8 +577,8 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         for (int u = 0; u < 4; ++u) rw[u] = r0 + u * NCW < nr ? s_rt[tb][r0 + u * NCW] : none;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          vA[u] = (rw[u].x >= 0 && cA.x >= 0) ? gval(Gs, rw[u], cA) : 0.0;
-          vB[u] = (rw[u].x >= 0 && cB.x >= 0) ? gval(Gs, rw[u], cB) : 0.0;
+          vA[u] = (rw[u].x >= 0 && cA.x >= 0) ? gval<DIAG>(Gs, rw[u], cA) : 0.0;
+          vB[u] = (rw[u].x >= 0 && cB.x >= 0) ? gval<DIAG>(Gs, rw[u], cB) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -589,8 +598,8 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         for (int u = 0; u < 4; ++u) cl[u] = c0 + u * NCW < nc ? s_ct[tb][c0 + u * NCW] : none;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          vA[u] = (cl[u].x >= 0 && rA.x >= 0) ? gval(Gs, rA, cl[u]) : 0.0;
-          vB[u] = (cl[u].x >= 0 && rB.x >= 0) ? gval(Gs, rB, cl[u]) : 0.0;
+          vA[u] = (cl[u].x >= 0 && rA.x >= 0) ? gval<DIAG>(Gs, rA, cl[u]) : 0.0;
+          vB[u] = (cl[u].x >= 0 && rB.x >= 0) ? gval<DIAG>(Gs, rB, cl[u]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -601,6 +610,9 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         }
       }
     }
+    };
+    if (dS || dT) passes(std::true_type{});
+    else passes(std::false_type{});
     phase_arrive(&s_pbar, nph);   // this warp is done reading Gs for the item
   }
 }
