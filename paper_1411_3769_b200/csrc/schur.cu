@@ -32,7 +32,11 @@ namespace polya {
 namespace {
 
 constexpr int Q = kChunk;  // 8
-constexpr int KB = 8;      // k terms per pipeline stage
+#ifndef SCHUR_KB
+#define SCHUR_KB 8
+#endif
+constexpr int KB = SCHUR_KB;   // k terms per pipeline stage (a multiple of 4 dividing kKStage)
+static_assert(KB % 4 == 0 && kKStage % KB == 0, "stage size");
 constexpr int NCW = 4;     // consumer (DMMA) warps: each a 4x4 grid of 8x8 tiles of the 64x64 sub-block
 #ifdef NT_OVERRIDE
 constexpr int NT = NT_OVERRIDE;
@@ -140,7 +144,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 #ifndef SCHUR_BULK
-#define SCHUR_BULK 0   // 1: operand rows by cp.async.bulk (measured: per-lane bulk copies serialise in the producer)
+#define SCHUR_BULK 0   // (needs SCHUR_KB == 8) 1: operand rows by cp.async.bulk (measured: per-lane bulk copies serialise in the producer)
 #endif
 // 64-byte row copy global -> shared by the bulk-copy (TMA) engine, completing `bytes` of the
 // mbarrier's transaction count.
@@ -283,7 +287,7 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
       const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
       const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
 #pragma unroll
-      for (int k4 = 0; k4 < 2; ++k4) {
+      for (int k4 = 0; k4 < KB / 4; ++k4) {
         double a[MI], b[NJ];
 #pragma unroll
         for (int i = 0; i < MI; ++i) a[i] = (SCHUR_EXP & 16) ? 1e-3 * (lane + i + k4) : fA[k4 * 4 * KS + i * AST];
