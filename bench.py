@@ -304,7 +304,7 @@ def run_gpu(args, cfg, cid):
         te = max_over_ranks(statistics.mean(e2e_ms))
         e2e = {"value": wg_total / (te * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": te,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
-        del Gh
+        del Gh, Gres
 
     # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step; N=1 only) ----
     ipm = None
