@@ -106,7 +106,7 @@ __device__ __forceinline__ int Tc(int c) {
 #define SCHUR_CA 0   // experiment: L1-allocating cp.async (.ca) instead of .cg
 #endif
 #ifndef SCHUR_L2HINTS
-#define SCHUR_L2HINTS 0   // measured: no gain (v13), kept as an experiment switch
+#define SCHUR_L2HINTS 0   // bit 1: evict-last operand loads, bit 2: evict-first G stores (v13: 3 = +0.5 ms)
 #endif
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t pol;
@@ -115,7 +115,7 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
 }
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, uint64_t pol) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  if (SCHUR_L2HINTS)
+  if (SCHUR_L2HINTS & 1)
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "l"(pol));
   else if (SCHUR_CA)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
@@ -123,7 +123,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src,
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void st_g(double* p, double v) {
-  if (SCHUR_L2HINTS) __stcs(p, v); else *p = v;
+  if (SCHUR_L2HINTS & 2) __stcs(p, v); else *p = v;
 }
 __device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
