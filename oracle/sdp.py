@@ -222,3 +222,44 @@ def schur_probe(P: Problem, Xb, Wb, v):
     Fv = apply_vmap(P, v)
     Y = np.matmul(np.matmul(Wb, Fv), Xb)
     return adjoint_trace(P, Y)
+
+
+def schur_structured(P: Problem, Xb, Wb, pairs=None):
+    """The SCM of Eq. T2 by the rank structure of the blocks (SURVEY 8(c) O6'(iii)/O7), derived here
+    directly from the trace: with F_(h,s)^m = -(H^T E_s + E_s H), H = H_{h,m}, H' = H_{h',m},
+    E_s = sum_{(a1,b1) in or(s)} e_a1 e_b1^T and tr(A e_a1 e_b1^T B e_c1 e_d1^T C) = B[b1,c1] (C A)[d1,a1],
+      tr(F_(h,s) W F_(h',t) X) = sum_{or(s), or(t)} sum_k L_k[b1,c1] R_k[d1,a1]
+    over the four terms (L, R) = (W H'^T, X H^T), (W, H' X H^T), (H W H'^T, X), (H W, H' X) of each
+    Lyapunov block and (beta_hj beta_h'j W_j, X_j) of each P-block.  Per pair (h <= h') the sum over
+    k is one library matmul Raw = [vec L_k]^T [vec R_k] (n^2 x n^2), folded by the four orientation
+    gathers.  pairs: optional list of (h, h') to compute (the rest of G stays zero)."""
+    n, N, L = P.n, P.Ntil, P.L
+    ia, ib = _ab(n)
+    a, b = ia[:, None], ib[:, None]
+    c, d = ia[None, :], ib[None, :]
+    G = np.zeros((P.K, P.K))
+    todo = pairs if pairs is not None else [(h, h2) for h in range(P.L0) for h2 in range(h, P.L0)]
+    for h, h2 in todo:
+        Ls, Rs = [], []
+        for j in range(L):
+            if P.beta[h, j] and P.beta[h2, j]:
+                Ls.append(float(P.beta[h, j] * P.beta[h2, j]) * Wb[j])
+                Rs.append(Xb[j])
+        for m in range(P.M):
+            H, H2 = P.H[h, m], P.H[h2, m]
+            if not (np.any(H) and np.any(H2)):
+                continue
+            W, X = Wb[L + m], Xb[L + m]
+            Ls += [W @ H2.T, W, H @ W @ H2.T, H @ W]
+            Rs += [X @ H.T, H2 @ X @ H.T, X, H2 @ X]
+        if not Ls:
+            continue
+        k = len(Ls)
+        R4 = (np.stack(Ls).reshape(k, n * n).T @ np.stack(Rs).reshape(k, n * n)).reshape(n, n, n, n)
+        sw, tw = a != b, c != d
+        blk = R4[b, c, d, a] + np.where(sw, R4[a, c, d, b], 0.0) + np.where(tw, R4[b, d, c, a], 0.0) \
+            + np.where(sw & tw, R4[a, d, c, b], 0.0)
+        G[h * N:(h + 1) * N, h2 * N:(h2 + 1) * N] = blk
+        if h2 != h:
+            G[h2 * N:(h2 + 1) * N, h * N:(h + 1) * N] = blk.T
+    return G

@@ -362,7 +362,15 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
   case MC * 4 + 1: orient<MI, 2, PY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
   case MC * 4 + 2: orient<MI, 2, PY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
   case MC * 4 + 3: orient<MI, 1, PY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break;
-__device__ __noinline__ void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
+#ifndef SCHUR_DISPATCH_INLINE
+#define SCHUR_DISPATCH_INLINE 0
+#endif
+#if SCHUR_DISPATCH_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
                                              uint64_t* empty, uint32_t& cnt, int nstage, int o, bool first,
                                              uint64_t* pbar, uint32_t& nph) {
   switch (code) {

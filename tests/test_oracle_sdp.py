@@ -166,3 +166,29 @@ def test_config1_unstable_copy_no_certificate():
     T = sdp.apply_vmap(P, y)
     assert max(np.linalg.eigvalsh(-T[P.L + m]).max() for m in range(P.M)) > 0 or \
         min(np.linalg.eigvalsh(T[P.L + m]).min() for m in range(P.M)) < 0
+
+
+@pytest.mark.parametrize("key", [1, "1u", 2, "n5_l1", "n9", "n12", "ex2"])
+def test_schur_structured_equals_literal(key):
+    """oracle.sdp.schur_structured (the rank-structured route of SURVEY O6'(iii), derived from the
+    trace) reproduces the literal Eq. T2 (schur_literal) -- a different computation of the same
+    definition -- including ragged n, l = 1 / d_p = 0, and d_a = 3 (Example 2's A)."""
+    import synth
+    from oracle import polya
+    rng = np.random.default_rng(3)
+    if key == "ex2":
+        from test_oracle_examples import example2_A
+        P = sdp.build_problem(example2_A(0.1), 3, 3, 1, 1, 1, da=3)
+    else:
+        c = {"n5_l1": synth.small_config(5, 1, 0, 2, 3), "n9": synth.small_config(9, 2, 1, 2, 1),
+             "n12": synth.small_config(12, 3, 2, 1, 2)}.get(key) or synth.CONFIGS[key]
+        A = synth.vertex_matrices(c, rng)
+        P = sdp.build_problem(A, c.n, c.l, c.dp, c.d1, c.d2)
+    X, W = synth.spd_blocks(P.n, P.nblocks, rng)
+    G1 = sdp.schur_literal(P, X, W)
+    G2 = sdp.schur_structured(P, X, W)
+    assert np.abs(G1 - G2).max() <= 1e-12 * np.abs(G1).max()
+    # a subset of pairs fills exactly those tiles
+    G3 = sdp.schur_structured(P, X, W, pairs=[(0, P.L0 - 1)])
+    N = P.Ntil
+    assert np.array_equal(G3[:N, (P.L0 - 1) * N:], G2[:N, (P.L0 - 1) * N:])
