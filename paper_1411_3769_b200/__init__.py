@@ -22,7 +22,8 @@ EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
            "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
-           "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization"]
+           "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization", "polya_schur_prepare",
+           "polya_schur_assemble"]
 
 
 class PolyaError(RuntimeError):
@@ -85,6 +86,8 @@ def lib():
     L.polya_apply.argtypes = [vp, vp, vp, vp]
     L.polya_adjoint.argtypes = [vp, vp, vp, vp]
     L.polya_schur.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
+    L.polya_schur_prepare.argtypes = [vp, vp, vp, vp]
+    L.polya_schur_assemble.argtypes = [vp, vp, ctypes.c_int, i64, i64, vp]
     L.polya_ipm_step.argtypes = [vp, ctypes.POINTER(_IpmState), ctypes.POINTER(_IpmStats), vp]
     L.polya_sync.argtypes = [vp]
     L.polya_set_timing.argtypes = [vp, ctypes.c_int]
@@ -268,6 +271,16 @@ class Polya:
         nbn = self.nblocks * self.n ** 2
         self._check(lib().polya_schur(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"), _dev_ptr(G, None, "G"),
                                       layout, _stream_ptr(stream)), "polya_schur")
+        return G
+
+    def schur_prepare(self, X, Zinv, stream=None):
+        nbn = self.nblocks * self.n ** 2
+        self._check(lib().polya_schur_prepare(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"),
+                                              _stream_ptr(stream)), "polya_schur_prepare")
+
+    def schur_assemble(self, G, pair_begin, pair_end, layout=G_PAIR_TILES, stream=None):
+        self._check(lib().polya_schur_assemble(self._h, _dev_ptr(G, None, "G"), layout, int(pair_begin), int(pair_end),
+                                               _stream_ptr(stream)), "polya_schur_assemble")
         return G
 
     def ipm_step(self, X, Z, y, mu, it=0, stream=None):

@@ -702,10 +702,8 @@ extern "C" polya_status polya_adjoint(polya_ctx* ctx, const double* X, double* y
   return POLYA_OK;
 }
 
-extern "C" polya_status polya_schur(polya_ctx* ctx, const double* X, const double* Zinv, double* G, int layout,
-                                    void* stream) {
-  if (!ctx || !X || !Zinv || !G) return POLYA_EINVAL;
-  if (layout != POLYA_G_FULL && layout != POLYA_G_PAIR_TILES) return POLYA_EINVAL;
+extern "C" polya_status polya_schur_prepare(polya_ctx* ctx, const double* X, const double* Zinv, void* stream) {
+  if (!ctx || !X || !Zinv) return POLYA_EINVAL;
   Ctx& c = ctx->c;
   cudaStream_t s = (cudaStream_t)stream;
   try {
@@ -716,12 +714,40 @@ extern "C" polya_status polya_schur(polya_ctx* ctx, const double* X, const doubl
     CU(launch_gemm(c, c.d_items_UV, c.d_terms_UV, c.n_items_UV, s));
     CU(launch_gemm(c, c.d_items_QR, c.d_terms_QR, c.n_items_QR, s));
     if (c.timing) CU(cudaEventRecord(c.ev[1], s));
-    CU(launch_schur(c, G, layout, s));
+  } catch (const Fail& f) {
+    return fail(ctx, f);
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_schur_assemble(polya_ctx* ctx, double* G, int layout, int64_t pair_begin,
+                                             int64_t pair_end, void* stream) {
+  if (!ctx || !G) return POLYA_EINVAL;
+  if (layout != POLYA_G_FULL && layout != POLYA_G_PAIR_TILES) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (pair_begin < 0 || pair_end > c.npairs_local || pair_begin > pair_end) return POLYA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    int64_t i0 = c.item0, i1 = c.item1;
+    if (c.npairs_local > 0) {
+      i0 = std::max(c.item0, c.pair_item_global[c.pair0 + pair_begin]);
+      i1 = std::min(c.item1, c.pair_item_global[c.pair0 + pair_end]);
+    }
+    CU(launch_schur(c, G, layout, i0, i1, s));
     if (c.timing) CU(cudaEventRecord(c.ev[2], s));
   } catch (const Fail& f) {
     return fail(ctx, f);
   }
   return POLYA_OK;
+}
+
+extern "C" polya_status polya_schur(polya_ctx* ctx, const double* X, const double* Zinv, double* G, int layout,
+                                    void* stream) {
+  if (!ctx || !X || !Zinv || !G) return POLYA_EINVAL;
+  if (layout != POLYA_G_FULL && layout != POLYA_G_PAIR_TILES) return POLYA_EINVAL;
+  polya_status st = polya_schur_prepare(ctx, X, Zinv, stream);
+  if (st != POLYA_OK) return st;
+  return polya_schur_assemble(ctx, G, layout, 0, ctx->c.npairs_local, stream);
 }
 
 extern "C" polya_status polya_set_timing(polya_ctx* ctx, int enable) {

@@ -111,7 +111,7 @@ cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, in
 cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
 cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s);
 cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
-cudaError_t launch_schur(Ctx& c, double* G, int layout, cudaStream_t s);
+cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t item0, int64_t item1, cudaStream_t s);
 
 }  // namespace polya
 

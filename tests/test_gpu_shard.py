@@ -101,3 +101,27 @@ def test_reduce_without_nccl_or_tiles_mode_fails_loudly(pb):
         b.reduce_G(G, out=G)                         # no communicator yet
     t.close()
     b.close()
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS[2], synth.small_config(12, 3, 2, 1, 2)], ids=lambda c: c.name)
+@pytest.mark.parametrize("world", [1, 3])
+def test_chunked_assembly_is_bitwise_the_full_call(pb, cfg, world):
+    """polya_schur_prepare + polya_schur_assemble over pair chunks (the streaming form bench.py's e2e
+    uses) writes exactly the entries polya_schur writes, bit for bit, for every rank's share."""
+    A, X, W = _inputs(cfg)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    for r in range(world):
+        ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=world)
+        npl = ctx.dims["pair1"] - ctx.dims["pair0"]
+        for layout in (pb.G_PAIR_TILES, pb.G_FULL):
+            ref = ctx.schur(Xd, Wd, layout=layout)
+            G = torch.zeros_like(ref)
+            ctx.schur_prepare(Xd, Wd)
+            cuts = sorted({0, npl // 3, (2 * npl) // 3, npl})
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                ctx.schur_assemble(G, a, b, layout=layout)
+            torch.cuda.synchronize()
+            assert torch.equal(G, ref)
+        with pytest.raises(pb.PolyaError):
+            ctx.schur_assemble(G, 0, npl + 1, layout=pb.G_FULL)
+        ctx.close()
