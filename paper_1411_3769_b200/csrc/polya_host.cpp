@@ -362,9 +362,8 @@ void build(Ctx& c, const double* A_host, bool device = true) {
 
   // ---- Schur tables for this rank's pairs ------------------------------------------------------
   {
-    std::vector<int32_t> qh, qh2, kL, kR, kf;
+    std::vector<int32_t> qh, qh2, kL, kR;
     std::vector<int64_t> kbeg, pitem;
-    std::vector<double> ks;
     std::vector<GemmItem> it;
     std::vector<GemmTerm> tm;
     int64_t q = 0;
@@ -387,22 +386,21 @@ void build(Ctx& c, const double* A_host, bool device = true) {
         ++q;
         // T1 = U_{h'}^T[b1,c1] V_h^T[d1,a1]; T2 = X[b1,c1] R_{h'h}[d1,a1];
         // T3 = Q_{hh'}[b1,c1] W[d1,a1];     T4 = U_h[b1,c1] V_{h'}[d1,a1]   (O7)
-        kL.push_back((int32_t)(c.id_Ut + th2)); kR.push_back((int32_t)(c.id_Vt + th)); kf.push_back(0); ks.push_back(1.0);
-        kL.push_back((int32_t)(c.id_X + b));   kR.push_back(idR);                     kf.push_back(0); ks.push_back(1.0);
-        kL.push_back(idQ);                     kR.push_back((int32_t)(c.id_W + b));   kf.push_back(0); ks.push_back(1.0);
-        kL.push_back((int32_t)(c.id_U + th));  kR.push_back((int32_t)(c.id_V + th2)); kf.push_back(0); ks.push_back(1.0);
+        kL.push_back((int32_t)(c.id_Ut + th2)); kR.push_back((int32_t)(c.id_Vt + th));
+        kL.push_back((int32_t)(c.id_X + b));   kR.push_back(idR);                    
+        kL.push_back(idQ);                     kR.push_back((int32_t)(c.id_W + b));  
+        kL.push_back((int32_t)(c.id_U + th));  kR.push_back((int32_t)(c.id_V + th2));
       }
       for (int64_t j = 0; j < c.L; ++j) {
         int64_t b1 = c.beta[h * c.L + j], b2 = c.beta[h2 * c.L + j];
         if (!b1 || !b2 || !owned(j)) continue;
         // P-block term beta_hj beta_h'j X_j (x) W_j as (beta_hj X_j) (x) (beta_h'j W_j)
         kL.push_back((int32_t)(c.id_Xb + bidx[h * c.L + j])); kR.push_back((int32_t)(c.id_Wb + bidx[h2 * c.L + j]));
-        kf.push_back(0); ks.push_back(1.0);
       }
       // zero terms up to a whole stage; a pair with no common block still gets one (all-zero)
       // stage so that every work item flows through the K4 pipeline
       while ((int64_t)(kL.size() - kbeg.back()) % kKStage || (int64_t)kL.size() == kbeg.back()) {
-        kL.push_back((int32_t)c.id_Zero); kR.push_back((int32_t)c.id_Zero); kf.push_back(0); ks.push_back(0.0);
+        kL.push_back((int32_t)c.id_Zero); kR.push_back((int32_t)c.id_Zero);
       }
       kbeg.push_back((int64_t)kL.size());
       pitem.push_back(c.pair_item_global[p + 1]);
@@ -415,10 +413,6 @@ void build(Ctx& c, const double* A_host, bool device = true) {
     c.st.pair_h2 = dupload(qh2);
     c.st.pair_kbeg = dupload(kbeg);
     c.st.pair_item = dupload(pitem);
-    c.st.k_L = dupload(kL);
-    c.st.k_R = dupload(kR);
-    c.st.k_flags = dupload(kf);
-    c.st.k_scale = dupload(ks);
     {
       std::vector<int2> kd(kL.size());
       for (size_t i = 0; i < kL.size(); ++i) kd[i] = make_int2(kL[i], kR[i]);
@@ -463,10 +457,10 @@ void build(Ctx& c, const double* A_host, bool device = true) {
 }
 
 void free_ctx(Ctx& c) {
-  void* ps[] = {c.arena, c.dA, c.dHw, c.dHm, c.dHgam, c.d_items_UV, c.d_terms_UV, c.d_items_QR, c.d_terms_QR,
+  void* ps[] = {c.arena, c.dA, c.dHw, c.d_items_UV, c.d_terms_UV, c.d_items_QR, c.d_terms_QR,
                 c.d_items_T, c.d_terms_T, c.d_sc_dst, c.d_sc_src, c.d_sc_w, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
-                c.st.pair_kbeg, c.st.pair_item, c.st.k_L, c.st.k_R, c.st.k_flags, c.st.k_scale, c.st.kdesc,
+                c.st.pair_kbeg, c.st.pair_item, c.st.kdesc,
                 c.st.cls_a, c.st.cls_b, c.st.counter};
   for (void* p : ps)
     if (p) cudaFree(p);

@@ -32,11 +32,7 @@ struct SchurTables {
   int32_t* pair_h2 = nullptr;     // [npairs_local]      h' (column block), h <= h'
   int64_t* pair_kbeg = nullptr;   // [npairs_local + 1]  k-entry range of each pair
   int64_t* pair_item = nullptr;   // [npairs_local + 1]  global work-item prefix (offset item_base)
-  int32_t* k_L = nullptr;         // [nk] arena id of the left factor  L_k
-  int32_t* k_R = nullptr;         // [nk] arena id of the right factor R_k
-  int32_t* k_flags = nullptr;     // [nk] bit0: L transposed, bit1: R transposed
-  double* k_scale = nullptr;      // [nk] scale of L_k (beta_h beta_h' on P-block terms, else 1)
-  int2* kdesc = nullptr;          // [nk] arena matrix ids (L_k, R_k) for K4
+  int2* kdesc = nullptr;          // [nk] arena matrix ids (L_k, R_k) of the pair k-lists for K4
   int32_t* cls_a = nullptr;       // [ncls] chunk index i of class (i <= j)
   int32_t* cls_b = nullptr;       // [ncls] chunk index j
   unsigned long long* counter = nullptr;  // dynamic work counter
@@ -72,8 +68,6 @@ struct Ctx {
   double* arena = nullptr;
   double* dA = nullptr;
   double* dHw = nullptr;
-  int32_t* dHm = nullptr;   // [nnzH] (h, m) for setup_H: packed pairs
-  int32_t* dHgam = nullptr; // [nnzH][nA][l] unused placeholder
   // batched gemm descriptors
   GemmItem* d_items_UV = nullptr; GemmTerm* d_terms_UV = nullptr; int64_t n_items_UV = 0;
   GemmItem* d_items_QR = nullptr; GemmTerm* d_terms_QR = nullptr; int64_t n_items_QR = 0;

@@ -143,22 +143,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-#ifndef SCHUR_BULK
-#define SCHUR_BULK 0   // (needs SCHUR_KB == 8) 1: operand rows by cp.async.bulk (measured: per-lane bulk copies serialise in the producer)
-#endif
-// 64-byte row copy global -> shared by the bulk-copy (TMA) engine, completing `bytes` of the
-// mbarrier's transaction count.
-__device__ __forceinline__ void bulk_row(void* smem_dst, const void* gmem_src, uint64_t* bar, unsigned bytes) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   sptr(smem_dst)),
-               "l"(gmem_src), "r"(bytes), "r"(sptr(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(sptr(bar)),
-               "r"(bytes)
-               : "memory");
-}
 // Consumer phases (each fold of an orientation, each item's epilogue) are ordered by one mbarrier
 // with one arrival per consumer warp: a warp arrives when its part of a phase is done and waits
 // for the previous phase only right before it touches Gs again, so a warp that finishes a fold
@@ -235,7 +219,7 @@ __device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int&
 
 #ifndef SCHUR_EXP
 #define SCHUR_EXP 0   // timing experiments only (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either,
-                      // 4 = no operand loads, 8 = no ragged-warp skip, 16 = no fragment LDS
+                      // 4 = no operand loads (results wrong by construction: never a bench value)
 #endif
 #ifndef SCHUR_MINB
 #define SCHUR_MINB 3
@@ -271,7 +255,6 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
                                        uint64_t* pbar, uint32_t& nph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int m0 = MI * (warp >> 1), n0 = NJ * (warp & 1);   // the warp's first M-tile and N-tile
-  constexpr bool active = true;
   constexpr int AST = PY ? 2 * Q : Q, BST = PW ? 2 * Q : Q;   // fragment strides per tile
   const int aoff = PY ? (2 * m0 + (g >> 2)) * Q + (g & 3) : m0 * Q + g;
   const int boff = PW ? (2 * n0 + (g >> 2)) * Q + (g & 3) : n0 * Q + g;
@@ -283,21 +266,19 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
   for (int s = 0; s < nstage; ++s) {
     const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
     mbar_wait(full + slot, ph);
-    if (active) {
-      const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
-      const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
+    const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
+    const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
 #pragma unroll
-      for (int k4 = 0; k4 < KB / 4; ++k4) {
-        double a[MI], b[NJ];
+    for (int k4 = 0; k4 < KB / 4; ++k4) {
+      double a[MI], b[NJ];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[i] = (SCHUR_EXP & 16) ? 1e-3 * (lane + i + k4) : fA[k4 * 4 * KS + i * AST];
+      for (int i = 0; i < MI; ++i) a[i] = fA[k4 * 4 * KS + i * AST];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) b[j] = (SCHUR_EXP & 16) ? 1e-3 * (lane - j + s) : fB[k4 * 4 * KS + j * BST];
+      for (int j = 0; j < NJ; ++j) b[j] = fB[k4 * 4 * KS + j * BST];
 #pragma unroll
-        for (int i = 0; i < MI; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      }
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + slot);
@@ -402,7 +383,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   }
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(full + i, SCHUR_BULK ? 1 : 33);   // lane 0's arrive(.expect_tx) (+ 32 cp.async completions)
+      mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
       mbar_init(empty + i, NCW);
     }
     mbar_init(&s_pbar, NCW);
@@ -448,10 +429,6 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         roles(o, it, cX, cY, cZ, cW);
         const int offL = (cX * Q + sr) * np + cY * Q + 2 * sc2;
         const int offR = (cZ * Q + sr) * np + cW * Q + 2 * sc2;
-        // bulk mode: lane copies rows 4(lane&1) .. +3 of tile lane>>1 (tiles 0-7: L_k, 8-15: R_k)
-        const int btile = lane >> 1, brow = 4 * (lane & 1);
-        const int boff = btile < KB ? (cX * Q + brow) * np + cY * Q : (cZ * Q + brow) * np + cW * Q;
-        double* bdst0 = smem + (btile < KB ? btile * KS : KB * KS + (btile - KB) * KS) + brow * Q;
         int2 dcur = dfirst;
         for (int s = 0; s < it.nstage; ++s) {
           // descriptors of the next stage: the next k-block, or the first one again (the next
@@ -467,21 +444,6 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
             s_info[slot] = si;
           }
           first_stage = false;
-          if (SCHUR_BULK) {
-            const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, btile & (KB - 1));
-            const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, btile & (KB - 1));
-            if (lane == 0) mbar_arrive_expect_tx(full + slot, (SCHUR_EXP & 4) ? 0u : 2u * KB * Q * Q * 8u);   // releases s_info
-            __syncwarp();
-            if (!(SCHUR_EXP & 4)) {
-              const double* src = p.arena + (uint64_t)(btile < KB ? idL : idR) * p.ms32 + boff;
-              double* dst = bdst0 + slot * STAGE;
-#pragma unroll
-              for (int r = 0; r < 4; ++r) bulk_row(dst + r * Q, src + r * np, full + slot, Q * 8);
-            }
-            dcur = dnext;
-            ++cnt;
-            continue;
-          }
           double* T = smem + slot * STAGE + sr * Q + 2 * sc2;
 #pragma unroll
           for (int kk = 0; kk < KB; ++kk) {
@@ -506,7 +468,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
       const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
       mbar_wait(empty + slot, ph ^ 1);
       if (lane == 0) s_info[slot].item = p.item1;
-      if (!SCHUR_BULK) cp_async_mbar_arrive(full + slot);
+      cp_async_mbar_arrive(full + slot);
       if (lane == 0) mbar_arrive(full + slot);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");

@@ -197,3 +197,24 @@ def test_schur_large_sampled_and_probe(pb, cfg_id, layout, nsamp):
     del G
     ctx.close()
     torch.cuda.empty_cache()
+
+
+def test_schur_more_ranks_than_items(pb):
+    """Config 1 has 3 work items; with 8 ranks most shares are empty (allowed): those ranks
+    write nothing, polya_schur returns OK, and the union is still G bit for bit."""
+    cfg = synth.CONFIGS[1]
+    ctx, A, X, W = _setup(pb, cfg)
+    Xd, Wd = _dev(X), _dev(W)
+    G1 = ctx.schur(Xd, Wd)
+    ctx.close()
+    G = torch.full_like(G1, float("nan"))
+    empty = 0
+    for r in range(8):
+        c = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=8)
+        empty += c.dims["item1"] == c.dims["item0"]
+        if c.dims["item1"] == c.dims["item0"]:
+            assert c.dims["useful_flops_schur"] == 0.0
+        c.schur(Xd, Wd, G=G)
+        c.close()
+    assert empty >= 5
+    assert torch.equal(G, G1)
