@@ -12,17 +12,20 @@
 // (M = N = n^2, inner dimension K_pair = 4 mu_hh' + nu_hh') and G is a fold of Raw in which
 // every raw entry is added to exactly one G entry.
 //
-// Work item = (pair, row class {i<=j}, column class {k<=l}) of 8-index chunks.  A CTA of 4 warps
-// computes the <= 4 raw 64x64 sub-blocks of the item (one per orientation) with FP64 DMMA
-// (mma.sync m8n8k4 -> DMMA.8x8x4; sm_100a has no f64 tcgen05 kind), each warp a 4x4 grid of
-// 8x8 MMA tiles.  Operands go global -> registers -> shared memory in a k-interleaved layout
-// [x][y][slot(k)] so one LDS.128 feeds the fragments of two k-steps (8 LDS.128 per 32 DMMA);
-// loads of stage s+1 are in flight while stage s computes.  Each orientation is folded into a
-// 32 KB XOR-swizzled shared G-block (conflict-free for all four orientations), and the item's
-// G entries are written with diagonal-ordered (contiguous-run) stores plus mirror stores.
-// Persistent CTAs pull items from an atomic counter in pair-major order so co-running CTAs
-// share a pair's operands in L2.  Every G entry is produced by one CTA in a fixed k order:
-// deterministic, and FULL layouts are bitwise symmetric.
+// Work item = (pair, row class {i<=j}, column class {k<=l}) of 8-index chunks.  A CTA (160
+// threads, 3 per SM) computes the <= 4 raw 64x64 sub-blocks of the item (one per orientation)
+// with FP64 DMMA (mma.sync m8n8k4 -> DMMA.8x8x4; sm_100a has no f64 tcgen05 kind):
+//  * a producer warp pulls items from an atomic counter (pair-major, so co-running CTAs share a
+//    pair's operands in L2), one item ahead, and streams each orientation's k-list in stages of
+//    8 terms (16 8x8 operand tiles, 16-byte cp.async) into a 4-slot mbarrier ring (tile stride
+//    68 doubles: conflict-free fragment loads);
+//  * 4 consumer warps split the valid M / N tiles 2 x 2 (4x4 DMMA tiles per warp, fewer for the
+//    ragged last chunk of n, whose rows are packed two x-values per tile), fold each orientation
+//    into a 32 KB XOR-swizzled shared G-block (conflict-free for all four orientations), ordered by
+//    a phase mbarrier instead of CTA barriers, and write the item's G entries with table-driven,
+//    diagonal-ordered (contiguous-run) stores plus mirror stores (FULL layout, diagonal pairs).
+// Every G entry is produced by one CTA in a fixed k order: deterministic, and FULL layouts are
+// bitwise symmetric.  DESIGN.md 5.2 has the measurements and the variants that were tried.
 #include <algorithm>
 #include <type_traits>
 
