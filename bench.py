@@ -8,11 +8,16 @@ on config 4 (n=100, l=4, dp=2, d1=d2=4; K=50,500, 204 Polya blocks) by default.
 value = W_G / t_step (TFLOP/s), W_G = n^4 (sum nu^2 + 4 sum mu^2) the algorithmic FP64 FLOPs
 of the Schur assembly; t_step is the max over ranks.
 
-Launch: python bench.py [--gpus N --steps K --warmup W --config 4]
-        torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU; output-tile
-        sharding of G: no inter-GPU traffic on the data path, NCCL only for the barrier and
-        the max-over-ranks timing)
+Launch: python bench.py [--gpus N --steps K --warmup W --config 4|5 --shard tiles|blocks]
+        torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU; default output-tile
+        sharding of G: no inter-GPU traffic on the data path, NCCL only for the barrier and the
+        max-over-ranks timing; --shard blocks: the paper's Polya-block partition with the partial
+        G summed by NCCL ReduceScatter inside the step)
         python bench.py --impl reference ...   (the CPU oracle, rank 0 only)
+The JSON line also carries the roofline of the dominant kernel (K4), the CPU-oracle baseline,
+an end-to-end figure through the public API (pinned host inputs in, all of G back out, streamed
+during the assembly), the seconds per IPM iteration (N = 1) and the SM clocks sampled during
+the timed region.
 """
 from __future__ import annotations
 
