@@ -179,7 +179,9 @@ polya_status polya_schur_assemble(polya_ctx* ctx, double* G_dev, int layout, int
  * readings R3-R6, on a single rank (nranks must be 1).  State lives on the device:
  * X, Z: double[nblocks][n][n] (symmetric PD), y: double[K]; updated in place.
  * mu is the barrier parameter of the previous step (Eq. mu).
- * The K x K factorisation uses cuSOLVER dpotrf/dpotrs (timed separately in stats).
+ * The K x K factorisation uses cuSOLVER dpotrf/dpotrs (timed separately in stats); if G is not
+ * numerically positive definite it is re-assembled and factorised once more as G + eps I,
+ * eps = 1e-12 tr(G) / K, before ENOTPD is returned.
  * Synchronous (returns after the step).  Errors: ENOTPD, ESTEP, ECUDA, ENOMEM.   */
 typedef struct { double* X; double* Z; double* y; double mu; int32_t iter; } polya_ipm_state;
 typedef struct {
@@ -188,6 +190,7 @@ typedef struct {
   double tp, td;   /* primal / dual step sizes (R5)                                  */
   double phi, psi; /* primal cost tr(C X), dual cost a^T y                            */
   float ms_schur, ms_factor, ms_other;
+  int32_t reg_retries;   /* 1 if G needed the regularised retry G + 1e-12 tr(G)/K I */
 } polya_ipm_stats;
 polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, polya_ipm_stats* stats, void* stream);
 

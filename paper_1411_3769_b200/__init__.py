@@ -61,7 +61,7 @@ class _SolveResult(ctypes.Structure):
 class _IpmStats(ctypes.Structure):
     _fields_ = [("gap", ctypes.c_double), ("mu", ctypes.c_double), ("tp", ctypes.c_double), ("td", ctypes.c_double),
                 ("phi", ctypes.c_double), ("psi", ctypes.c_double), ("ms_schur", ctypes.c_float),
-                ("ms_factor", ctypes.c_float), ("ms_other", ctypes.c_float)]
+                ("ms_factor", ctypes.c_float), ("ms_other", ctypes.c_float), ("reg_retries", ctypes.c_int32)]
 
 
 _lib = None

@@ -309,6 +309,33 @@ __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__
   if (threadIdx.x == 0 && !(lyap && pos)) atomicAdd(nfail, 1);
 }
 
+// Diagonal of the Schur complement, dense (K x K) or tiled (diagonal pair tiles, Ntil x Ntil):
+// element q of the diagonal sits at G + q*(K+1) (dense) or tile(h,h) + s*(Ntil+1), q = h*Ntil + s.
+__device__ __forceinline__ int64_t diag_off(int64_t q, int64_t K, int64_t Ntil, int64_t L0, int tiled) {
+  if (!tiled) return q * (K + 1);
+  const int64_t h = q / Ntil, s = q - h * Ntil;
+  const int64_t p = h * L0 - h * (h - 1) / 2;   // pair index of (h, h)
+  return p * Ntil * Ntil + s * (Ntil + 1);
+}
+__global__ void k_diag_sum(const double* __restrict__ G, int64_t K, int64_t Ntil, int64_t L0, int tiled,
+                           double* __restrict__ part) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x)
+    acc += G[diag_off(q, K, Ntil, L0, tiled)];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void k_diag_shift(double* __restrict__ G, int64_t K, int64_t Ntil, int64_t L0, int tiled, double shift) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < K; q += (int64_t)gridDim.x * blockDim.x)
+    G[diag_off(q, K, Ntil, L0, tiled)] += shift;
+}
+
 struct Ipm {
   int64_t nb = 0, n = 0, K = 0;
   double *W = nullptr, *Rd = nullptr, *T1 = nullptr, *T2 = nullptr, *dX1 = nullptr, *dZ1 = nullptr, *dX2 = nullptr,
@@ -509,6 +536,24 @@ void tiled_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
   c.launches += 2 * T * (T + 1) / 2 + 2 * T;
 }
 
+// Cholesky of the Schur complement (dense or tiled); false if not positive definite.
+bool factor(Ctx& c, Ipm* w, cudaStream_t s) {
+  if (w->tiled) {
+    try {
+      tiled_potrf(c, w, s);
+    } catch (const IpmFail& f) {
+      if (f.s == POLYA_ENOTPD) return false;
+      throw;
+    }
+    return true;
+  }
+  CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, w->work, w->lwork, w->info));
+  int hinfo = 0;
+  CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return hinfo == 0;
+}
+
 polya_status call(polya_status st, Ctx& c) {
   if (st != POLYA_OK) throw IpmFail{st, c.last_error};
   return st;
@@ -557,21 +602,36 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     CK(cudaGetLastError());
     // G (FULL layout), then its Cholesky factor (timed separately)
     CK(cudaEventRecord(w->ev[1], s));
-    call(polya_schur(ctx, X, w->W, w->G, w->tiled ? POLYA_G_PAIR_TILES : POLYA_G_FULL, s), c);
+    const int glayout = w->tiled ? POLYA_G_PAIR_TILES : POLYA_G_FULL;
+    call(polya_schur(ctx, X, w->W, w->G, glayout, s), c);
     CK(cudaEventRecord(w->ev[2], s));
-    if (w->tiled) {
-      CK(cudaMemsetAsync(w->info, 0, sizeof(int), s));
-      tiled_potrf(c, w, s);
-    } else {
-      CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, w->G, (int)c.K, w->work, w->lwork, w->info));
-    }
-    CK(cudaEventRecord(w->ev[3], s));
-    int hinfo = 0, hfail = 0;
-    CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int hfail = 0;
     CK(cudaMemcpyAsync(&hfail, w->fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (hfail) throw IpmFail{POLYA_ENOTPD, "a Z block is not positive definite"};
-    if (hinfo != 0) throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite (potrf info " + std::to_string(hinfo) + ")"};
+    int retries = 0;
+    if (!factor(c, w, s)) {
+      // G near-singular (it becomes ill-conditioned near convergence): one retry on G + eps I with
+      // eps = 1e-12 tr(G) / K (SURVEY 8(b) ENOTPD).  potrf destroyed G: re-assemble it.
+      call(polya_schur(ctx, X, w->W, w->G, glayout, s), c);
+      const int tiled = w->tiled ? 1 : 0;
+      k_diag_sum<<<kScalarBlocks, 256, 0, s>>>(w->G, c.K, c.Ntil, c.L0, tiled, w->part);
+      ++c.launches;
+      CK(cudaGetLastError());
+      std::vector<double> part(kScalarBlocks);
+      CK(cudaMemcpyAsync(part.data(), w->part, kScalarBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double tr = 0.0;
+      for (double v : part) tr += v;
+      const double eps = 1e-12 * std::fabs(tr) / (double)c.K;
+      k_diag_shift<<<kScalarBlocks, 256, 0, s>>>(w->G, c.K, c.Ntil, c.L0, tiled, eps);
+      ++c.launches;
+      CK(cudaGetLastError());
+      retries = 1;
+      if (!(eps > 0.0) || !factor(c, w, s))
+        throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite after one regularised retry"};
+    }
+    CK(cudaEventRecord(w->ev[3], s));
     // dy^ = G^-1 O1
     CK(cudaMemcpyAsync(w->dy1, w->O1, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (w->tiled) tiled_potrs(c, w, w->dy1, s);
@@ -638,6 +698,7 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
       stats->ms_schur = a;
       stats->ms_factor = b;
       stats->ms_other = tot - a - b;
+      stats->reg_retries = retries;
     }
   } catch (const IpmFail& f) {
     c.last_error = f.msg;
