@@ -67,61 +67,81 @@ __global__ void k_scale_copy(double* __restrict__ arena, int64_t ms, const int32
   }
 }
 
-// Batched GEMM on np x np arena matrices; CTA = one 32x32 tile of one output matrix, 4 warps,
-// each warp a 16x16 block = 2x2 DMMA m8n8 tiles.  K is staged 8 at a time through shared memory
-// in k-major layout (row stride 40 doubles: conflict-free fragment reads).
+// Batched GEMM on np x np arena matrices: C[c_id] = sum_terms alpha A[a_id] op(B[b_id]).  CTA = one
+// 32x32 tile of one output matrix, 4 warps, each a 16x16 block = 2x2 DMMA m8n8 tiles.  The K
+// dimension of all terms is streamed in chunks of 8 through a 2-stage cp.async double buffer:
+// A as [i][k] (row stride 12 doubles), B as [k][j] (stride 36) or, transposed, [j][k] (stride 12),
+// so every fragment load of a half-warp hits 16 distinct bank slots.
 constexpr int GT = 32;
-constexpr int GS = 40;
+constexpr int AS = 12;
+constexpr int BSN = 36;
+constexpr int BBUF = GT * AS > 8 * BSN ? GT * AS : 8 * BSN;
+__device__ __forceinline__ void cp16z(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
+}
 __global__ void __launch_bounds__(128) k_gemm(double* __restrict__ arena, int64_t ms, int np,
                                               const GemmItem* __restrict__ items,
                                               const GemmTerm* __restrict__ terms, int tiles) {
-  __shared__ __align__(16) double As[8 * GS];
-  __shared__ __align__(16) double Bs[8 * GS];
+  __shared__ __align__(16) double As[2][GT * AS];
+  __shared__ __align__(16) double Bs[2][BBUF];
   const GemmItem it = items[blockIdx.y];
   const int ti = blockIdx.x / tiles, tj = blockIdx.x - ti * tiles;
   const int i0 = ti * GT, j0 = tj * GT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int wr = (warp >> 1) * 16, wc = (warp & 1) * 16;
-  double acc[2][2][2] = {};
-  for (int q = it.tbeg; q < it.tend; ++q) {
-    const GemmTerm tm = terms[q];
+  const int nk = np / 8, total = (it.tend - it.tbeg) * nk;
+  auto issue = [&](int c, int buf) {
+    const GemmTerm tm = terms[it.tbeg + c / nk];
+    const int k0 = (c % nk) * 8;
     const double* A = arena + (int64_t)tm.a_id * ms;
     const double* B = arena + (int64_t)tm.b_id * ms;
-    for (int k0 = 0; k0 < np; k0 += 8) {
-      {  // A: 32 rows x 8 k -> As[k][i]
-        const int idx = tid * 2, i = idx >> 3, k = idx & 7;
-        double2 v = make_double2(0.0, 0.0);
-        if (i0 + i < np) v = *reinterpret_cast<const double2*>(A + (int64_t)(i0 + i) * np + k0 + k);
-        As[k * GS + i] = tm.alpha * v.x;
-        As[(k + 1) * GS + i] = tm.alpha * v.y;
-      }
-      if (!tm.transB) {  // B[k][j]: 8 k x 32 j
-        const int idx = tid * 2, k = idx >> 5, j = idx & 31;
-        double2 v = make_double2(0.0, 0.0);
-        if (j0 + j < np) v = *reinterpret_cast<const double2*>(B + (int64_t)(k0 + k) * np + j0 + j);
-        *reinterpret_cast<double2*>(&Bs[k * GS + j]) = v;
-      } else {  // B[k][j] = Bm[j][k]
-        const int idx = tid * 2, j = idx >> 3, k = idx & 7;
-        double2 v = make_double2(0.0, 0.0);
-        if (j0 + j < np) v = *reinterpret_cast<const double2*>(B + (int64_t)(j0 + j) * np + k0 + k);
-        Bs[k * GS + j] = v.x;
-        Bs[(k + 1) * GS + j] = v.y;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        double a[2], b[2];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) a[mi] = As[(ks * 4 + t) * GS + wr + mi * 8 + g];
-#pragma unroll
-        for (int nj = 0; nj < 2; ++nj) b[nj] = Bs[(ks * 4 + t) * GS + wc + nj * 8 + g];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
-      }
-      __syncthreads();
+    {  // A rows i0..i0+31, columns k0..k0+7: one 16-byte copy per thread
+      const int i = tid >> 2, kc = (tid & 3) * 2;
+      const bool v = i0 + i < np;
+      cp16z(&As[buf][i * AS + kc], v ? A + (int64_t)(i0 + i) * np + k0 + kc : A, v);
     }
+    if (!tm.transB) {  // B rows k0..k0+7, columns j0..j0+31
+      const int k = tid >> 4, jc = (tid & 15) * 2;
+      const bool v = j0 + jc < np;
+      cp16z(&Bs[buf][k * BSN + jc], v ? B + (int64_t)(k0 + k) * np + j0 + jc : B, v);
+    } else {           // op(B)[k][j] = B[j][k]: rows j0..j0+31 of B, columns k0..k0+7
+      const int j = tid >> 2, kc = (tid & 3) * 2;
+      const bool v = j0 + j < np;
+      cp16z(&Bs[buf][j * AS + kc], v ? B + (int64_t)(j0 + j) * np + k0 + kc : B, v);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double acc[2][2][2] = {};
+  if (total > 0) issue(0, 0);
+  for (int c = 0; c < total; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < total) {
+      issue(c + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const GemmTerm tm = terms[it.tbeg + c / nk];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      double a[2], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) a[mi] = As[buf][(wr + mi * 8 + g) * AS + ks * 4 + t];
+      if (tm.alpha != 1.0) {
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) a[mi] *= tm.alpha;
+      }
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+        b[nj] = tm.transB ? Bs[buf][(wc + nj * 8 + g) * AS + ks * 4 + t] : Bs[buf][(ks * 4 + t) * BSN + wc + nj * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+    }
+    __syncthreads();   // the buffer is refilled by the issue of chunk c + 2
   }
   double* C = arena + (int64_t)it.c_id * ms;
 #pragma unroll
