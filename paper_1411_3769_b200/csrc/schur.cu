@@ -268,7 +268,17 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int s = 0; s < nstage; ++s) {
     const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
+#if SCHUR_EXP & 64   // experiment: histogram of consumer waits on `full` by stage index (warp 0, lane 0)
+    const long long w0 = clock64();
     mbar_wait(full + slot, ph);
+    if (tid == 0) {
+      const int bkt = s < 4 ? s : (s == nstage - 1 ? 5 : 4);
+      atomicAdd(p.G + (int64_t)p.npl * p.Ntil * p.Ntil + bkt, (double)(clock64() - w0));
+      atomicAdd(p.G + (int64_t)p.npl * p.Ntil * p.Ntil + 8 + bkt, 1.0);
+    }
+#else
+    mbar_wait(full + slot, ph);
+#endif
     const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
     const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
 #pragma unroll
