@@ -263,7 +263,7 @@ polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, const polya_so
  * with P(alpha) = sum_h alpha^h V_h(y) (reading R7; y_dev: double[K] on the device) and A(alpha) the
  * set-up's A, counts the points alpha = pts_host[p] (double[npts][l], host, points of the simplex)
  * where P(alpha) > 0 or -(A^T P + P A)(alpha) > 0 fails a Cholesky test, into *nfail_out.
- * One CTA per point on the device; n <= 64.  Synchronous.                                     */
+ * One CTA per point on the device; n <= 118.  Synchronous.                                     */
 polya_status polya_verdict(polya_ctx* ctx, const double* y_dev, int32_t npts, const double* pts_host,
                            int32_t* nfail_out, void* stream);
 

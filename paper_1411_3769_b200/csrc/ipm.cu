@@ -270,14 +270,17 @@ __global__ void k_identity(int64_t total, int n, double* __restrict__ X, double*
 //   P(alpha) = sum_h alpha^h V_h(y)   (reading R7; V_h in the arena after k_vmap)
 //   A(alpha) = sum_lambda alpha^lambda A_lambda
 // and the test P(alpha) > 0, -(A^T P + P A)(alpha) > 0 by in-shared-memory Cholesky.
+// Shared memory: P(alpha) and A(alpha) (2 n^2 doubles, n <= 118); -(A^T P + P A) is formed in a
+// per-point global scratch and copied over A for its Cholesky test.
 __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__ Wp, const int32_t* __restrict__ Wa,
                        const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
-                       const double* __restrict__ A, const double* __restrict__ pts, int* __restrict__ nfail) {
+                       const double* __restrict__ A, const double* __restrict__ pts, double* __restrict__ scratch,
+                       int* __restrict__ nfail) {
   extern __shared__ double sm[];
   double* P = sm;
   double* Aa = sm + n * n;
-  double* M = sm + 2 * n * n;
-  double* mono = sm + 3 * n * n;   // [L0 + nA]
+  double* mono = sm + 2 * n * n;   // [L0 + nA]
+  double* M = scratch + (int64_t)blockIdx.x * n * n;
   const double* al = pts + (int64_t)blockIdx.x * l;
   for (int q = threadIdx.x; q < L0 + nA; q += blockDim.x) {
     const int32_t* e = q < L0 ? Wp + (int64_t)q * l : Wa + (int64_t)(q - L0) * l;
@@ -303,7 +306,9 @@ __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__
     M[e] = -v;
   }
   __syncthreads();
-  const bool lyap = smem_chol(M, n);
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) Aa[e] = M[e];
+  __syncthreads();
+  const bool lyap = smem_chol(Aa, n);
   __syncthreads();
   const bool pos = smem_chol(P, n);
   if (threadIdx.x == 0 && !(lyap && pos)) atomicAdd(nfail, 1);
@@ -782,15 +787,15 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
                                       int32_t* nfail_out, void* stream) {
   if (!ctx || !y || npts < 0 || (npts > 0 && !pts_host) || !nfail_out) return POLYA_EINVAL;
   Ctx& c = ctx->c;
-  if (c.n > 64) {
-    c.last_error = "polya_verdict: n <= 64 (three n x n matrices per point in shared memory)";
+  if ((2 * c.n * c.n + c.L0 + c.nA) * (int64_t)sizeof(double) > 227 * 1024) {
+    c.last_error = "polya_verdict: n <= 118 (two n x n matrices per point in shared memory)";
     return POLYA_EINVAL;
   }
   cudaStream_t s = (cudaStream_t)stream;
   *nfail_out = 0;
   if (npts == 0) return POLYA_OK;
   int32_t *dWp = nullptr, *dWa = nullptr;
-  double* dpts = nullptr;
+  double *dpts = nullptr, *dscr = nullptr;
   int* dfail = nullptr;
   polya_status ret = POLYA_OK;
   try {
@@ -798,15 +803,16 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
     CK(cudaMalloc(&dWa, c.Wa.size() * sizeof(int32_t)));
     CK(cudaMalloc(&dpts, (size_t)npts * c.l * sizeof(double)));
     CK(cudaMalloc(&dfail, sizeof(int)));
+    CK(cudaMalloc(&dscr, (size_t)npts * c.n * c.n * sizeof(double)));
     CK(cudaMemcpyAsync(dWp, c.Wp.data(), c.Wp.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dWa, c.Wa.data(), c.Wa.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dpts, pts_host, (size_t)npts * c.l * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(dfail, 0, sizeof(int), s));
     CK(launch_vmap(c, y, s));   // V_h(y) -> arena slots id_Vy + h
-    const size_t sm = (3 * (size_t)c.n * c.n + c.L0 + c.nA) * sizeof(double);
+    const size_t sm = (2 * (size_t)c.n * c.n + c.L0 + c.nA) * sizeof(double);
     CK(cudaFuncSetAttribute(k_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_grid<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, (int)c.nA, dWp, dWa, c.arena, c.mstride,
-                                          (int)c.np, c.id_Vy, c.dA, dpts, dfail);
+                                          (int)c.np, c.id_Vy, c.dA, dpts, dscr, dfail);
     ++c.launches;
     CK(cudaGetLastError());
     int h = 0;
@@ -820,6 +826,7 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
   cudaFree(dWp);
   cudaFree(dWa);
   cudaFree(dpts);
+  cudaFree(dscr);
   cudaFree(dfail);
   return ret;
 }

@@ -29,7 +29,7 @@ r = ctx.ipm_solve(eps=1e-8, tol=1e-8, maxit=maxit)
 torch.cuda.synchronize()
 solve_s = time.time() - t1
 nfail = None
-if r["converged"] and cfg.n <= 64:
+if r["converged"] and cfg.n <= 118:
     nfail = ctx.verdict(r["y"], robust.simplex_points(cfg.l, 1000, 0))
 out = {"config": cid, "n": cfg.n, "l": cfg.l, "dp": cfg.dp, "d1": cfg.d1, "d2": cfg.d2, "K": ctx.K,
        "nblocks": ctx.nblocks, "converged": bool(r["converged"]), "status": r["status"], "iterations": r["iterations"],
@@ -37,5 +37,5 @@ out = {"config": cid, "n": cfg.n, "l": cfg.l, "dp": cfg.dp, "d1": cfg.d1, "d2": 
        "certified": bool(r["converged"] and (nfail == 0 if nfail is not None else True)),
        "setup_s": setup_s, "solve_s": solve_s, "s_per_iteration": solve_s / max(r["iterations"], 1),
        "ms_schur_total": r["ms_schur"], "ms_factor_total": r["ms_factor"], "ms_other_total": r["ms_other"],
-       "note": "grid check skipped for n > 64 (polya_verdict limit); certified then means converged with Z > 0"}
+       "note": "grid check: polya_verdict at the simplex vertices, edge midpoints and 1000 Dirichlet(1) points (n <= 118)"}
 print(json.dumps(out))
