@@ -9,6 +9,8 @@
 // K9 adjoint    : B(X)_i = sum_b tr(F_i^b X_b), segmented reduction over blocks
 #include <algorithm>
 
+#include <cassert>
+
 #include "polya_internal.h"
 
 namespace polya {
@@ -93,6 +95,9 @@ __global__ void __launch_bounds__(128) k_gemm(double* __restrict__ arena, int64_
   const int nk = np / 8, total = (it.tend - it.tbeg) * nk;
   auto issue = [&](int c, int buf) {
     const GemmTerm tm = terms[it.tbeg + c / nk];
+#ifdef POLYA_BOUNDS_CHECK
+    assert(tm.a_id >= 0 && tm.b_id >= 0 && it.c_id >= 0 && (int64_t)tm.a_id * ms >= 0);
+#endif
     const int k0 = (c % nk) * 8;
     const double* A = arena + (int64_t)tm.a_id * ms;
     const double* B = arena + (int64_t)tm.b_id * ms;

@@ -27,6 +27,7 @@
 // Every G entry is produced by one CTA in a fixed k order: deterministic, and FULL layouts are
 // bitwise symmetric.  DESIGN.md 5.2 has the measurements and the variants that were tried.
 #include <algorithm>
+#include <cassert>
 #include <type_traits>
 
 #include "polya_internal.h"
@@ -71,7 +72,16 @@ struct SchurArgs {
   double* G;
   int layout;
   int64_t K, Ntil;
+  int64_t nmats;   // arena matrices (bounds checks of the POLYA_BOUNDS_CHECK build)
 };
+
+// Device-side bounds checks, compiled in only with -DPOLYA_BOUNDS_CHECK (compute-sanitizer is not
+// available on this pool): arena matrix ids and G entries of every access are asserted in range.
+#ifdef POLYA_BOUNDS_CHECK
+#define POLYA_ASSERT(c) assert(c)
+#else
+#define POLYA_ASSERT(c) ((void)0)
+#endif
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -126,6 +136,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src,
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void st_g(double* p, double v) {
+  POLYA_ASSERT(p != nullptr);
   if (SCHUR_L2HINTS & 2) __stcs(p, v); else *p = v;
 }
 __device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -462,6 +473,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
           for (int kk = 0; kk < KB; ++kk) {
             const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, kk);
             const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, kk);
+            POLYA_ASSERT(idL < p.nmats && idR < p.nmats);
             if (!(SCHUR_EXP & 4)) {   // experiment bit 4: no operand loads (timing of the DMMA side only)
               cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL, pol);
               cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR, pol);
@@ -570,6 +582,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (rw[u].x < 0) continue;
+          POLYA_ASSERT(rw[u].x < p.Ntil && cA.x < p.Ntil && cB.x < p.Ntil && it.pl < p.npl);
           double* dst = fullG ? p.G + (rowbase + rw[u].x) * p.K + colbase : tile + (int64_t)rw[u].x * p.Ntil;
           if (cA.x >= 0 && !(same_cls && rw[u].x > cA.x)) st_g(dst + cA.x, vA[u]);
           if (cB.x >= 0 && !(same_cls && rw[u].x > cB.x)) st_g(dst + cB.x, vB[u]);
@@ -591,6 +604,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (cl[u].x < 0) continue;
+          POLYA_ASSERT(cl[u].x < p.Ntil && rA.x < p.Ntil && rB.x < p.Ntil && it.pl < p.npl);
           double* dst = fullG ? p.G + (colbase + cl[u].x) * p.K + rowbase : tile + (int64_t)cl[u].x * p.Ntil;
           if (rA.x >= 0 && !(same_cls && rA.x > cl[u].x)) st_g(dst + rA.x, vA[u]);
           if (rB.x >= 0 && !(same_cls && rB.x > cl[u].x)) st_g(dst + rB.x, vB[u]);
@@ -624,7 +638,7 @@ cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, 
   a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
   a.pair_kbeg = c.st.pair_kbeg; a.pair_item = c.st.pair_item; a.kdesc = c.st.kdesc;
   a.item0 = i0; a.item1 = i1; a.counter = c.st.counter;
-  a.G = G; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil;
+  a.G = G; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil; a.nmats = c.nmats;
   k_schur<<<(unsigned)want, NT, kSmemBytes, s>>>(a);
   ++c.launches;
   return cudaGetLastError();
