@@ -250,7 +250,12 @@ polya_status polya_simplex_map(int32_t l, int32_t d, int32_t n, const double* sc
  * definite (reading R10); otherwise res->status says why (ENOTPD: a block or G lost definiteness,
  * ESTEP: no admissible step, EMAXIT).  The return value reports only misuse / CUDA failures.
  * Single rank (nranks = 1).  Synchronous.                                                   */
-typedef struct { double eps, tol; int32_t maxit, init; } polya_solve_opts;
+typedef struct {
+  double eps, tol;
+  int32_t maxit, init;
+  polya_ipm_stats* history;   /* optional host array of maxit entries: the stats of every iteration
+                                 (the iteration log of S:448); NULL = none */
+} polya_solve_opts;
 typedef struct {
   int32_t converged, iterations, status;
   double gap, pinf, mu;

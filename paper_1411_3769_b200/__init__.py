@@ -48,10 +48,6 @@ class _IpmState(ctypes.Structure):
                 ("mu", ctypes.c_double), ("iter", ctypes.c_int32)]
 
 
-class _SolveOpts(ctypes.Structure):
-    _fields_ = [("eps", ctypes.c_double), ("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("init", ctypes.c_int32)]
-
-
 class _SolveResult(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int32), ("iterations", ctypes.c_int32), ("status", ctypes.c_int32),
                 ("gap", ctypes.c_double), ("pinf", ctypes.c_double), ("mu", ctypes.c_double),
@@ -62,6 +58,11 @@ class _IpmStats(ctypes.Structure):
     _fields_ = [("gap", ctypes.c_double), ("mu", ctypes.c_double), ("tp", ctypes.c_double), ("td", ctypes.c_double),
                 ("phi", ctypes.c_double), ("psi", ctypes.c_double), ("ms_schur", ctypes.c_float),
                 ("ms_factor", ctypes.c_float), ("ms_other", ctypes.c_float), ("reg_retries", ctypes.c_int32)]
+
+
+class _SolveOpts(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("init", ctypes.c_int32),
+                ("history", ctypes.POINTER(_IpmStats))]
 
 
 _lib = None
@@ -316,11 +317,13 @@ class Polya:
         y = torch.empty(self.K, dtype=torch.float64, device="cuda") if y is None else y
         st = _IpmState(_dev_ptr(X, None, "X").value, _dev_ptr(Z, None, "Z").value, _dev_ptr(y, self.K, "y").value,
                        1.0 / 3.0, 0)
-        opt = _SolveOpts(float(eps), float(tol), int(maxit), int(bool(init)))
+        hist = (_IpmStats * max(int(maxit), 1))()
+        opt = _SolveOpts(float(eps), float(tol), int(maxit), int(bool(init)), hist)
         res = _SolveResult()
         self._check(lib().polya_ipm_solve(self._h, ctypes.byref(st), ctypes.byref(opt), ctypes.byref(res),
                                           _stream_ptr(stream)), "polya_ipm_solve")
         out = {k: getattr(res, k) for k, _ in _SolveResult._fields_}
+        out["history"] = [{k: getattr(hist[i], k) for k, _ in _IpmStats._fields_} for i in range(res.iterations)]
         out.update(X=X, Z=Z, y=y)
         return out
 

@@ -734,8 +734,10 @@ extern "C" polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, con
     std::vector<double> part(kScalarBlocks);
     for (int it = 0; it < opt->maxit; ++it) {
       polya_ipm_stats ps;
+      std::memset(&ps, 0, sizeof(ps));
       const polya_status r = polya_ipm_step(ctx, st, &ps, stream);
       res->iterations = it + 1;
+      if (opt->history) opt->history[it] = ps;
       if (r != POLYA_OK) {   // an outcome, not an exception: Z or G lost definiteness, no step
         res->status = r;
         return POLYA_OK;

@@ -37,5 +37,6 @@ out = {"config": cid, "n": cfg.n, "l": cfg.l, "dp": cfg.dp, "d1": cfg.d1, "d2": 
        "certified": bool(r["converged"] and (nfail == 0 if nfail is not None else True)),
        "setup_s": setup_s, "solve_s": solve_s, "s_per_iteration": solve_s / max(r["iterations"], 1),
        "ms_schur_total": r["ms_schur"], "ms_factor_total": r["ms_factor"], "ms_other_total": r["ms_other"],
+       "history": [{k: h[k] for k in ("gap", "mu", "tp", "td", "ms_schur", "ms_factor", "ms_other")} for h in r["history"]],
        "note": "grid check: polya_verdict at the simplex vertices, edge midpoints and 1000 Dirichlet(1) points (n <= 118)"}
 print(json.dumps(out))

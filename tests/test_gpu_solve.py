@@ -52,6 +52,8 @@ def test_solve_matches_oracle_solution_config1(pb):
     ctx = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
     r = ctx.ipm_solve()
     assert bool(r["converged"]) == ok and r["iterations"] == it
+    hist = r["history"]                       # per-iteration log
+    assert len(hist) == it and hist[-1]["gap"] == r["gap"] and hist[-1]["gap"] <= 1e-8 < hist[0]["gap"]
     yg = r["y"].cpu().numpy()
     assert np.linalg.norm(yg - y) <= 1e-6 * np.linalg.norm(y)
     ctx.close()
