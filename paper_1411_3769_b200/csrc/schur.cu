@@ -150,12 +150,32 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(sptr(bar)) : "memory");
 }
+#ifndef SCHUR_WAIT_MODE
+#define SCHUR_WAIT_MODE 0   // 0: try_wait (hardware-chosen suspend), 1: test_wait spin, 2: try_wait with a
+#endif                      //    SCHUR_WAIT_NS suspend-time hint (timing experiments)
+#ifndef SCHUR_WAIT_NS
+#define SCHUR_WAIT_NS 100
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if SCHUR_WAIT_MODE == 1
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          sptr(bar)),
+      "r"(parity)
+      : "memory");
+#elif SCHUR_WAIT_MODE == 2
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          sptr(bar)),
+      "r"(parity), "n"(SCHUR_WAIT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
           sptr(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 // Consumer phases (each fold of an orientation, each item's epilogue) are ordered by one mbarrier
 // with one arrival per consumer warp: a warp arrives when its part of a phase is done and waits
