@@ -117,11 +117,16 @@ def grid_check(P, y, samples=1000, seed=0):
     pts = [np.eye(P.l)[i] for i in range(P.l)]
     pts += [0.5 * (np.eye(P.l)[i] + np.eye(P.l)[j]) for i in range(P.l) for j in range(i + 1, P.l)]
     pts += list(rng.dirichlet(np.ones(P.l), size=samples))
-    Wa = enumerate_W(P.l, P.da)
+    from . import polya as _polya
     for al in pts:
         Pa = sum(math.prod(a ** e for a, e in zip(al, h)) * Ph[i] for i, h in enumerate(Wp))
-        Aa = sum(math.prod(a ** e for a, e in zip(al, lam)) * P.A[i] for i, lam in enumerate(Wa))
-        if np.linalg.eigvalsh(Pa).min() <= 0 or np.linalg.eigvalsh(Aa.T @ Pa + Pa @ Aa).max() >= 0:
+        if P.gen is not None:   # generalised form: sum_i At_i(alpha) P Bt_i(alpha) + transpose < 0
+            Lm = sum(_polya.evaluate(At, P.l, a, al) @ Pa @ _polya.evaluate(Bt, P.l, b, al) for At, a, Bt, b in P.pairs)
+            Lm = Lm + Lm.T
+        else:
+            Aa = _polya.evaluate(P.A, P.l, P.da, al)
+            Lm = Aa.T @ Pa + Pa @ Aa
+        if np.linalg.eigvalsh(Pa).min() <= 0 or np.linalg.eigvalsh(Lm).max() >= 0:
             return False
     return True
 

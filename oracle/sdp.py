@@ -12,6 +12,8 @@ Follows PAPER.md Sec. III.B "SDP Problem Elements" and Algorithm 2:
 * B(X) = [tr(B_1 X) ... tr(B_K X)]^T,
   B^T(y) = sum_i y_i B_i (Eq. AT, PAPER.md:335-338);
 * lambda_{k,l} = sum_blocks tr(B_k Z^{-1} B_l X) (Eq. T2).
+* the generalised form sum_i (At_i P Bt_i + Bt_i^T P At_i^T) < 0 (reading R18):
+  build_problem_general; Lyapunov block m of the element (h, k) is -sum_q (A_q E_k B_q + B_q^T E_k A_q^T).
 
 Block order: P-blocks 0..L-1 in W_{dp+d1} order, then Lyapunov blocks in
 W_{dp+da+d2} order.  Dual index i = k + Ntil*h (0-based).
@@ -27,7 +29,7 @@ from .monomials import enumerate_W
 
 __all__ = ["basis", "trE", "Problem", "build_problem", "vmap", "F_block", "F_stack",
            "apply_literal", "apply_vmap", "adjoint_literal", "adjoint_trace",
-           "schur_literal", "schur_entries", "schur_probe"]
+           "schur_literal", "schur_entries", "schur_probe", "schur_structured", "build_problem_general"]
 
 
 def basis(n: int):
@@ -72,6 +74,8 @@ class Problem:
     c: np.ndarray             # (L,)
     A: np.ndarray
     E: list
+    gen: list = None          # generalised form: gen[h][m] = [(A_q, B_q), ...] (build_problem_general)
+    pairs: list = None        # its (Atil_i, deg_a, Btil_i, deg_b) terms
 
     @property
     def nblocks(self):
@@ -81,6 +85,8 @@ class Problem:
         """Whether F^b_{(h,.)} is structurally non-zero."""
         if b < self.L:
             return self.beta[h, b] != 0
+        if self.gen is not None:
+            return len(self.gen[h][b - self.L]) > 0
         return bool(np.any(self.H[h, b - self.L] != 0))
 
 
@@ -93,6 +99,42 @@ def build_problem(A, n, l, dp, d1, d2, da=1, delta=1e-3) -> Problem:
     Ntil = n * (n + 1) // 2
     c = polya.C_scalars(beta, l, dp, delta)
     return Problem(n, l, dp, da, d1, d2, delta, L0, L, M, Ntil, L0 * Ntil, beta, H, c, A, basis(n))
+
+
+def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3) -> Problem:
+    """The generalised LMI form of PAPER.md:454-459, square case, R_i = 0:
+        P(alpha) > 0,   sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) < 0,
+    with pairs = [(At_i coefficients [f(l,a_i)][n][n] in W_{a_i} order, a_i, Bt_i coefficients, b_i)],
+    all with the same total degree e = a_i + b_i.  Polya's multiplier (sum alpha)^{d2} turns the
+    second condition into M = |W_{dp+e+d2}| coefficient blocks (as Eqs. LMI_2/LMI_4 do for A^T P + P A),
+    found here by explicit polynomial multiplication: the coefficient of alpha^gamma in
+    (sum alpha)^{d2} alpha^h At_i(alpha) (.) Bt_i(alpha) is the list of pairs
+    (multinomial(d2; gamma - h - lambda - mu) At_{i,lambda}, Bt_{i,mu}), and block m of the dual
+    basis element (h, k) is F = -sum_pairs (A E_k B + B^T E_k A^T).  A^T P + P A is the case
+    [(A^T, 1, I, 0)] (tests/test_oracle_general.py)."""
+    es = {a + b for _, a, _, b in pairs}
+    assert len(es) == 1, "all terms must have the same total degree"
+    e = es.pop()
+    beta = polya.beta_table(l, dp, d1)
+    L0, L = beta.shape
+    Wp = enumerate_W(l, dp)
+    idx = polya.index_map(l, dp + e + d2)
+    M = len(idx)
+    S = polya.simplex_power(l, d2)
+    gen = [[[] for _ in range(M)] for _ in range(L0)]
+    for hi, h in enumerate(Wp):
+        for At, a, Bt, b in pairs:
+            Wa, Wb = enumerate_W(l, a), enumerate_W(l, b)
+            for li, lam in enumerate(Wa):
+                for mi, mu in enumerate(Wb):
+                    mono = tuple(x + y + z for x, y, z in zip(h, lam, mu))
+                    for e2, w in polya.poly_mul(S, {mono: 1}).items():
+                        gen[hi][idx[e2]].append((float(w) * np.asarray(At[li], dtype=float),
+                                                 np.asarray(Bt[mi], dtype=float)))
+    Ntil = n * (n + 1) // 2
+    c = polya.C_scalars(beta, l, dp, delta)
+    return Problem(n, l, dp, e, d1, d2, delta, L0, L, M, Ntil, L0 * Ntil, beta, np.zeros((L0, M, 0, 0)), c, None,
+                   basis(n), gen=gen, pairs=pairs)
 
 
 def vmap(P: Problem, x, h: int):
@@ -123,6 +165,11 @@ def F_block(P: Problem, i: int, b: int):
     E = E_matrix(P.n, P.E[k])
     if b < P.L:
         return float(P.beta[h, b]) * E
+    if P.gen is not None:
+        F = np.zeros((P.n, P.n))
+        for Aq, Bq in P.gen[h][b - P.L]:
+            F -= Aq @ E @ Bq + Bq.T @ E @ Aq.T
+        return F
     Hm = P.H[h, b - P.L]
     return -(Hm.T @ E + E @ Hm)
 
@@ -153,6 +200,10 @@ def apply_vmap(P: Problem, y):
             out[j] += float(P.beta[h, j]) * V[h]
     for m in range(P.M):
         for h in range(P.L0):
+            if P.gen is not None:
+                for Aq, Bq in P.gen[h][m]:
+                    out[P.L + m] -= Aq @ V[h] @ Bq + Bq.T @ V[h] @ Aq.T
+                continue
             Hm = P.H[h, m]
             out[P.L + m] -= Hm.T @ V[h] + V[h] @ Hm
     return out
@@ -177,6 +228,12 @@ def adjoint_trace(P: Problem, Xb):
                 if P.beta[h, b] == 0:
                     continue
                 M = float(P.beta[h, b]) * Xb[b]
+            elif P.gen is not None:
+                terms = P.gen[h][b - P.L]
+                if not terms:
+                    continue
+                # tr(F X) with F = -sum (A E B + B^T E A^T) = tr(E_k M), M = -sum (B X A + A^T X B^T)
+                M = -sum(Bq @ Xb[b] @ Aq + Aq.T @ Xb[b] @ Bq.T for Aq, Bq in terms)
             else:
                 Hm = P.H[h, b - P.L]
                 if not np.any(Hm):
@@ -246,10 +303,19 @@ def schur_structured(P: Problem, Xb, Wb, pairs=None):
                 Ls.append(float(P.beta[h, j] * P.beta[h2, j]) * Wb[j])
                 Rs.append(Xb[j])
         for m in range(P.M):
+            W, X = Wb[L + m], Xb[L + m]
+            if P.gen is not None:
+                # F = -sum_q (A_q E B_q + B_q^T E A_q^T): the same four terms per (q, q'), here
+                # (B W A', B' X A), (B W B'^T, A'^T X A), (A^T W A', B' X B^T), (A^T W B'^T, A'^T X B^T)
+                # (H^T, I) for (A, B) gives back the continuous-time terms below (reading R18)
+                for A1, B1 in P.gen[h][m]:
+                    for A2, B2 in P.gen[h2][m]:
+                        Ls += [B1 @ W @ A2, B1 @ W @ B2.T, A1.T @ W @ A2, A1.T @ W @ B2.T]
+                        Rs += [B2 @ X @ A1, A2.T @ X @ A1, B2 @ X @ B1.T, A2.T @ X @ B1.T]
+                continue
             H, H2 = P.H[h, m], P.H[h2, m]
             if not (np.any(H) and np.any(H2)):
                 continue
-            W, X = Wb[L + m], Xb[L + m]
             Ls += [W @ H2.T, W, H @ W @ H2.T, H @ W]
             Rs += [X @ H.T, H2 @ X @ H.T, X, H2 @ X]
         if not Ls:

@@ -21,7 +21,8 @@ import dataclasses
 
 import numpy as np
 
-__all__ = ["CONFIGS", "Config", "vertex_matrices", "spd_blocks", "make_case", "small_config"]
+__all__ = ["CONFIGS", "Config", "vertex_matrices", "spd_blocks", "make_case", "small_config",
+           "discrete_vertex_matrices", "discrete_time_terms", "random_terms"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -122,3 +123,41 @@ def make_case(cfg: Config, nblocks: int, seed: int = 0):
     A = vertex_matrices(cfg, rng)
     X, W = spd_blocks(cfg.n, nblocks, rng)
     return A, X, W
+
+
+# ---- generalised LMI form (reading R18) --------------------------------
+# A term list is [(At, a, Bt, b), ...]: At has shape (f(l, a), n, n), Bt (f(l, b), n, n), the
+# coefficients of At_i(alpha), Bt_i(alpha) in the library's W_d order; for degree 1 that order is
+# e_1, ..., e_l (vertex order), the only one used below.
+
+def discrete_vertex_matrices(n: int, l: int, rho: float, rng, unstable: bool = False) -> np.ndarray:
+    """Vertices of a discrete-time polytope x+ = A(alpha) x: iid N(0,1) matrices scaled to spectral
+    norm rho (< 1: every A(alpha) on the simplex is a contraction, so P = I certifies it).  With
+    ``unstable`` vertex 1 becomes 1.05 Q (Q orthogonal): spectral radius 1.05, not Schur stable."""
+    A = []
+    for _ in range(l):
+        g = rng.normal(0.0, 1.0, size=(n, n))
+        A.append(rho * g / np.linalg.norm(g, 2))
+    A = np.array(A)
+    if unstable:
+        q, _ = np.linalg.qr(rng.normal(0.0, 1.0, size=(n, n)))
+        A[0] = 1.05 * q
+    return A
+
+
+def discrete_time_terms(A: np.ndarray):
+    """A(alpha)^T P A(alpha) - (sum alpha)^2 P < 0 (discrete-time robust stability, both sides
+    homogeneous of degree 2) as generalised terms:
+        (1/2 A^T(alpha)) P A(alpha) + transpose   and   (-1/2 sum alpha I) P (sum alpha I) + transpose."""
+    l, n, _ = A.shape
+    half = np.array([0.5 * a.T for a in A])
+    neg = np.array([-0.5 * np.eye(n)] * l)
+    eye = np.array([np.eye(n)] * l)
+    return [(half, 1, A.copy(), 1), (neg, 1, eye, 1)]
+
+
+def random_terms(n: int, l: int, degs, rng, counts):
+    """Random term list with degree pairs ``degs`` [(a, b), ...]; ``counts(d)`` = f(l, d) is passed
+    in by the caller (this module enumerates nothing)."""
+    return [(rng.normal(0.0, 1.0, size=(counts(a), n, n)), a, rng.normal(0.0, 1.0, size=(counts(b), n, n)), b)
+            for a, b in degs]

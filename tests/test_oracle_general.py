@@ -1,0 +1,98 @@
+"""Pins for the oracle's generalised LMI form (reading R18 in DESIGN.md):
+    sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) < 0,  square case, R_i = 0.
+
+* the continuous-time LMI is the case [(A^T, 1, I, 0)]: every operator and the Schur complement
+  equal those of build_problem (itself pinned in test_oracle_sdp.py);
+* Polya's coefficient blocks are a polynomial identity: at random alpha,
+  sum_gamma alpha^gamma B^T(y)_{L+gamma} = -(sum alpha)^{d2} sum_i (At_i P Bt_i + transpose)(alpha)
+  with P(alpha) = sum_h alpha^h V_h(y), evaluated by plain substitution (not by build's products);
+* the adjoint identity <B^T(y), X> = y^T B(X) and G y = B(X B^T(y) W) (two routes to G);
+* discrete-time robust stability (A^T P A - P < 0): a contraction polytope is certified, a polytope
+  with a vertex of spectral radius 1.05 is not (Theorem 1's certificate is sufficient, and no P
+  exists when a vertex is unstable).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import ipm, polya, sdp
+from oracle.monomials import enumerate_W
+
+
+def _f(l):
+    return lambda d: len(enumerate_W(l, d))
+
+
+def test_continuous_time_is_the_special_case():
+    c = synth.small_config(4, 3, 2, 1, 2)
+    rng = np.random.default_rng(0)
+    A = synth.vertex_matrices(c, rng)
+    P = sdp.build_problem(A, c.n, c.l, c.dp, c.d1, c.d2)
+    Pg = sdp.build_problem_general([(np.array([a.T for a in A]), 1, np.eye(c.n)[None], 0)], c.n, c.l, c.dp, c.d1, c.d2)
+    assert (P.M, P.K, P.L) == (Pg.M, Pg.K, Pg.L)
+    assert all(P.active(h, b) == Pg.active(h, b) for h in range(P.L0) for b in range(P.nblocks))
+    X, W = synth.spd_blocks(c.n, P.nblocks, rng)
+    y = rng.normal(size=P.K)
+    G = sdp.schur_literal(P, X, W)
+    assert np.abs(sdp.schur_literal(Pg, X, W) - G).max() <= 1e-13 * np.abs(G).max()
+    T = sdp.apply_vmap(P, y)
+    assert np.abs(sdp.apply_vmap(Pg, y) - T).max() <= 1e-13 * np.abs(T).max()
+    b = sdp.adjoint_trace(P, X)
+    assert np.abs(sdp.adjoint_trace(Pg, X) - b).max() <= 1e-13 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("degs,shape", [([(1, 1), (2, 0)], (3, 2, 1, 1, 2)), ([(0, 2), (1, 1), (2, 0)], (2, 3, 1, 2, 1)),
+                                        ([(1, 0)], (3, 2, 2, 1, 0))])
+def test_polya_blocks_are_a_polynomial_identity(degs, shape):
+    n, l, dp, d1, d2 = shape
+    rng = np.random.default_rng(1)
+    terms = synth.random_terms(n, l, degs, rng, _f(l))
+    P = sdp.build_problem_general(terms, n, l, dp, d1, d2)
+    y = rng.normal(size=P.K)
+    out = sdp.apply_vmap(P, y)
+    Wp, Wm = enumerate_W(l, dp), enumerate_W(l, P.da + dp + d2)
+    V = [sdp.vmap(P, y, h) for h in range(P.L0)]
+    for _ in range(4):
+        al = rng.dirichlet(np.ones(l)) * rng.uniform(0.5, 2.0)     # identity holds off the simplex too
+        mono = lambda e: math.prod(a ** k for a, k in zip(al, e))
+        Pa = sum(mono(h) * V[i] for i, h in enumerate(Wp))
+        lhs = sum(mono(g) * out[P.L + m] for m, g in enumerate(Wm))
+        S = sum(polya.evaluate(At, l, a, al) @ Pa @ polya.evaluate(Bt, l, b, al) for At, a, Bt, b in terms)
+        rhs = -(sum(al) ** d2) * (S + S.T)
+        assert np.abs(lhs - rhs).max() <= 1e-12 * np.abs(rhs).max()
+    # the P-blocks are untouched by the generalisation: sum_h beta_hj V_h
+    for j in range(P.L):
+        assert np.allclose(out[j], sum(P.beta[h, j] * V[h] for h in range(P.L0)), rtol=0, atol=1e-13 * np.abs(out[j]).max() + 1e-300)
+
+
+def test_adjoint_and_two_routes_to_G():
+    n, l, dp, d1, d2 = 3, 2, 1, 1, 1
+    rng = np.random.default_rng(2)
+    terms = synth.random_terms(n, l, [(1, 1), (2, 0)], rng, _f(l))
+    P = sdp.build_problem_general(terms, n, l, dp, d1, d2)
+    X, W = synth.spd_blocks(n, P.nblocks, rng)
+    y = rng.normal(size=P.K)
+    T = sdp.apply_vmap(P, y)
+    lhs = sum(np.sum(T[b] * X[b]) for b in range(P.nblocks))
+    assert abs(lhs - y @ sdp.adjoint_trace(P, X)) <= 1e-12 * abs(lhs)
+    G = sdp.schur_literal(P, X, W)
+    Gs = sdp.schur_structured(P, X, W)      # the rank-structured route (used at larger sizes)
+    assert np.abs(Gs - G).max() <= 1e-12 * np.abs(G).max()
+    assert np.allclose(G, G.T, rtol=0, atol=1e-12 * np.abs(G).max())
+    Y = np.array([X[b] @ T[b] @ W[b] for b in range(P.nblocks)])
+    Y = 0.5 * (Y + Y.transpose(0, 2, 1))
+    Gy = sdp.adjoint_trace(P, Y)
+    assert np.abs(G @ y - Gy).max() <= 1e-11 * np.abs(Gy).max()
+    assert np.linalg.eigvalsh(G).min() > -1e-10 * np.abs(G).max()
+
+
+@pytest.mark.parametrize("unstable", [False, True])
+def test_discrete_time_verdicts(unstable):
+    n, l = 3, 2
+    A = synth.discrete_vertex_matrices(n, l, 0.8, np.random.default_rng(3), unstable=unstable)
+    P = sdp.build_problem_general(synth.discrete_time_terms(A), n, l, 1, 1, 1)
+    assert ipm.verdict(P, samples=200) == (not unstable)
+    if unstable:   # the vertex itself violates A^T P A - P < 0 for every P > 0
+        assert max(abs(np.linalg.eigvals(A[0]))) > 1.0
