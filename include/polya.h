@@ -120,6 +120,20 @@ typedef enum { POLYA_G_FULL = 0, POLYA_G_PAIR_TILES = 1 } polya_G_layout;
  * [0,nranks), null pointers), EOVERFLOW, ENOMEM, ECUDA.  *out = NULL on error. */
 polya_status polya_setup(const polya_config* cfg, const double* A_host, polya_ctx** out);
 
+/* The generalised form (reading R18):
+ *     P(alpha) > 0,   sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) < 0,
+ * square case (At_i, Bt_i n x n), R_i = 0.  Term i has At_i of degree deg_a[i] and Bt_i of degree
+ * deg_b[i] with deg_a[i] + deg_b[i] = cfg->da for every i (homogenise first; EINVAL otherwise).
+ * At: the concatenation over i of double[f(l,deg_a[i])][n][n] (coefficients in W_{deg_a[i]} order),
+ * Bt likewise; both copied.  The continuous-time polya_setup is the case nterms = 1,
+ * (A^T, 1, I, 0); discrete time A^T P A - P < 0 is [(A^T/2, 1, A, 1), (-I/2 per vertex, 1, I per
+ * vertex, 1)].  Lyapunov block gamma of the dual element (h, k) is
+ *     -sum_{i,lambda,mu} multinomial(d2; gamma - h - lambda - mu) (At_{i,lambda} E_k Bt_{i,mu} + transpose);
+ * every other entry point (apply, adjoint, Schur, IPM, solve, verdict, sharding) works unchanged
+ * on the resulting context, except polya_get_H (EINVAL: no H table).  Errors as polya_setup. */
+polya_status polya_setup_general(const polya_config* cfg, int32_t nterms, const int32_t* deg_a, const int32_t* deg_b,
+                                 const double* At_host, const double* Bt_host, polya_ctx** out);
+
 polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* out);
 
 /* Host-only planning (no CUDA call, no A needed: the sparsity of beta and H depends
@@ -267,7 +281,8 @@ polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, const polya_so
 /* polya_verdict: the grid check of the certificate (Theorem 1):
  * with P(alpha) = sum_h alpha^h V_h(y) (reading R7; y_dev: double[K] on the device) and A(alpha) the
  * set-up's A, counts the points alpha = pts_host[p] (double[npts][l], host, points of the simplex)
- * where P(alpha) > 0 or -(A^T P + P A)(alpha) > 0 fails a Cholesky test, into *nfail_out.
+ * where P(alpha) > 0 or -(A^T P + P A)(alpha) > 0 fails a Cholesky test, into *nfail_out
+ * (generalised form: -sum_i (At_i P Bt_i + transpose)(alpha) > 0 instead).
  * One CTA per point on the device; n <= 118.  Synchronous.                                     */
 polya_status polya_verdict(polya_ctx* ctx, const double* y_dev, int32_t npts, const double* pts_host,
                            int32_t* nfail_out, void* stream);

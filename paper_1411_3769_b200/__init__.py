@@ -23,7 +23,7 @@ EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
            "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
            "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization", "polya_schur_prepare",
-           "polya_schur_assemble"]
+           "polya_schur_assemble", "polya_setup_general"]
 
 
 class PolyaError(RuntimeError):
@@ -78,6 +78,7 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
+    L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, vp, vp, vp, vp, ctypes.POINTER(vp)]
     L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
     L.polya_plan.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Dims)]
     L.polya_get_exponents.argtypes = [vp, ctypes.c_int, vp]
@@ -191,16 +192,34 @@ def _dev_ptr(t, numel=None, name="tensor"):
 
 class Polya:
     """One context = one rank / GPU (``polya_setup``).  ``A`` is the host array
-    double[f(l,da)][n][n] of A(alpha)'s coefficients in W_da order."""
+    double[f(l,da)][n][n] of A(alpha)'s coefficients in W_da order.  With ``terms`` =
+    [(At_i, deg_a_i, Bt_i, deg_b_i), ...] (A ignored, da = deg_a + deg_b) the context is the
+    generalised form sum_i (At_i P Bt_i + transpose) < 0 (``polya_setup_general``)."""
 
-    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES):
+    @classmethod
+    def general(cls, terms, n, l, dp, d1, d2, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES):
+        return cls(n, l, dp, d1, d2, None, delta=delta, rank=rank, nranks=nranks, shard=shard, terms=terms)
+
+    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES, terms=None):
         L = lib()
-        A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
-        cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks, shard)
         h = ctypes.c_void_p()
-        st = L.polya_setup(ctypes.byref(cfg), A.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h))
+        if terms is None:
+            A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+            cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks, shard)
+            st = L.polya_setup(ctypes.byref(cfg), A.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h))
+            what = "polya_setup"
+        else:   # generalised form (polya_setup_general): terms = [(At, deg_a, Bt, deg_b), ...]
+            da = int(terms[0][1]) + int(terms[0][3])
+            cfg = _Config(n, l, dp, da, d1, d2, delta, rank, nranks, shard)
+            dega = np.array([t[1] for t in terms], dtype=np.int32)
+            degb = np.array([t[3] for t in terms], dtype=np.int32)
+            At = np.ascontiguousarray(np.concatenate([np.asarray(t[0], dtype=np.float64).reshape(-1) for t in terms]))
+            Bt = np.ascontiguousarray(np.concatenate([np.asarray(t[2], dtype=np.float64).reshape(-1) for t in terms]))
+            cp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+            st = L.polya_setup_general(ctypes.byref(cfg), len(terms), cp(dega), cp(degb), cp(At), cp(Bt), ctypes.byref(h))
+            what = "polya_setup_general"
         if st != 0:
-            raise PolyaError(f"polya_setup: {L.polya_strerror(st).decode()}")
+            raise PolyaError(f"{what}: {L.polya_strerror(st).decode()}")
         self._h = h
         self.n, self.l, self.dp, self.da, self.d1, self.d2 = n, l, dp, da, d1, d2
         self.delta, self.rank, self.nranks, self.shard = delta, rank, nranks, shard

@@ -314,6 +314,77 @@ __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__
   if (threadIdx.x == 0 && !(lyap && pos)) atomicAdd(nfail, 1);
 }
 
+// The same check for the generalised form (reading R18): -sum_i (At_i P Bt_i + transpose)(alpha) > 0.
+// Shared memory: P(alpha), the accumulator S = sum_i At_i P Bt_i, monomials; global scratch per point:
+// At_i(alpha), Bt_i(alpha), P Bt_i(alpha).
+__global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, const int32_t* __restrict__ Wp,
+                           const int32_t* __restrict__ cexp, const int32_t* __restrict__ aoff,
+                           const int32_t* __restrict__ boff, const double* __restrict__ coef,
+                           const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
+                           const double* __restrict__ pts, double* __restrict__ scratch, int* __restrict__ nfail) {
+  extern __shared__ double sm[];
+  double* P = sm;
+  double* S = sm + n * n;
+  double* mono = sm + 2 * n * n;   // [L0 + ncoef]
+  const int64_t nn = (int64_t)n * n;
+  double* Ae = scratch + (int64_t)blockIdx.x * 3 * nn;
+  double* Be = Ae + nn;
+  double* PB = Be + nn;
+  const double* al = pts + (int64_t)blockIdx.x * l;
+  for (int q = threadIdx.x; q < L0 + ncoef; q += blockDim.x) {
+    const int32_t* e = q < L0 ? Wp + (int64_t)q * l : cexp + (int64_t)(q - L0) * l;
+    double m = 1.0;
+    for (int i = 0; i < l; ++i)
+      for (int k = 0; k < e[i]; ++k) m *= al[i];
+    mono[q] = m;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    double p = 0.0;
+    for (int h = 0; h < L0; ++h) p += mono[h] * arena[(id_Vy + h) * ms + (int64_t)i * np + j];
+    P[e] = p;
+    S[e] = 0.0;
+  }
+  __syncthreads();
+  for (int t = 0; t < nterms; ++t) {
+    const int a0 = aoff[t], a1 = boff[t], b0 = boff[t], b1 = t + 1 < nterms ? aoff[t + 1] : ncoef;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      double a = 0.0, b = 0.0;
+      for (int q = a0; q < a1; ++q) a += mono[L0 + q] * coef[q * nn + e];
+      for (int q = b0; q < b1; ++q) b += mono[L0 + q] * coef[q * nn + e];
+      Ae[e] = a;
+      Be[e] = b;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      double v = 0.0;
+      for (int k = 0; k < n; ++k) v += P[i * n + k] * Be[k * n + j];
+      PB[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      double v = 0.0;
+      for (int k = 0; k < n; ++k) v += Ae[i * n + k] * PB[k * n + j];
+      S[e] += v;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    Ae[e] = -(S[e] + S[j * n + i]);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[e] = Ae[e];
+  __syncthreads();
+  const bool lmi = smem_chol(S, n);
+  __syncthreads();
+  const bool pos = smem_chol(P, n);
+  if (threadIdx.x == 0 && !(lmi && pos)) atomicAdd(nfail, 1);
+}
+
 // Diagonal of the Schur complement, dense (K x K) or tiled (diagonal pair tiles, Ntil x Ntil):
 // element q of the diagonal sits at G + q*(K+1) (dense) or tile(h,h) + s*(Ntil+1), q = h*Ntil + s.
 __device__ __forceinline__ int64_t diag_off(int64_t q, int64_t K, int64_t Ntil, int64_t L0, int tiled) {
@@ -789,14 +860,15 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
                                       int32_t* nfail_out, void* stream) {
   if (!ctx || !y || npts < 0 || (npts > 0 && !pts_host) || !nfail_out) return POLYA_EINVAL;
   Ctx& c = ctx->c;
-  if ((2 * c.n * c.n + c.L0 + c.nA) * (int64_t)sizeof(double) > 227 * 1024) {
+  const int64_t nextra = c.gen ? c.ncoef : c.nA;
+  if ((2 * c.n * c.n + c.L0 + nextra) * (int64_t)sizeof(double) > 227 * 1024) {
     c.last_error = "polya_verdict: n <= 118 (two n x n matrices per point in shared memory)";
     return POLYA_EINVAL;
   }
   cudaStream_t s = (cudaStream_t)stream;
   *nfail_out = 0;
   if (npts == 0) return POLYA_OK;
-  int32_t *dWp = nullptr, *dWa = nullptr;
+  int32_t *dWp = nullptr, *dWa = nullptr, *dgen = nullptr;
   double *dpts = nullptr, *dscr = nullptr;
   int* dfail = nullptr;
   polya_status ret = POLYA_OK;
@@ -805,16 +877,31 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
     CK(cudaMalloc(&dWa, c.Wa.size() * sizeof(int32_t)));
     CK(cudaMalloc(&dpts, (size_t)npts * c.l * sizeof(double)));
     CK(cudaMalloc(&dfail, sizeof(int)));
-    CK(cudaMalloc(&dscr, (size_t)npts * c.n * c.n * sizeof(double)));
+    CK(cudaMalloc(&dscr, (size_t)npts * (c.gen ? 3 : 1) * c.n * c.n * sizeof(double)));
     CK(cudaMemcpyAsync(dWp, c.Wp.data(), c.Wp.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dWa, c.Wa.data(), c.Wa.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dpts, pts_host, (size_t)npts * c.l * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(dfail, 0, sizeof(int), s));
     CK(launch_vmap(c, y, s));   // V_h(y) -> arena slots id_Vy + h
-    const size_t sm = (2 * (size_t)c.n * c.n + c.L0 + c.nA) * sizeof(double);
-    CK(cudaFuncSetAttribute(k_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_grid<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, (int)c.nA, dWp, dWa, c.arena, c.mstride,
-                                          (int)c.np, c.id_Vy, c.dA, dpts, dscr, dfail);
+    const size_t sm = (2 * (size_t)c.n * c.n + c.L0 + nextra) * sizeof(double);
+    if (c.gen) {
+      const int nt = (int)c.gp_aoff.size();
+      std::vector<int32_t> tab(c.coef_exp);   // [ncoef][l] exponents, then aoff[nt], boff[nt]
+      tab.insert(tab.end(), c.gp_aoff.begin(), c.gp_aoff.end());
+      tab.insert(tab.end(), c.gp_boff.begin(), c.gp_boff.end());
+      CK(cudaMalloc(&dgen, tab.size() * sizeof(int32_t)));
+      CK(cudaMemcpyAsync(dgen, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      const int32_t* dexp = dgen;
+      const int32_t* dao = dgen + c.coef_exp.size();
+      CK(cudaFuncSetAttribute(k_grid_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_grid_gen<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, nt, (int)c.ncoef, dWp, dexp, dao,
+                                                 dao + nt, c.d_coef, c.arena, c.mstride, (int)c.np, c.id_Vy, dpts,
+                                                 dscr, dfail);
+    } else {
+      CK(cudaFuncSetAttribute(k_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_grid<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, (int)c.nA, dWp, dWa, c.arena, c.mstride,
+                                            (int)c.np, c.id_Vy, c.dA, dpts, dscr, dfail);
+    }
     ++c.launches;
     CK(cudaGetLastError());
     int h = 0;
@@ -827,6 +914,7 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
   }
   cudaFree(dWp);
   cudaFree(dWa);
+  cudaFree(dgen);
   cudaFree(dpts);
   cudaFree(dscr);
   cudaFree(dfail);

@@ -43,6 +43,23 @@ __global__ void k_setup_H(double* __restrict__ arena, int64_t ms, int np, int n,
   }
 }
 
+// Generalised form (reading R18): dst = sum_q w_q coef[src_q] (trans: its transpose), zero-padded.
+__global__ void k_wsum(double* __restrict__ arena, int64_t ms, int np, int n, const double* __restrict__ coef,
+                       const WsumItem* __restrict__ items, const WsumTerm* __restrict__ terms) {
+  const WsumItem it = items[blockIdx.x];
+  double* D = arena + (int64_t)it.dst * ms;
+  const int64_t nn = (int64_t)n * n;
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    double v = 0.0;
+    if (i < n && j < n) {
+      const int64_t off = it.trans ? (int64_t)j * n + i : (int64_t)i * n + j;
+      for (int q = it.beg; q < it.end; ++q) v += terms[q].w * coef[terms[q].src * nn + off];
+    }
+    D[e] = v;
+  }
+}
+
 __global__ void k_pad_copy(double* __restrict__ arena, int64_t ms, int np, int n, const double* __restrict__ src,
                            int64_t id0, int sym) {
   const int64_t b = blockIdx.x;
@@ -236,6 +253,13 @@ cudaError_t launch_setup_H(Ctx& c, cudaStream_t s) {
   const int64_t nnzH = (int64_t)c.Hh.size();
   if (nnzH == 0) return cudaSuccess;
   k_setup_H<<<(unsigned)nnzH, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, (int)c.nA, c.dA, c.dHw, c.id_H);
+  ++c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wsum(Ctx& c, cudaStream_t s) {
+  if (c.n_ws == 0) return cudaSuccess;
+  k_wsum<<<(unsigned)c.n_ws, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.d_coef, c.d_ws_items, c.d_ws_terms);
   ++c.launches;
   return cudaGetLastError();
 }

@@ -108,7 +108,14 @@ T* dupload(const std::vector<T>& v) {
   return p;
 }
 
-void build(Ctx& c, const double* A_host, bool device = true) {
+// The generalised form's input terms (polya_setup_general, reading R18).
+struct GenInput {
+  int32_t nterms;
+  const int32_t *deg_a, *deg_b;
+  const double *At, *Bt;
+};
+
+void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi = nullptr) {
   const polya_config& g = c.cfg;
   c.n = g.n;
   c.l = g.l;
@@ -163,9 +170,66 @@ void build(Ctx& c, const double* A_host, bool device = true) {
       }
   // nonzero H entries (h, m), m-major, with their integer weights per lambda
   c.Hidx.assign(c.L0 * c.M, -1);
+  c.Hcnt.assign(c.L0 * c.M, 0);
   c.Hh.clear(); c.Hm.clear(); c.Hw.clear();
   std::vector<double> w(c.nA);
-  for (int64_t m = 0; m < c.M; ++m) {
+  // generalised form: term t = (A_t, B_t) as weighted sums of coefficient matrices (src, weight)
+  std::vector<std::vector<std::pair<int32_t, double>>> tA, tB;
+  c.gen = gi != nullptr;
+  if (c.gen) {
+    // coefficient layout: pair i's At coefficients (W_{a_i} order), then its Bt coefficients
+    std::vector<std::vector<int32_t>> Wa_i(gi->nterms), Wb_i(gi->nterms);
+    c.gp_da.assign(gi->deg_a, gi->deg_a + gi->nterms);
+    c.gp_db.assign(gi->deg_b, gi->deg_b + gi->nterms);
+    c.gp_aoff.clear(); c.gp_boff.clear(); c.coef_exp.clear();
+    int64_t off = 0;
+    for (int32_t i = 0; i < gi->nterms; ++i) {
+      enumerate(l, c.gp_da[i], Wa_i[i]);
+      enumerate(l, c.gp_db[i], Wb_i[i]);
+      c.gp_aoff.push_back((int32_t)off);
+      off += (int64_t)Wa_i[i].size() / l;
+      c.gp_boff.push_back((int32_t)off);
+      off += (int64_t)Wb_i[i].size() / l;
+      c.coef_exp.insert(c.coef_exp.end(), Wa_i[i].begin(), Wa_i[i].end());
+      c.coef_exp.insert(c.coef_exp.end(), Wb_i[i].begin(), Wb_i[i].end());
+    }
+    c.ncoef = off;
+    // block gamma_m of element (h, k): -sum_{i, lambda, mu} multinomial(d2; gamma - h - lambda - mu)
+    //   (At_{i,lambda} E_k Bt_{i,mu} + transpose); the sum over the larger of W_{a_i}, W_{b_i} is folded
+    //   into one weighted coefficient sum, so (h, m) gets min(f(l,a_i), f(l,b_i)) terms per i at most
+    for (int64_t m = 0; m < c.M; ++m) {
+      const int32_t* gm = &c.WM[m * l];
+      for (int64_t h = 0; h < c.L0; ++h) {
+        const int32_t first = (int32_t)c.Hh.size();
+        for (int32_t i = 0; i < gi->nterms; ++i) {
+          const int64_t na = (int64_t)Wa_i[i].size() / l, nbm = (int64_t)Wb_i[i].size() / l;
+          const bool byA = na <= nbm;   // one term per lambda (B summed) or per mu (A summed)
+          for (int64_t u = 0; u < (byA ? na : nbm); ++u) {
+            std::vector<std::pair<int32_t, double>> sum;
+            for (int64_t v = 0; v < (byA ? nbm : na); ++v) {
+              const int64_t lam = byA ? u : v, mu = byA ? v : u;
+              for (int64_t x = 0; x < l; ++x)
+                tmp[x] = gm[x] - c.Wp[h * l + x] - Wa_i[i][lam * l + x] - Wb_i[i][mu * l + x];
+              const int64_t wv = multinomial(g.d2, tmp.data(), l);
+              if (wv) sum.push_back({(int32_t)((byA ? c.gp_boff[i] + mu : c.gp_aoff[i] + lam)), (double)wv});
+            }
+            if (sum.empty()) continue;
+            std::vector<std::pair<int32_t, double>> one{{(int32_t)(byA ? c.gp_aoff[i] + u : c.gp_boff[i] + u), 1.0}};
+            tA.push_back(byA ? one : sum);
+            tB.push_back(byA ? sum : one);
+            c.Hh.push_back((int32_t)h);
+            c.Hm.push_back((int32_t)m);
+          }
+        }
+        const int32_t cnt = (int32_t)c.Hh.size() - first;
+        if (cnt) {
+          c.Hidx[h * c.M + m] = first;
+          c.Hcnt[h * c.M + m] = cnt;
+        }
+      }
+    }
+  }
+  for (int64_t m = 0; m < c.M && !c.gen; ++m) {
     const int32_t* gm = &c.WM[m * l];
     for (int64_t h = 0; h < c.L0; ++h) {
       bool nz = false;
@@ -177,6 +241,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
       }
       if (!nz) continue;
       c.Hidx[h * c.M + m] = (int32_t)c.Hh.size();
+      c.Hcnt[h * c.M + m] = 1;
       c.Hh.push_back((int32_t)h);
       c.Hm.push_back((int32_t)m);
       c.Hw.insert(c.Hw.end(), w.begin(), w.end());
@@ -198,7 +263,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
     }
     for (int64_t m = 0; m < c.M; ++m) {
       int64_t mu = 0;
-      for (int64_t h = 0; h < c.L0; ++h) mu += c.Hidx[h * c.M + m] >= 0;
+      for (int64_t h = 0; h < c.L0; ++h) mu += c.Hcnt[h * c.M + m];
       bc[c.L + m + 1] = bc[c.L + m] + 4.0 * (double)(mu * mu);
     }
     auto at = [&](int64_t r) -> int64_t {
@@ -224,7 +289,7 @@ void build(Ctx& c, const double* A_host, bool device = true) {
         ph2[p] = (int32_t)h2;
         int64_t mu = 0, nu = 0;
         for (int64_t m = 0; m < c.M; ++m)
-          if (owned(c.L + m) && c.Hidx[h * c.M + m] >= 0 && c.Hidx[h2 * c.M + m] >= 0) ++mu;
+          if (owned(c.L + m)) mu += (int64_t)c.Hcnt[h * c.M + m] * c.Hcnt[h2 * c.M + m];  // (q, q') entries
         for (int64_t j = 0; j < c.L; ++j)
           if (owned(j) && c.beta[h * c.L + j] && c.beta[h2 * c.L + j]) ++nu;
         pMu[p] = mu;
@@ -291,12 +356,19 @@ void build(Ctx& c, const double* A_host, bool device = true) {
   c.id_Zero = id; id += 1;
   c.id_Xb = id; id += c.nnz_beta;
   c.id_Wb = id; id += c.nnz_beta;
-  c.id_Q = id; id += nQR;
-  c.id_R = id; id += nQR;
+  const int64_t qr_per = c.gen ? 4 : 1;   // generalised: L1..L4 and R1..R4 per (pair, m, q, q')
+  c.id_Q = id; id += qr_per * nQR;
+  c.id_R = id; id += qr_per * nQR;
   c.id_Xt = id; id += c.nb;
   c.id_T = id; id += nnzH;
   c.id_Vy = id; id += c.L0;
   c.id_S = id; id += c.M;
+  if (c.gen) {
+    c.id_B = id; id += nnzH;      // B_t
+    c.id_Abar = id; id += nnzH;   // A_t^T
+    c.id_XA = id; id += nnzH;     // Xs A_t (adjoint)
+    c.id_VB = id; id += nnzH;     // V_h(y) B_t (apply)
+  }
   c.nmats = id;
   if (c.nmats > INT32_MAX) throw Fail{POLYA_EOVERFLOW, "too many arena matrices"};
   c.arena = dalloc<double>(mul_chk(c.nmats, c.mstride));
@@ -324,6 +396,16 @@ void build(Ctx& c, const double* A_host, bool device = true) {
     for (int64_t t = 0; t < nnzH; ++t) {
       int32_t b = (int32_t)(c.L + c.Hm[t]);
       if (!owned(b)) continue;   // SHARD_BLOCKS: only this rank's Lyapunov blocks enter its partial G
+      if (c.gen) {   // U = B X, V = B W, Ut = A^T X, Vt = A^T W
+        const int32_t ids[4][2] = {{(int32_t)(c.id_B + t), (int32_t)(c.id_X + b)}, {(int32_t)(c.id_B + t), (int32_t)(c.id_W + b)},
+                                   {(int32_t)(c.id_Abar + t), (int32_t)(c.id_X + b)}, {(int32_t)(c.id_Abar + t), (int32_t)(c.id_W + b)}};
+        const int64_t dst[4] = {c.id_U, c.id_V, c.id_Ut, c.id_Vt};
+        for (int k = 0; k < 4; ++k) {
+          it.push_back({(int32_t)(dst[k] + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+          tm.push_back({ids[k][0], ids[k][1], 0, 0, 1.0});
+        }
+        continue;
+      }
       it.push_back({(int32_t)(c.id_U + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
       tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_X + b), 0, 0, 1.0});
       it.push_back({(int32_t)(c.id_V + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
@@ -336,22 +418,51 @@ void build(Ctx& c, const double* A_host, bool device = true) {
     c.n_items_UV = (int64_t)it.size();
     c.d_items_UV = dupload(it);
     c.d_terms_UV = dupload(tm);
-    // adjoint: T_t = H_t Xt_{L+m}
+    // adjoint: T_t = H_t Xt_{L+m}; generalised T_t = B_t (Xt_{L+m} A_t) (two passes)
     it.clear(); tm.clear();
+    if (c.gen) {
+      for (int64_t t = 0; t < nnzH; ++t) {
+        it.push_back({(int32_t)(c.id_XA + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        tm.push_back({(int32_t)(c.id_Xt + c.L + c.Hm[t]), (int32_t)(c.id_Abar + t), 1, 0, 1.0});
+      }
+      c.n_items_T0 = (int64_t)it.size();
+      c.d_items_T0 = dupload(it);
+      c.d_terms_T0 = dupload(tm);
+      it.clear(); tm.clear();
+    }
     for (int64_t t = 0; t < nnzH; ++t) {
       it.push_back({(int32_t)(c.id_T + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
-      tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_Xt + c.L + c.Hm[t]), 0, 0, 1.0});
+      if (c.gen)
+        tm.push_back({(int32_t)(c.id_B + t), (int32_t)(c.id_XA + t), 0, 0, 1.0});
+      else
+        tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_Xt + c.L + c.Hm[t]), 0, 0, 1.0});
     }
     c.n_items_T = (int64_t)it.size();
     c.d_items_T = dupload(it);
     c.d_terms_T = dupload(tm);
-    // apply: S_m = sum_h V_h(y) H_{h,m}
+    // apply: S_m = sum_h V_h(y) H_{h,m}; generalised S_m = sum_t A_t (V_h(y) B_t) (two passes)
     it.clear(); tm.clear();
+    if (c.gen) {
+      for (int64_t t = 0; t < nnzH; ++t) {
+        it.push_back({(int32_t)(c.id_VB + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        tm.push_back({(int32_t)(c.id_Vy + c.Hh[t]), (int32_t)(c.id_B + t), 0, 0, 1.0});
+      }
+      c.n_items_S0 = (int64_t)it.size();
+      c.d_items_S0 = dupload(it);
+      c.d_terms_S0 = dupload(tm);
+      it.clear(); tm.clear();
+    }
     for (int64_t m = 0; m < c.M; ++m) {
       int32_t b0 = (int32_t)tm.size();
       for (int64_t h = 0; h < c.L0; ++h) {
         int32_t t = c.Hidx[h * c.M + m];
-        if (t >= 0) tm.push_back({(int32_t)(c.id_Vy + h), (int32_t)(c.id_H + t), 0, 0, 1.0});
+        if (t < 0) continue;
+        if (c.gen) {
+          for (int32_t q = t; q < t + c.Hcnt[h * c.M + m]; ++q)
+            tm.push_back({(int32_t)(c.id_H + q), (int32_t)(c.id_VB + q), 0, 0, 1.0});
+        } else {
+          tm.push_back({(int32_t)(c.id_Vy + h), (int32_t)(c.id_H + t), 0, 0, 1.0});
+        }
       }
       it.push_back({(int32_t)(c.id_S + m), b0, (int32_t)tm.size(), 0});
     }
@@ -377,6 +488,30 @@ void build(Ctx& c, const double* A_host, bool device = true) {
         int32_t th = c.Hidx[h * c.M + m], th2 = c.Hidx[h2 * c.M + m];
         if (th < 0 || th2 < 0 || !owned(c.L + m)) continue;
         const int32_t b = (int32_t)(c.L + m);
+        if (c.gen) {
+          // F = -sum_q (A_q E B_q + B_q^T E A_q^T): per (q, q') the four (L, R) of tr(E_k L E_l R) are
+          // (B X A', B' W A), (B X B'^T, A'^T W A), (A^T X A', B' W B^T), (A^T X B'^T, A'^T W B^T)
+          // (reading R18; (H^T, I) gives back the four terms below)
+          for (int32_t q1 = th; q1 < th + c.Hcnt[h * c.M + m]; ++q1)
+            for (int32_t q2 = th2; q2 < th2 + c.Hcnt[h2 * c.M + m]; ++q2) {
+              const int32_t Ab1 = (int32_t)(c.id_Abar + q1), Ab2 = (int32_t)(c.id_Abar + q2);
+              const int32_t B1 = (int32_t)(c.id_B + q1), B2 = (int32_t)(c.id_B + q2);
+              const int32_t spec[4][4] = {{(int32_t)(c.id_U + q1), Ab2, (int32_t)(c.id_V + q2), Ab1},
+                                          {(int32_t)(c.id_U + q1), B2, (int32_t)(c.id_Vt + q2), Ab1},
+                                          {(int32_t)(c.id_Ut + q1), Ab2, (int32_t)(c.id_V + q2), B1},
+                                          {(int32_t)(c.id_Ut + q1), B2, (int32_t)(c.id_Vt + q2), B1}};
+              for (int k = 0; k < 4; ++k) {
+                const int32_t idL = (int32_t)(c.id_Q + 4 * q + k), idR = (int32_t)(c.id_R + 4 * q + k);
+                it.push_back({idL, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+                tm.push_back({spec[k][0], spec[k][1], 1, 0, 1.0});
+                it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+                tm.push_back({spec[k][2], spec[k][3], 1, 0, 1.0});
+                kL.push_back(idL); kR.push_back(idR);
+              }
+              ++q;
+            }
+          continue;
+        }
         const int32_t idQ = (int32_t)(c.id_Q + q), idR = (int32_t)(c.id_R + q);
         // Q_{hh'} = U_h H_{h'}^T,  R_{h'h} = V_{h'} H_h^T
         it.push_back({idQ, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
@@ -440,7 +575,10 @@ void build(Ctx& c, const double* A_host, bool device = true) {
         if (c.beta[h * c.L + j]) { hj.push_back((int32_t)j); hw.push_back((double)c.beta[h * c.L + j]); }
       hbeg.push_back((int32_t)hj.size());
       for (int64_t m = 0; m < c.M; ++m)
-        if (c.Hidx[h * c.M + m] >= 0) { lt.push_back(c.Hidx[h * c.M + m]); lm.push_back((int32_t)m); }
+        for (int32_t t = c.Hidx[h * c.M + m]; t >= 0 && t < c.Hidx[h * c.M + m] + c.Hcnt[h * c.M + m]; ++t) {
+          lt.push_back(t);
+          lm.push_back((int32_t)m);
+        }
       lbeg.push_back((int32_t)lt.size());
     }
     c.d_bP_beg = dupload(bbeg); c.d_bP_h = dupload(bh); c.d_bP_w = dupload(bw);
@@ -449,6 +587,38 @@ void build(Ctx& c, const double* A_host, bool device = true) {
   }
 
   // ---- H on the device (kernel K1) ----------------------------------------------------------------
+  if (c.gen) {   // A_t, A_t^T, B_t as weighted coefficient sums (k_wsum)
+    std::vector<double> coef;
+    const int64_t nn = c.n * c.n;
+    coef.reserve(c.ncoef * nn);
+    int64_t ua = 0, ub = 0;   // running offsets into the caller's At / Bt concatenations
+    for (size_t i = 0; i < c.gp_da.size(); ++i) {
+      const int64_t na = c.gp_boff[i] - c.gp_aoff[i];
+      const int64_t nbm = (i + 1 < c.gp_da.size() ? c.gp_aoff[i + 1] : c.ncoef) - c.gp_boff[i];
+      coef.insert(coef.end(), gi->At + ua * nn, gi->At + (ua + na) * nn);
+      coef.insert(coef.end(), gi->Bt + ub * nn, gi->Bt + (ub + nbm) * nn);
+      ua += na;
+      ub += nbm;
+    }
+    c.d_coef = dupload(coef);
+    std::vector<WsumItem> wi;
+    std::vector<WsumTerm> wt;
+    auto add = [&](int64_t dst, const std::vector<std::pair<int32_t, double>>& sum, int trans) {
+      wi.push_back({(int32_t)dst, (int32_t)wt.size(), (int32_t)(wt.size() + sum.size()), trans});
+      for (auto& p : sum) wt.push_back({p.first, 0, p.second});
+    };
+    for (int64_t t = 0; t < nnzH; ++t) {
+      add(c.id_H + t, tA[t], 0);
+      add(c.id_Abar + t, tA[t], 1);
+      add(c.id_B + t, tB[t], 0);
+    }
+    c.n_ws = (int64_t)wi.size();
+    c.d_ws_items = dupload(wi);
+    c.d_ws_terms = dupload(wt);
+    CU(launch_wsum(c, 0));
+    CU(cudaDeviceSynchronize());
+    return;
+  }
   c.dA = dalloc<double>(mul_chk(c.nA, mul_chk(c.n, c.n)));
   CU(cudaMemcpy(c.dA, A_host, (size_t)c.nA * c.n * c.n * sizeof(double), cudaMemcpyHostToDevice));
   c.dHw = dupload(c.Hw);
@@ -461,7 +631,8 @@ void free_ctx(Ctx& c) {
                 c.d_items_T, c.d_terms_T, c.d_sc_dst, c.d_sc_src, c.d_sc_w, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
                 c.st.pair_kbeg, c.st.pair_item, c.st.kdesc,
-                c.st.cls_a, c.st.cls_b, c.st.counter};
+                c.st.cls_a, c.st.cls_b, c.st.counter, c.d_coef, c.d_ws_items, c.d_ws_terms, c.d_items_T0,
+                c.d_terms_T0, c.d_items_S0, c.d_terms_S0};
   for (void* p : ps)
     if (p) cudaFree(p);
 }
@@ -492,6 +663,39 @@ extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_hos
   } catch (const Fail& f) {
     polya_status s = f.s;
     fprintf(stderr, "polya_setup: %s\n", f.msg.c_str());
+    free_ctx(ctx->c);
+    delete ctx;
+    return s;
+  } catch (const std::bad_alloc&) {
+    free_ctx(ctx->c);
+    delete ctx;
+    return POLYA_ENOMEM;
+  }
+  *out = ctx;
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nterms, const int32_t* deg_a,
+                                           const int32_t* deg_b, const double* At, const double* Bt, polya_ctx** out) {
+  if (!out) return POLYA_EINVAL;
+  *out = nullptr;
+  if (!cfg || nterms < 1 || !deg_a || !deg_b || !At || !Bt) return POLYA_EINVAL;
+  const polya_config& g = *cfg;
+  if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
+      g.rank < 0 || g.rank >= g.nranks || (g.shard != POLYA_SHARD_TILES && g.shard != POLYA_SHARD_BLOCKS))
+    return POLYA_EINVAL;
+  for (int32_t i = 0; i < nterms; ++i)   // every term homogeneous of the one total degree cfg->da (R18)
+    if (deg_a[i] < 0 || deg_b[i] < 0 || deg_a[i] + deg_b[i] != g.da) return POLYA_EINVAL;
+  polya_ctx* ctx = new (std::nothrow) polya_ctx();
+  if (!ctx) return POLYA_ENOMEM;
+  ctx->c.cfg = g;
+  const GenInput gi{nterms, deg_a, deg_b, At, Bt};
+  try {
+    if (cudaGetDevice(&ctx->c.device) != cudaSuccess) throw Fail{POLYA_ECUDA, "no CUDA device"};
+    build(ctx->c, nullptr, true, &gi);
+  } catch (const Fail& f) {
+    polya_status s = f.s;
+    fprintf(stderr, "polya_setup_general: %s\n", f.msg.c_str());
     free_ctx(ctx->c);
     delete ctx;
     return s;
@@ -651,6 +855,10 @@ extern "C" polya_status polya_get_C(const polya_ctx* ctx, double* out) {
 extern "C" polya_status polya_get_H(const polya_ctx* ctx, double* out) {
   if (!ctx || !out) return POLYA_EINVAL;
   const Ctx& c = ctx->c;
+  if (c.gen) {
+    const_cast<polya_ctx*>(ctx)->c.last_error = "polya_get_H: no H table in the generalised form";
+    return POLYA_EINVAL;
+  }
   const int64_t n = c.n, nn = n * n;
   std::memset(out, 0, (size_t)c.L0 * c.M * nn * sizeof(double));
   std::vector<double> buf(c.mstride);
@@ -674,6 +882,7 @@ extern "C" polya_status polya_apply(polya_ctx* ctx, const double* y, double* out
   cudaStream_t s = (cudaStream_t)stream;
   try {
     CU(launch_vmap(c, y, s));
+    CU(launch_gemm(c, c.d_items_S0, c.d_terms_S0, c.n_items_S0, s));   // generalised form only
     CU(launch_gemm(c, c.d_items_S, c.d_terms_S, c.n_items_S, s));
     CU(launch_apply_out(c, y, out, s));
   } catch (const Fail& f) {
@@ -688,6 +897,7 @@ extern "C" polya_status polya_adjoint(polya_ctx* ctx, const double* X, double* y
   cudaStream_t s = (cudaStream_t)stream;
   try {
     CU(launch_pad_copy(c, X, c.id_Xt, c.nb, 1, s));
+    CU(launch_gemm(c, c.d_items_T0, c.d_terms_T0, c.n_items_T0, s));   // generalised form only
     CU(launch_gemm(c, c.d_items_T, c.d_terms_T, c.n_items_T, s));
     CU(launch_adjoint_reduce(c, y, s));
   } catch (const Fail& f) {

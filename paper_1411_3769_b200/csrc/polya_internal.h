@@ -26,6 +26,15 @@ struct GemmItem {
   int32_t c_id, tbeg, tend, pad_;
 };
 
+// dst = sum_terms w * coef[src] (or its transpose): the generalised form's A_t, A_t^T, B_t (set-up).
+struct WsumItem {
+  int32_t dst, beg, end, trans;
+};
+struct WsumTerm {
+  int32_t src, pad_;
+  double w;
+};
+
 // Device-side tables of the Schur assembly (kernel K4).
 struct SchurTables {
   int32_t* pair_h = nullptr;      // [npairs_local]      h  (row block of the pair)
@@ -49,7 +58,15 @@ struct Ctx {
   std::vector<int64_t> beta;           // [L0][L]
   std::vector<double> c;               // [L]
   std::vector<int32_t> Hh, Hm;         // nonzero H entries t -> (h, m), m-major
-  std::vector<int32_t> Hidx;           // [L0][M] -> t or -1
+  std::vector<int32_t> Hidx;           // [L0][M] -> first t or -1
+  std::vector<int32_t> Hcnt;           // [L0][M] -> number of terms t of (h, m): 0/1, or any (generalised)
+  // generalised form (polya_setup_general, reading R18): term t = (A_t, B_t), F = -sum_t (A_t E B_t + B_t^T E A_t^T)
+  bool gen = false;
+  int64_t ncoef = 0;                   // coefficient matrices of all At_i, Bt_i (n x n each)
+  std::vector<int32_t> gp_da, gp_db, gp_aoff, gp_boff;  // per input term i: degrees, coefficient offsets
+  std::vector<int32_t> coef_exp;       // [ncoef][l] exponent of each coefficient matrix
+  double* d_coef = nullptr;            // [ncoef][n][n]
+  WsumItem* d_ws_items = nullptr; WsumTerm* d_ws_terms = nullptr; int64_t n_ws = 0;
   std::vector<double> Hw;              // [nnzH][nA] integer weights multinomial(d2; gamma-h-lambda)
   // pairs and work items
   int64_t npairs = 0, pair0 = 0, pair1 = 0;
@@ -62,6 +79,7 @@ struct Ctx {
   int64_t mstride = 0, nmats = 0;
   int64_t id_Ut = 0, id_Vt = 0, id_Zero = 0, id_Xb = 0, id_Wb = 0;
   int32_t* d_sc_dst = nullptr; int32_t* d_sc_src = nullptr; double* d_sc_w = nullptr; int64_t n_sc = 0;
+  int64_t id_B = 0, id_Abar = 0, id_XA = 0, id_VB = 0;   // generalised form only
   int64_t id_X = 0, id_W = 0, id_H = 0, id_U = 0, id_V = 0, id_Q = 0, id_R = 0, id_Xt = 0, id_T = 0,
           id_Vy = 0, id_S = 0;
   int64_t nQR = 0;
@@ -73,6 +91,8 @@ struct Ctx {
   GemmItem* d_items_QR = nullptr; GemmTerm* d_terms_QR = nullptr; int64_t n_items_QR = 0;
   GemmItem* d_items_T = nullptr; GemmTerm* d_terms_T = nullptr; int64_t n_items_T = 0;
   GemmItem* d_items_S = nullptr; GemmTerm* d_terms_S = nullptr; int64_t n_items_S = 0;
+  GemmItem* d_items_T0 = nullptr; GemmTerm* d_terms_T0 = nullptr; int64_t n_items_T0 = 0;  // generalised: XA_t
+  GemmItem* d_items_S0 = nullptr; GemmTerm* d_terms_S0 = nullptr; int64_t n_items_S0 = 0;  // generalised: VB_t
   // apply / adjoint tables
   int32_t* d_bP_beg = nullptr;   // [L+1]  P-block active-h ranges
   int32_t* d_bP_h = nullptr;     // [nnz_beta]
@@ -97,6 +117,7 @@ struct Ctx {
 
 // ---- kernel launchers (kernels.cu / schur.cu) -------------------------------------------------
 cudaError_t launch_setup_H(Ctx& c, cudaStream_t s);
+cudaError_t launch_wsum(Ctx& c, cudaStream_t s);
 cudaError_t launch_pad_copy(Ctx& c, const double* src, int64_t id0, int64_t count, int symmetrize,
                             cudaStream_t s);
 cudaError_t launch_scale_copy(Ctx& c, cudaStream_t s);

@@ -59,3 +59,15 @@ def test_library_then_torch_import_order():
             "import torch; import torch.distributed; print('ok')") % ROOT
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_setup_general_rejects_mixed_degrees_without_a_gpu():
+    """polya_setup_general validates before touching the device: terms of different total degree
+    (R18: one common degree cfg->da) are EINVAL."""
+    import numpy as np
+    import pytest
+    import paper_1411_3769_b200 as pb
+    n, l = 2, 2
+    terms = [(np.zeros((2, n, n)), 1, np.zeros((2, n, n)), 1), (np.zeros((2, n, n)), 1, np.zeros((1, n, n)), 0)]
+    with pytest.raises(pb.PolyaError, match="invalid argument"):
+        pb.Polya.general(terms, n, l, 1, 1, 1)

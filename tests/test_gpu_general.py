@@ -1,0 +1,142 @@
+"""GPU parity of the generalised LMI form (polya_setup_general, reading R18)
+against the oracle's build_problem_general (pinned in tests/test_oracle_general.py).
+
+Bars as tests/test_gpu_parity.py: B^T(y), B(X) and G within 1e-10 relative error; plus the
+continuous-time special case against the standard context, the block / tile shardings, and
+discrete-time certificates end to end (polya_ipm_solve + polya_verdict on the device).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ipm as oipm
+from oracle import sdp as osdp
+from oracle.monomials import enumerate_W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_1411_3769_b200 as pb
+    pb.lib()
+    assert torch.cuda.is_available()
+    return pb
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# (n, l, dp, d1, d2, degree pairs): ragged n, several chunks, mixed degrees, d2 = 0, dp = 0
+CASES = [(3, 2, 1, 1, 1, [(1, 1), (2, 0)]),
+         (9, 2, 1, 1, 1, [(1, 1), (0, 2)]),
+         (13, 3, 1, 1, 1, [(1, 0), (0, 1)]),
+         (6, 2, 2, 1, 0, [(1, 1)]),
+         (5, 1, 0, 2, 2, [(2, 0), (1, 1), (0, 2)]),
+         (20, 2, 1, 1, 1, [(1, 1)])]
+
+
+def _case(n, l, dp, d1, d2, degs, seed=0):
+    rng = np.random.default_rng(seed)
+    terms = synth.random_terms(n, l, degs, rng, lambda d: len(enumerate_W(l, d)))
+    P = osdp.build_problem_general(terms, n, l, dp, d1, d2)
+    X, W = synth.spd_blocks(n, P.nblocks, rng)
+    return terms, P, X, W
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "n{}l{}dp{}d{}{}_{}".format(*c[:5], len(c[5])))
+def test_operators_and_schur_parity(pb, case):
+    terms, P, X, W = _case(*case)
+    n, l, dp, d1, d2, _ = case
+    ctx = pb.Polya.general(terms, n, l, dp, d1, d2)
+    assert (ctx.K, ctx.M, ctx.nblocks) == (P.K, P.M, P.nblocks)
+    rng = np.random.default_rng(7)
+    y = rng.normal(size=P.K)
+    assert _rel(ctx.apply(_dev(y)).cpu().numpy(), osdp.apply_vmap(P, y)) <= TOL
+    R = rng.normal(size=X.shape)
+    assert _rel(ctx.adjoint(_dev(R)).cpu().numpy(), osdp.adjoint_trace(P, R)) <= TOL
+    Gref = osdp.schur_structured(P, X, W)
+    if P.K <= 60:
+        assert _rel(Gref, osdp.schur_literal(P, X, W)) <= 1e-12
+    G = ctx.schur(_dev(X), _dev(W)).cpu().numpy()
+    assert _rel(G, Gref) <= TOL
+    assert np.array_equal(G, G.T)
+    ctx.close()
+
+
+def test_continuous_time_case_equals_standard_context(pb):
+    c = synth.small_config(12, 3, 2, 1, 2)
+    rng = np.random.default_rng(0)
+    A = synth.vertex_matrices(c, rng)
+    std = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
+    gen = pb.Polya.general([(np.array([a.T for a in A]), 1, np.eye(c.n)[None], 0)], c.n, c.l, c.dp, c.d1, c.d2)
+    X, W = synth.spd_blocks(c.n, std.nblocks, rng)
+    Gs = std.schur(_dev(X), _dev(W)).cpu().numpy()
+    Gg = gen.schur(_dev(X), _dev(W)).cpu().numpy()
+    assert _rel(Gg, Gs) <= 1e-13
+    y = rng.normal(size=std.K)
+    assert _rel(gen.apply(_dev(y)).cpu().numpy(), std.apply(_dev(y)).cpu().numpy()) <= 1e-14
+    assert std.dims["useful_flops_schur"] == gen.dims["useful_flops_schur"]
+    with pytest.raises(pb.PolyaError):
+        gen.H()
+    std.close()
+    gen.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shardings_partition_G(pb, world):
+    terms, P, X, W = _case(13, 3, 1, 1, 1, [(1, 1), (2, 0)], seed=3)
+    Xd, Wd = _dev(X), _dev(W)
+    ref = pb.Polya.general(terms, 13, 3, 1, 1, 1)
+    G = ref.schur(Xd, Wd).cpu().numpy()
+    ref.close()
+    acc_b = np.zeros_like(G)
+    acc_t = np.zeros_like(G)
+    for r in range(world):
+        cb = pb.Polya.general(terms, 13, 3, 1, 1, 1, rank=r, nranks=world, shard=pb.SHARD_BLOCKS)
+        acc_b += cb.schur(Xd, Wd).cpu().numpy()
+        cb.close()
+        ct = pb.Polya.general(terms, 13, 3, 1, 1, 1, rank=r, nranks=world)
+        Gr = ct.schur(Xd, Wd, G=torch.zeros(P.K, P.K, dtype=torch.float64, device="cuda")).cpu().numpy()
+        acc_t += Gr
+        ct.close()
+    assert _rel(acc_b, G) <= 1e-12
+    assert _rel(acc_t, G) == 0.0     # tile sharding writes disjoint entries
+
+
+@pytest.mark.parametrize("unstable", [False, True])
+def test_discrete_time_certificates(pb, unstable):
+    from paper_1411_3769_b200 import robust
+    n, l = 4, 3
+    A = synth.discrete_vertex_matrices(n, l, 0.8, np.random.default_rng(3), unstable=unstable)
+    terms = synth.discrete_time_terms(A)
+    r = robust.certify(None, n, l, 1, 1, 1, terms=terms, samples=300)
+    assert r["certified"] == (not unstable), r
+    P = osdp.build_problem_general(terms, n, l, 1, 1, 1)
+    assert oipm.verdict(P, samples=100) == (not unstable)
+
+
+def test_verdict_kernel_matches_oracle_grid_check(pb):
+    from paper_1411_3769_b200 import robust
+    n, l = 3, 2
+    A = synth.discrete_vertex_matrices(n, l, 0.7, np.random.default_rng(5))
+    terms = synth.discrete_time_terms(A)
+    P = osdp.build_problem_general(terms, n, l, 1, 1, 1)
+    ok, X, Z, y, it = oipm.solve(P)
+    assert ok
+    ctx = pb.Polya.general(terms, n, l, 1, 1, 1)
+    pts = robust.simplex_points(l, 200, 0)
+    assert ctx.verdict(_dev(y), pts) == 0 and oipm.grid_check(P, y, 200, 0)
+    bad = y.copy()
+    bad[:P.Ntil] *= -1.0
+    assert ctx.verdict(_dev(bad), pts) > 0 and not oipm.grid_check(P, bad, 200, 0)
+    ctx.close()
