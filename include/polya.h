@@ -127,12 +127,15 @@ polya_status polya_setup(const polya_config* cfg, const double* A_host, polya_ct
  * At: the concatenation over i of double[f(l,deg_a[i])][n][n] (coefficients in W_{deg_a[i]} order),
  * Bt likewise; both copied.  The continuous-time polya_setup is the case nterms = 1,
  * (A^T, 1, I, 0); discrete time A^T P A - P < 0 is [(A^T/2, 1, A, 1), (-I/2 per vertex, 1, I per
- * vertex, 1)].  Lyapunov block gamma of the dual element (h, k) is
+ * vertex, 1)].  R_host (nullable = 0): the constant term sum_i R_i(alpha), homogeneous of degree
+ * dp + da, double[f(l,dp+da)][n][n] symmetric, W_{dp+da} order; it becomes C on the Lyapunov blocks,
+ * C_{L+m} = sum_rho multinomial(d2; gamma_m - rho) R_rho (the dual constraint B^T(y) - C >= 0 is then
+ * the LMI with "+ R < 0").  Lyapunov block gamma of the dual element (h, k) is
  *     -sum_{i,lambda,mu} multinomial(d2; gamma - h - lambda - mu) (At_{i,lambda} E_k Bt_{i,mu} + transpose);
  * every other entry point (apply, adjoint, Schur, IPM, solve, verdict, sharding) works unchanged
  * on the resulting context, except polya_get_H (EINVAL: no H table).  Errors as polya_setup. */
 polya_status polya_setup_general(const polya_config* cfg, int32_t nterms, const int32_t* deg_a, const int32_t* deg_b,
-                                 const double* At_host, const double* Bt_host, polya_ctx** out);
+                                 const double* At_host, const double* Bt_host, const double* R_host, polya_ctx** out);
 
 polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* out);
 

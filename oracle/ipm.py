@@ -37,10 +37,13 @@ __all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "g
 
 
 def C_blocks(P):
-    """C = diag(c_1 I, ..., c_L I, 0, ..., 0) (Eq. C, Eq. Cj)."""
+    """C = diag(c_1 I, ..., c_L I, 0, ..., 0) (Eq. C, Eq. Cj); the generalised form's constant term
+    R puts (sum alpha)^{d2} R(alpha)'s coefficients on the Lyapunov blocks (reading R18)."""
     C = np.zeros((P.nblocks, P.n, P.n))
     for j in range(P.L):
         C[j] = P.c[j] * np.eye(P.n)
+    if P.CL is not None:
+        C[P.L:] = P.CL
     return C
 
 
@@ -123,6 +126,8 @@ def grid_check(P, y, samples=1000, seed=0):
         if P.gen is not None:   # generalised form: sum_i At_i(alpha) P Bt_i(alpha) + transpose < 0
             Lm = sum(_polya.evaluate(At, P.l, a, al) @ Pa @ _polya.evaluate(Bt, P.l, b, al) for At, a, Bt, b in P.pairs)
             Lm = Lm + Lm.T
+            if P.R is not None:
+                Lm = Lm + _polya.evaluate(P.R, P.l, P.dp + P.da, al)
         else:
             Aa = _polya.evaluate(P.A, P.l, P.da, al)
             Lm = Aa.T @ Pa + Pa @ Aa

@@ -76,6 +76,8 @@ class Problem:
     E: list
     gen: list = None          # generalised form: gen[h][m] = [(A_q, B_q), ...] (build_problem_general)
     pairs: list = None        # its (Atil_i, deg_a, Btil_i, deg_b) terms
+    R: np.ndarray = None      # its constant term R(alpha), coefficients in W_{dp+e} order (or None)
+    CL: np.ndarray = None     # C on the Lyapunov blocks: coefficients of (sum alpha)^{d2} R(alpha)
 
     @property
     def nblocks(self):
@@ -101,9 +103,9 @@ def build_problem(A, n, l, dp, d1, d2, da=1, delta=1e-3) -> Problem:
     return Problem(n, l, dp, da, d1, d2, delta, L0, L, M, Ntil, L0 * Ntil, beta, H, c, A, basis(n))
 
 
-def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3) -> Problem:
-    """The generalised LMI form of PAPER.md:454-459, square case, R_i = 0:
-        P(alpha) > 0,   sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) < 0,
+def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3, R=None) -> Problem:
+    """The generalised LMI form of PAPER.md:454-459, square case:
+        P(alpha) > 0,   sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) + R(alpha) < 0,
     with pairs = [(At_i coefficients [f(l,a_i)][n][n] in W_{a_i} order, a_i, Bt_i coefficients, b_i)],
     all with the same total degree e = a_i + b_i.  Polya's multiplier (sum alpha)^{d2} turns the
     second condition into M = |W_{dp+e+d2}| coefficient blocks (as Eqs. LMI_2/LMI_4 do for A^T P + P A),
@@ -111,7 +113,10 @@ def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3) -> Problem:
     (sum alpha)^{d2} alpha^h At_i(alpha) (.) Bt_i(alpha) is the list of pairs
     (multinomial(d2; gamma - h - lambda - mu) At_{i,lambda}, Bt_{i,mu}), and block m of the dual
     basis element (h, k) is F = -sum_pairs (A E_k B + B^T E_k A^T).  A^T P + P A is the case
-    [(A^T, 1, I, 0)] (tests/test_oracle_general.py)."""
+    [(A^T, 1, I, 0)] (tests/test_oracle_general.py).  R (optional; the sum of the paper's R_i) is
+    homogeneous of degree dp + e, coefficients [f(l, dp+e)][n][n] symmetric in W_{dp+e} order; the
+    dual constraint B^T(y) - C >= 0 then carries C_{L+m} = coefficient of alpha^{gamma_m} in
+    (sum alpha)^{d2} R(alpha) on the Lyapunov blocks (reading R18)."""
     es = {a + b for _, a, _, b in pairs}
     assert len(es) == 1, "all terms must have the same total degree"
     e = es.pop()
@@ -133,8 +138,14 @@ def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3) -> Problem:
                                                  np.asarray(Bt[mi], dtype=float)))
     Ntil = n * (n + 1) // 2
     c = polya.C_scalars(beta, l, dp, delta)
+    CL = None
+    if R is not None:
+        CL = np.zeros((M, n, n))
+        for ri, rho in enumerate(enumerate_W(l, dp + e)):
+            for e2, w in polya.poly_mul(S, {tuple(rho): 1}).items():
+                CL[idx[e2]] += float(w) * np.asarray(R[ri], dtype=float)
     return Problem(n, l, dp, e, d1, d2, delta, L0, L, M, Ntil, L0 * Ntil, beta, np.zeros((L0, M, 0, 0)), c, None,
-                   basis(n), gen=gen, pairs=pairs)
+                   basis(n), gen=gen, pairs=pairs, R=R, CL=CL)
 
 
 def vmap(P: Problem, x, h: int):

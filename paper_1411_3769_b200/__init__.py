@@ -78,7 +78,7 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
-    L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, vp, vp, vp, vp, ctypes.POINTER(vp)]
+    L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
     L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
     L.polya_plan.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Dims)]
     L.polya_get_exponents.argtypes = [vp, ctypes.c_int, vp]
@@ -197,10 +197,11 @@ class Polya:
     generalised form sum_i (At_i P Bt_i + transpose) < 0 (``polya_setup_general``)."""
 
     @classmethod
-    def general(cls, terms, n, l, dp, d1, d2, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES):
-        return cls(n, l, dp, d1, d2, None, delta=delta, rank=rank, nranks=nranks, shard=shard, terms=terms)
+    def general(cls, terms, n, l, dp, d1, d2, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES, R=None):
+        """R: optional constant term, coefficients double[f(l, dp+e)][n][n] in W_{dp+e} order."""
+        return cls(n, l, dp, d1, d2, None, delta=delta, rank=rank, nranks=nranks, shard=shard, terms=terms, R=R)
 
-    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES, terms=None):
+    def __init__(self, n, l, dp, d1, d2, A, da=1, delta=1e-3, rank=0, nranks=1, shard=SHARD_TILES, terms=None, R=None):
         L = lib()
         h = ctypes.c_void_p()
         if terms is None:
@@ -216,7 +217,9 @@ class Polya:
             At = np.ascontiguousarray(np.concatenate([np.asarray(t[0], dtype=np.float64).reshape(-1) for t in terms]))
             Bt = np.ascontiguousarray(np.concatenate([np.asarray(t[2], dtype=np.float64).reshape(-1) for t in terms]))
             cp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
-            st = L.polya_setup_general(ctypes.byref(cfg), len(terms), cp(dega), cp(degb), cp(At), cp(Bt), ctypes.byref(h))
+            Rh = None if R is None else np.ascontiguousarray(np.asarray(R, dtype=np.float64))
+            st = L.polya_setup_general(ctypes.byref(cfg), len(terms), cp(dega), cp(degb), cp(At), cp(Bt),
+                                       None if Rh is None else cp(Rh), ctypes.byref(h))
             what = "polya_setup_general"
         if st != 0:
             raise PolyaError(f"{what}: {L.polya_strerror(st).decode()}")

@@ -92,13 +92,14 @@ __global__ void __launch_bounds__(128) k_bgemm(int n, const double* __restrict__
 // out = a X + b Y (+ c * C_b on the P-blocks' diagonals when cdiag != nullptr), elementwise
 __global__ void k_axpby(int64_t total, int n, int64_t Lp, double a, const double* __restrict__ X, double b,
                         const double* __restrict__ Y, double* __restrict__ out, const double* __restrict__ cdiag,
-                        double cs) {
+                        double cs, const double* __restrict__ cL) {
   const int64_t nn = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     double v = a * X[e] + (Y ? b * Y[e] : 0.0);
-    if (cdiag) {
+    if (cdiag) {   // C: c_j I on the P-blocks, the dense C_L (generalised form's R) on the Lyapunov blocks
       const int64_t blk = e / nn, r = e - blk * nn;
       if (blk < Lp && (r / n) == (r % n)) v += cs * cdiag[blk];
+      if (blk >= Lp && cL) v += cs * cL[e - Lp * nn];
     }
     out[e] = v;
   }
@@ -206,7 +207,7 @@ __global__ void k_block_tmax(int n, const double* __restrict__ S, const double* 
 // partial sums: out[0] = sum_b tr(Z_b X_b) = sum Z.*X^T, out[1] = sum_{j<L} c_j tr(X_j), out[2] = sum y
 __global__ void k_scalars(int64_t total, int n, int64_t Lp, const double* __restrict__ Z, const double* __restrict__ X,
                           const double* __restrict__ c, const double* __restrict__ y, int64_t K,
-                          double* __restrict__ part) {
+                          double* __restrict__ part, const double* __restrict__ cL) {
   __shared__ double red[3][256];
   const int64_t nn = (int64_t)n * n;
   double s0 = 0, s1 = 0, s2 = 0;
@@ -215,6 +216,7 @@ __global__ void k_scalars(int64_t total, int n, int64_t Lp, const double* __rest
     const int i = (int)(r / n), j = (int)(r % n);
     s0 += Z[e] * X[blk * nn + (int64_t)j * n + i];
     if (blk < Lp && i == j) s1 += c[blk] * X[e];
+    if (blk >= Lp && cL) s1 += cL[e - Lp * nn] * X[blk * nn + (int64_t)j * n + i];   // tr(C_L X)
   }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x) s2 += y[e];
   red[0][threadIdx.x] = s0; red[1][threadIdx.x] = s1; red[2][threadIdx.x] = s2;
@@ -317,7 +319,7 @@ __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__
 // The same check for the generalised form (reading R18): -sum_i (At_i P Bt_i + transpose)(alpha) > 0.
 // Shared memory: P(alpha), the accumulator S = sum_i At_i P Bt_i, monomials; global scratch per point:
 // At_i(alpha), Bt_i(alpha), P Bt_i(alpha).
-__global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, const int32_t* __restrict__ Wp,
+__global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, int roff, const int32_t* __restrict__ Wp,
                            const int32_t* __restrict__ cexp, const int32_t* __restrict__ aoff,
                            const int32_t* __restrict__ boff, const double* __restrict__ coef,
                            const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
@@ -348,7 +350,7 @@ __global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, const in
   }
   __syncthreads();
   for (int t = 0; t < nterms; ++t) {
-    const int a0 = aoff[t], a1 = boff[t], b0 = boff[t], b1 = t + 1 < nterms ? aoff[t + 1] : ncoef;
+    const int a0 = aoff[t], a1 = boff[t], b0 = boff[t], b1 = t + 1 < nterms ? aoff[t + 1] : roff;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
       double a = 0.0, b = 0.0;
       for (int q = a0; q < a1; ++q) a += mono[L0 + q] * coef[q * nn + e];
@@ -372,6 +374,12 @@ __global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, const in
     }
     __syncthreads();
   }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {   // the constant term R(alpha), coefficients [roff, ncoef)
+    double r = 0.0;
+    for (int q = roff; q < ncoef; ++q) r += mono[L0 + q] * coef[q * nn + e];
+    S[e] += 0.5 * r;
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
     Ae[e] = -(S[e] + S[j * n + i]);
@@ -522,7 +530,7 @@ void axpby(Ctx& c, double a, const double* X, double b, const double* Y, double*
            cudaStream_t s) {
   const int64_t total = c.nb * c.n * c.n;
   k_axpby<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(total, (int)c.n, c.L, a, X, b, Y, out,
-                                                                                 cdiag, cs);
+                                                                                 cdiag, cs, c.d_CL);
   ++c.launches;
   CK(cudaGetLastError());
 }
@@ -748,7 +756,7 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     vaxpby(c, 1.0, y, td, w->dy1, y, s);
     // step 4 scalars
     const int64_t total = c.nb * c.n * c.n;
-    k_scalars<<<kScalarBlocks, 256, 0, s>>>(total, (int)c.n, c.L, Z, X, w->dc, y, c.K, w->part);
+    k_scalars<<<kScalarBlocks, 256, 0, s>>>(total, (int)c.n, c.L, Z, X, w->dc, y, c.K, w->part, c.d_CL);
     ++c.launches;
     CK(cudaGetLastError());
     std::vector<double> part(kScalarBlocks * 3);
@@ -894,7 +902,7 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
       const int32_t* dexp = dgen;
       const int32_t* dao = dgen + c.coef_exp.size();
       CK(cudaFuncSetAttribute(k_grid_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      k_grid_gen<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, nt, (int)c.ncoef, dWp, dexp, dao,
+      k_grid_gen<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, nt, (int)c.ncoef, (int)c.r_off, dWp, dexp, dao,
                                                  dao + nt, c.d_coef, c.arena, c.mstride, (int)c.np, c.id_Vy, dpts,
                                                  dscr, dfail);
     } else {

@@ -112,7 +112,7 @@ T* dupload(const std::vector<T>& v) {
 struct GenInput {
   int32_t nterms;
   const int32_t *deg_a, *deg_b;
-  const double *At, *Bt;
+  const double *At, *Bt, *R;
 };
 
 void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi = nullptr) {
@@ -192,6 +192,15 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
       off += (int64_t)Wb_i[i].size() / l;
       c.coef_exp.insert(c.coef_exp.end(), Wa_i[i].begin(), Wa_i[i].end());
       c.coef_exp.insert(c.coef_exp.end(), Wb_i[i].begin(), Wb_i[i].end());
+    }
+    c.r_off = off;
+    c.r_cnt = 0;
+    if (gi->R) {   // the constant term: coefficients in W_{dp+da} order (verdict) and C on Lyapunov blocks
+      std::vector<int32_t> Wr;
+      enumerate(l, (int64_t)g.dp + g.da, Wr);
+      c.r_cnt = (int64_t)Wr.size() / l;
+      off += c.r_cnt;
+      c.coef_exp.insert(c.coef_exp.end(), Wr.begin(), Wr.end());
     }
     c.ncoef = off;
     // block gamma_m of element (h, k): -sum_{i, lambda, mu} multinomial(d2; gamma - h - lambda - mu)
@@ -594,13 +603,12 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     int64_t ua = 0, ub = 0;   // running offsets into the caller's At / Bt concatenations
     for (size_t i = 0; i < c.gp_da.size(); ++i) {
       const int64_t na = c.gp_boff[i] - c.gp_aoff[i];
-      const int64_t nbm = (i + 1 < c.gp_da.size() ? c.gp_aoff[i + 1] : c.ncoef) - c.gp_boff[i];
+      const int64_t nbm = (i + 1 < c.gp_da.size() ? c.gp_aoff[i + 1] : c.r_off) - c.gp_boff[i];
       coef.insert(coef.end(), gi->At + ua * nn, gi->At + (ua + na) * nn);
       coef.insert(coef.end(), gi->Bt + ub * nn, gi->Bt + (ub + nbm) * nn);
       ua += na;
       ub += nbm;
     }
-    c.d_coef = dupload(coef);
     std::vector<WsumItem> wi;
     std::vector<WsumTerm> wt;
     auto add = [&](int64_t dst, const std::vector<std::pair<int32_t, double>>& sum, int trans) {
@@ -615,6 +623,22 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     c.n_ws = (int64_t)wi.size();
     c.d_ws_items = dupload(wi);
     c.d_ws_terms = dupload(wt);
+    if (c.r_cnt) coef.insert(coef.end(), gi->R, gi->R + c.r_cnt * nn);
+    // C_{L+m} = sum_rho multinomial(d2; gamma_m - rho) R_rho (exact integer weights; host, once)
+    if (c.r_cnt) {
+      std::vector<int32_t> Wr;
+      enumerate(l, (int64_t)g.dp + g.da, Wr);
+      std::vector<double> CL((size_t)c.M * nn, 0.0);
+      for (int64_t m = 0; m < c.M; ++m)
+        for (int64_t r = 0; r < c.r_cnt; ++r) {
+          for (int64_t x = 0; x < l; ++x) tmp[x] = c.WM[m * l + x] - Wr[r * l + x];
+          const int64_t wv = multinomial(g.d2, tmp.data(), l);
+          if (!wv) continue;
+          for (int64_t e = 0; e < nn; ++e) CL[m * nn + e] += (double)wv * gi->R[r * nn + e];
+        }
+      c.d_CL = dupload(CL);
+    }
+    c.d_coef = dupload(coef);
     CU(launch_wsum(c, 0));
     CU(cudaDeviceSynchronize());
     return;
@@ -632,7 +656,7 @@ void free_ctx(Ctx& c) {
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
                 c.st.pair_kbeg, c.st.pair_item, c.st.kdesc,
                 c.st.cls_a, c.st.cls_b, c.st.counter, c.d_coef, c.d_ws_items, c.d_ws_terms, c.d_items_T0,
-                c.d_terms_T0, c.d_items_S0, c.d_terms_S0};
+                c.d_terms_T0, c.d_items_S0, c.d_terms_S0, c.d_CL};
   for (void* p : ps)
     if (p) cudaFree(p);
 }
@@ -676,7 +700,8 @@ extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_hos
 }
 
 extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nterms, const int32_t* deg_a,
-                                           const int32_t* deg_b, const double* At, const double* Bt, polya_ctx** out) {
+                                           const int32_t* deg_b, const double* At, const double* Bt, const double* R,
+                                           polya_ctx** out) {
   if (!out) return POLYA_EINVAL;
   *out = nullptr;
   if (!cfg || nterms < 1 || !deg_a || !deg_b || !At || !Bt) return POLYA_EINVAL;
@@ -689,7 +714,7 @@ extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nte
   polya_ctx* ctx = new (std::nothrow) polya_ctx();
   if (!ctx) return POLYA_ENOMEM;
   ctx->c.cfg = g;
-  const GenInput gi{nterms, deg_a, deg_b, At, Bt};
+  const GenInput gi{nterms, deg_a, deg_b, At, Bt, R};
   try {
     if (cudaGetDevice(&ctx->c.device) != cudaSuccess) throw Fail{POLYA_ECUDA, "no CUDA device"};
     build(ctx->c, nullptr, true, &gi);

@@ -65,7 +65,9 @@ struct Ctx {
   int64_t ncoef = 0;                   // coefficient matrices of all At_i, Bt_i (n x n each)
   std::vector<int32_t> gp_da, gp_db, gp_aoff, gp_boff;  // per input term i: degrees, coefficient offsets
   std::vector<int32_t> coef_exp;       // [ncoef][l] exponent of each coefficient matrix
-  double* d_coef = nullptr;            // [ncoef][n][n]
+  double* d_coef = nullptr;            // [ncoef][n][n] (the constant term R's coefficients last)
+  int64_t r_off = 0, r_cnt = 0;        // R's coefficients in d_coef (r_cnt = 0: no constant term)
+  double* d_CL = nullptr;              // [M][n][n] C on the Lyapunov blocks (from R), or null
   WsumItem* d_ws_items = nullptr; WsumTerm* d_ws_terms = nullptr; int64_t n_ws = 0;
   std::vector<double> Hw;              // [nnzH][nA] integer weights multinomial(d2; gamma-h-lambda)
   // pairs and work items

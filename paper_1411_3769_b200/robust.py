@@ -25,14 +25,14 @@ def simplex_points(l, samples=1000, seed=0):
     return np.array(pts)
 
 
-def certify(A, n, l, dp, d1, d2, da=1, delta=1e-3, eps=1e-8, tol=1e-8, maxit=60, samples=1000, seed=0, terms=None):
+def certify(A, n, l, dp, d1, d2, da=1, delta=1e-3, eps=1e-8, tol=1e-8, maxit=60, samples=1000, seed=0, terms=None, R=None):
     """Is x' = A(alpha) x certified robustly stable on Delta_l by the Polya LMIs of degree
     (dp, d1, d2)?  A: coefficients double[f(l,da)][n][n] of the homogeneous A(alpha) in W_da order.
     Certified = Algorithm 2 met its stopping rule with Z positive definite (polya_ipm_solve) and the
     reconstructed P(alpha) passes the grid check at every sample point (polya_verdict).
     With ``terms`` (A ignored) the LMI is the generalised form sum_i (At_i P Bt_i + transpose) < 0
     (polya_setup_general), e.g. discrete-time stability A^T P A - P < 0."""
-    ctx = Polya(n, l, dp, d1, d2, A, da=da, delta=delta, terms=terms)
+    ctx = Polya(n, l, dp, d1, d2, A, da=da, delta=delta, terms=terms, R=R)
     try:
         r = ctx.ipm_solve(eps=eps, tol=tol, maxit=maxit)
         nfail = -1

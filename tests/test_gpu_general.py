@@ -140,3 +140,46 @@ def test_verdict_kernel_matches_oracle_grid_check(pb):
     bad[:P.Ntil] *= -1.0
     assert ctx.verdict(_dev(bad), pts) > 0 and not oipm.grid_check(P, bad, 200, 0)
     ctx.close()
+
+
+@pytest.mark.parametrize("avals,r", [([-1.0], 3.0), ([-1.0, -0.5], 3.0), ([-2.0, -1.0, -4.0], 1.0)])
+def test_constant_term_scalar_closed_form(pb, avals, r):
+    """R on the device (C on the Lyapunov blocks): polya_ipm_solve reaches the closed-form optimum
+    p* = max_i r / (2 |a_i|) of tests/test_oracle_general.py."""
+    l = len(avals)
+    A = np.array(avals).reshape(l, 1, 1)
+    ctx = pb.Polya.general([(A, 1, np.ones((1, 1, 1)), 0)], 1, l, 0, 0, 0, R=np.full((l, 1, 1), r))
+    res = ctx.ipm_solve()
+    assert res["converged"]
+    assert abs(res["y"].cpu().numpy()[0] - max(r / (2 * abs(a)) for a in avals)) <= 1e-6
+    ctx.close()
+
+
+def test_constant_term_ipm_step_parity_and_verdict(pb):
+    from paper_1411_3769_b200 import robust
+    n, l, dp, d1, d2 = 4, 2, 1, 1, 1
+    rng = np.random.default_rng(11)
+    A = synth.discrete_vertex_matrices(n, l, 0.6, rng)
+    terms = synth.discrete_time_terms(A)
+    Wr = enumerate_W(l, dp + 2)
+    Q = rng.normal(size=(n, n))
+    R = np.array([0.1 * (Q @ Q.T) * (1.0 if sum(w) == w[0] or sum(w) == w[-1] else 2.0) for w in Wr])
+    P = osdp.build_problem_general(terms, n, l, dp, d1, d2, R=R)
+    ctx = pb.Polya.general(terms, n, l, dp, d1, d2, R=R)
+    X, Z, y, mu = oipm.initial_state(P)
+    Xd, Zd, yd = (torch.from_numpy(v.copy()).cuda() for v in (X, Z, y))
+    mud = mu
+    for it in range(3):
+        X, Z, y, st = oipm.ipm_step(P, X, Z, y, mu)
+        mu = st["mu"]
+        s = ctx.ipm_step(Xd, Zd, yd, mud, it)
+        mud = s["mu"]
+        assert _rel(Xd.cpu().numpy(), X) <= 1e-8, it
+        assert _rel(Zd.cpu().numpy(), Z) <= 1e-8, it
+        assert _rel(yd.cpu().numpy(), y) <= 1e-8, it
+        for k in ("tp", "td", "mu", "phi", "psi"):
+            assert abs(s[k] - st[k]) <= 1e-8 * max(1.0, abs(st[k])), (it, k)
+    ctx.close()
+    ok = oipm.verdict(P, samples=100)
+    r = robust.certify(None, n, l, dp, d1, d2, terms=terms, R=R, samples=100)
+    assert r["certified"] == ok

@@ -96,3 +96,41 @@ def test_discrete_time_verdicts(unstable):
     assert ipm.verdict(P, samples=200) == (not unstable)
     if unstable:   # the vertex itself violates A^T P A - P < 0 for every P > 0
         assert max(abs(np.linalg.eigvals(A[0]))) > 1.0
+
+
+def _scalar_vertex_problem(avals, r, d2=0):
+    """n = 1, dp = 0: A(alpha) = sum a_i alpha_i, R(alpha) = r sum alpha_i; min y = p s.t. p >= delta c
+    and -(2 a_i p + r) >= 0 at every vertex, so p* = max(delta, max_i r / (2 |a_i|))."""
+    l = len(avals)
+    A = np.array(avals, dtype=float).reshape(l, 1, 1)
+    R = np.full((l, 1, 1), float(r))
+    return sdp.build_problem_general([(A, 1, np.ones((1, 1, 1)), 0)], 1, l, 0, 0, d2, R=R)
+
+
+@pytest.mark.parametrize("avals,r", [([-1.0], 3.0), ([-1.0, -0.5], 3.0), ([-2.0, -1.0, -4.0], 1.0)])
+def test_constant_term_scalar_closed_form(avals, r):
+    """R enters as C on the Lyapunov blocks with the sign of the paper's LMI (sum ... + R < 0): the
+    IPM's optimum is the closed form p* = max_i r / (2 |a_i|) (a sign error gives p* = delta c)."""
+    P = _scalar_vertex_problem(avals, r)
+    ok, X, Z, y, it = ipm.solve(P)
+    assert ok
+    assert abs(y[0] - max(r / (2 * abs(a)) for a in avals)) <= 1e-6
+
+
+def test_constant_term_polynomial_identity():
+    n, l, dp, d1, d2 = 3, 2, 1, 1, 2
+    rng = np.random.default_rng(4)
+    terms = synth.random_terms(n, l, [(1, 1)], rng, _f(l))
+    Wr = enumerate_W(l, dp + 2)
+    R = rng.normal(size=(len(Wr), n, n))
+    R = R + R.transpose(0, 2, 1)
+    P = sdp.build_problem_general(terms, n, l, dp, d1, d2, R=R)
+    C = ipm.C_blocks(P)
+    Wm = enumerate_W(l, dp + 2 + d2)
+    for _ in range(3):
+        al = rng.uniform(0.2, 1.5, size=l)
+        lhs = sum(math.prod(a ** k for a, k in zip(al, g)) * C[P.L + m] for m, g in enumerate(Wm))
+        rhs = sum(al) ** d2 * polya.evaluate(R, l, dp + 2, al)
+        assert np.abs(lhs - rhs).max() <= 1e-12 * np.abs(rhs).max()
+    # and the P-blocks keep c_j I
+    assert np.array_equal(C[0], P.c[0] * np.eye(n))
