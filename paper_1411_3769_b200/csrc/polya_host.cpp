@@ -195,6 +195,27 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     }
     c.r_off = off;
     c.r_cnt = 0;
+    // canonical coefficient ids: bitwise-equal coefficient matrices (an identity repeated per vertex,
+    // say) share the smallest id, so that the merges below see them as one matrix
+    std::vector<int32_t> canon(off);
+    {
+      const int64_t nn = (int64_t)g.n * g.n;
+      std::vector<const double*> cptr(off);
+      int64_t ua = 0, ub = 0;
+      for (int32_t i = 0; i < gi->nterms; ++i) {
+        for (int64_t q = c.gp_aoff[i]; q < c.gp_boff[i]; ++q) cptr[q] = gi->At + (ua++) * nn;
+        const int64_t bend = i + 1 < gi->nterms ? c.gp_aoff[i + 1] : off;
+        for (int64_t q = c.gp_boff[i]; q < bend; ++q) cptr[q] = gi->Bt + (ub++) * nn;
+      }
+      for (int64_t q = 0; q < off; ++q) {
+        canon[q] = (int32_t)q;
+        for (int64_t r = 0; r < q; ++r)
+          if (canon[r] == r && std::memcmp(cptr[q], cptr[r], (size_t)nn * sizeof(double)) == 0) {
+            canon[q] = (int32_t)r;
+            break;
+          }
+      }
+    }
     if (gi->R) {   // the constant term: coefficients in W_{dp+da} order (verdict) and C on Lyapunov blocks
       std::vector<int32_t> Wr;
       enumerate(l, (int64_t)g.dp + g.da, Wr);
@@ -206,10 +227,67 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     // block gamma_m of element (h, k): -sum_{i, lambda, mu} multinomial(d2; gamma - h - lambda - mu)
     //   (At_{i,lambda} E_k Bt_{i,mu} + transpose); the sum over the larger of W_{a_i}, W_{b_i} is folded
     //   into one weighted coefficient sum, so (h, m) gets min(f(l,a_i), f(l,b_i)) terms per i at most
+    // Exact term merges per (h, gamma) (the weights are integers): a side that is one coefficient
+    // matrix times a weight takes the weight over to the other side; terms whose B side is the same
+    // single matrix then merge by adding their A sides (A E B + A' E B = (A + A') E B), and likewise
+    // for a shared single A side.  Discrete time's (-1/2 sum alpha I, sum alpha I) becomes one term.
+    std::vector<std::vector<std::pair<int32_t, double>>> rawA, rawB;
+    auto canon_sum = [&](std::vector<std::pair<int32_t, double>>& v) {
+      std::map<int32_t, double> acc;
+      for (auto& e : v) acc[canon[e.first]] += e.second;
+      v.clear();
+      for (auto& e : acc)
+        if (e.second != 0.0) v.push_back(e);
+    };
+    auto merge_side = [&](bool onB) {   // merge terms whose (onB ? B : A) side is one identical matrix
+      std::vector<std::vector<std::pair<int32_t, double>>> nA, nB;
+      std::map<int32_t, size_t> at;
+      for (size_t q = 0; q < rawA.size(); ++q) {
+        auto& key = onB ? rawB[q] : rawA[q];
+        auto& other = onB ? rawA[q] : rawB[q];
+        if (key.size() == 1) {
+          const double wk = key[0].second;
+          for (auto& e : other) e.second *= wk;
+          key[0].second = 1.0;
+          auto f = at.find(key[0].first);
+          if (f != at.end()) {
+            auto& o = onB ? nA[f->second] : nB[f->second];
+            o.insert(o.end(), other.begin(), other.end());
+            canon_sum(o);
+            continue;
+          }
+          at[key[0].first] = nA.size();
+        }
+        nA.push_back(rawA[q]);
+        nB.push_back(rawB[q]);
+      }
+      rawA.swap(nA);
+      rawB.swap(nB);
+    };
+    auto merge_terms = [&]() {
+      for (size_t q = 0; q < rawA.size(); ++q) {
+        canon_sum(rawA[q]);
+        canon_sum(rawB[q]);
+      }
+      for (size_t q = rawA.size(); q-- > 0;)   // drop terms that cancelled
+        if (rawA[q].empty() || rawB[q].empty()) {
+          rawA.erase(rawA.begin() + q);
+          rawB.erase(rawB.begin() + q);
+        }
+      merge_side(true);
+      merge_side(false);
+      for (size_t q = rawA.size(); q-- > 0;)
+        if (rawA[q].empty() || rawB[q].empty()) {
+          rawA.erase(rawA.begin() + q);
+          rawB.erase(rawB.begin() + q);
+        }
+    };
     for (int64_t m = 0; m < c.M; ++m) {
       const int32_t* gm = &c.WM[m * l];
       for (int64_t h = 0; h < c.L0; ++h) {
         const int32_t first = (int32_t)c.Hh.size();
+        rawA.clear();
+        rawB.clear();
         for (int32_t i = 0; i < gi->nterms; ++i) {
           const int64_t na = (int64_t)Wa_i[i].size() / l, nbm = (int64_t)Wb_i[i].size() / l;
           const bool byA = na <= nbm;   // one term per lambda (B summed) or per mu (A summed)
@@ -224,11 +302,16 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
             }
             if (sum.empty()) continue;
             std::vector<std::pair<int32_t, double>> one{{(int32_t)(byA ? c.gp_aoff[i] + u : c.gp_boff[i] + u), 1.0}};
-            tA.push_back(byA ? one : sum);
-            tB.push_back(byA ? sum : one);
-            c.Hh.push_back((int32_t)h);
-            c.Hm.push_back((int32_t)m);
+            rawA.push_back(byA ? one : sum);
+            rawB.push_back(byA ? sum : one);
           }
+        }
+        merge_terms();
+        for (size_t q = 0; q < rawA.size(); ++q) {
+          tA.push_back(rawA[q]);
+          tB.push_back(rawB[q]);
+          c.Hh.push_back((int32_t)h);
+          c.Hm.push_back((int32_t)m);
         }
         const int32_t cnt = (int32_t)c.Hh.size() - first;
         if (cnt) {

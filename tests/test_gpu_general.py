@@ -86,6 +86,7 @@ def test_continuous_time_case_equals_standard_context(pb):
     y = rng.normal(size=std.K)
     assert _rel(gen.apply(_dev(y)).cpu().numpy(), std.apply(_dev(y)).cpu().numpy()) <= 1e-14
     assert std.dims["useful_flops_schur"] == gen.dims["useful_flops_schur"]
+    assert std.dims["nnz_H"] == gen.dims["nnz_H"]       # one term per (h, gamma): (H^T, I)
     with pytest.raises(pb.PolyaError):
         gen.H()
     std.close()
@@ -183,3 +184,35 @@ def test_constant_term_ipm_step_parity_and_verdict(pb):
     ok = oipm.verdict(P, samples=100)
     r = robust.certify(None, n, l, dp, d1, d2, terms=terms, R=R, samples=100)
     assert r["certified"] == ok
+
+
+def test_discrete_time_terms_merge_to_l_plus_one(pb):
+    """The exact merges of polya_setup_general: the identity term (-1/2 sum alpha I, sum alpha I)
+    collapses to one term per (h, gamma), so (h, gamma) holds at most l + 1 terms instead of 2 l,
+    and the operators still match the (unmerged) oracle."""
+    import math
+    n, l, dp, d1, d2 = 5, 3, 1, 1, 2
+    A = synth.discrete_vertex_matrices(n, l, 0.8, np.random.default_rng(2))
+    terms = synth.discrete_time_terms(A)
+    ctx = pb.Polya.general(terms, n, l, dp, d1, d2)
+    Wp, Wm, W1 = enumerate_W(l, dp), enumerate_W(l, dp + 2 + d2), enumerate_W(l, 1)
+
+    def mnom(d, parts):
+        if any(p < 0 for p in parts) or sum(parts) != d:
+            return 0
+        return math.factorial(d) // math.prod(math.factorial(p) for p in parts)
+
+    want = 0
+    for h in Wp:
+        for g in Wm:
+            w = [[mnom(d2, [gi - hi - li - mi for gi, hi, li, mi in zip(g, h, lam, mu)]) for mu in W1] for lam in W1]
+            want += sum(1 for row in w if any(row))     # term 0: one per lambda with a non-zero weight
+            want += 1 if sum(map(sum, w)) else 0        # term 1: a single merged term
+    assert ctx.dims["nnz_H"] == want
+    P = osdp.build_problem_general(terms, n, l, dp, d1, d2)
+    rng = np.random.default_rng(3)
+    X, W = synth.spd_blocks(n, P.nblocks, rng)
+    y = rng.normal(size=P.K)
+    assert _rel(ctx.apply(_dev(y)).cpu().numpy(), osdp.apply_vmap(P, y)) <= TOL
+    assert _rel(ctx.schur(_dev(X), _dev(W)).cpu().numpy(), osdp.schur_structured(P, X, W)) <= TOL
+    ctx.close()
