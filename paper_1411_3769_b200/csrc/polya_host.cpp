@@ -646,8 +646,16 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
       c.st.kdesc = dupload(kd);
     }
     std::vector<int32_t> ca, cb;
-    for (int64_t i = 0; i < c.r; ++i)
-      for (int64_t j = i; j < c.r; ++j) { ca.push_back((int32_t)i); cb.push_back((int32_t)j); }
+#ifndef POLYA_CLS_ORDER
+#define POLYA_CLS_ORDER 0
+#endif
+    if (POLYA_CLS_ORDER == 1) {   // experiment: classes along class diagonals (i, i+d)
+      for (int64_t d = 0; d < c.r; ++d)
+        for (int64_t i = 0; i + d < c.r; ++i) { ca.push_back((int32_t)i); cb.push_back((int32_t)(i + d)); }
+    } else {
+      for (int64_t i = 0; i < c.r; ++i)
+        for (int64_t j = i; j < c.r; ++j) { ca.push_back((int32_t)i); cb.push_back((int32_t)j); }
+    }
     c.st.cls_a = dupload(ca);
     c.st.cls_b = dupload(cb);
     c.st.counter = dalloc<unsigned long long>(1);
