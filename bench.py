@@ -249,7 +249,7 @@ def run_gpu(args, cfg, cid):
             dist.broadcast_object_list(uid, src=0)
         ctx.nccl_init(uid[0])
     K, N = ctx.K, ctx.Ntil
-    npl = ctx.dims["pair1"] - ctx.dims["pair0"]
+    npl = ctx.dims["npairs_local"]
     wg_rank = ctx.dims["useful_flops_schur"]
     wg_total = sum_over_ranks(wg_rank)
 

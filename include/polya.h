@@ -65,8 +65,13 @@ typedef enum {
  *  POLYA_SHARD_BLOCKS  the paper's decentralised scheme: rank r owns a
  *                      cost-balanced contiguous range [b0, b1) of the Polya blocks and computes
  *                      the partial G^(r) = sum_{b in [b0,b1)} G^(b) over ALL entries; the partials
- *                      are summed by polya_reduce_G (NCCL ReduceScatter / AllReduce).       */
-typedef enum { POLYA_SHARD_TILES = 0, POLYA_SHARD_BLOCKS = 1 } polya_shard;
+ *                      are summed by polya_reduce_G (NCCL ReduceScatter / AllReduce).
+ *  POLYA_SHARD_CYCLIC  the distributed factorisation's layout:
+ *                      rank r assembles the pair tiles (h, h') with h = r mod nranks -- the block
+ *                      columns r, r + nranks, ... of the lower Cholesky factor -- completely, in
+ *                      the PAIR_TILES layout in pair order; polya_ipm_step / polya_ipm_solve then
+ *                      factor G across the ranks (NCCL broadcasts of each factored panel).  */
+typedef enum { POLYA_SHARD_TILES = 0, POLYA_SHARD_BLOCKS = 1, POLYA_SHARD_CYCLIC = 2 } polya_shard;
 
 /* Problem shape.  delta > 0 is the P-positivity margin of Eq. Cj ("a small
  * positive parameter"; R9 default 1e-3).  rank / nranks select
@@ -98,6 +103,8 @@ typedef struct {
   int64_t reduce_count; /* SHARD_BLOCKS: doubles each rank receives from polya_reduce_G in
                            the PAIR_TILES layout = ceil(npairs*Ntil^2 / nranks); the partial-G
                            buffer holds nranks*reduce_count doubles (zero padding at the end) */
+  int64_t npairs_local; /* pair tiles held by this rank (PAIR_TILES layout: npairs_local tiles);
+                           = pair1 - pair0 except with SHARD_CYCLIC (pairs not contiguous) */
 } polya_dims;
 
 /* Output layouts of the Schur complement G (symmetric K x K):
@@ -289,6 +296,16 @@ polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, const polya_so
  * One CTA per point on the device; n <= 118.  Synchronous.                                     */
 polya_status polya_verdict(polya_ctx* ctx, const double* y_dev, int32_t npts, const double* pts_host,
                            int32_t* nfail_out, void* stream);
+
+/* Test hook of the distributed factorisation (SHARD_CYCLIC): ctxs[r] (r < nranks) are
+ * the nranks contexts of one problem, all in this process on one device, ctxs[r] with rank r and
+ * shard POLYA_SHARD_CYCLIC; G_local[r] is rank r's POLYA_G_PAIR_TILES output of polya_schur,
+ * overwritten by its tiles of the Cholesky factor.  x (double[K], device) is overwritten by
+ * G^{-1} x.  Runs the same per-step functions as the NCCL path of polya_ipm_step, the ranks one
+ * after another, with device copies in place of the broadcasts.  Synchronous.
+ * Errors: EINVAL (inconsistent contexts), ENOTPD (G not positive definite), ECUDA. */
+polya_status polya_factor_solve_loopback(polya_ctx** ctxs, int32_t nranks, double* const* G_local, double* x_dev,
+                                         void* stream);
 
 /* Surfaces asynchronous errors (device synchronise + last-error check). */
 polya_status polya_sync(polya_ctx* ctx);

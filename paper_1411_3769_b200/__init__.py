@@ -11,19 +11,19 @@ import os
 
 import numpy as np
 
-__all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "SHARD_TILES", "SHARD_BLOCKS", "EXPORTS",
-           "LIB_PATH", "plan", "nccl_unique_id", "homogenize", "simplex_map"]
+__all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "SHARD_TILES", "SHARD_BLOCKS", "SHARD_CYCLIC",
+           "EXPORTS", "LIB_PATH", "plan", "nccl_unique_id", "homogenize", "simplex_map", "factor_solve_loopback"]
 
 # POLYA_LIB overrides the library path (timing-experiment variants built by tools/schur_exp.py)
 LIB_PATH = os.environ.get("POLYA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
 G_FULL, G_PAIR_TILES = 0, 1
-SHARD_TILES, SHARD_BLOCKS = 0, 1
+SHARD_TILES, SHARD_BLOCKS, SHARD_CYCLIC = 0, 1, 2
 EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents", "polya_get_beta", "polya_get_H",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
            "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
            "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization", "polya_schur_prepare",
-           "polya_schur_assemble", "polya_setup_general"]
+           "polya_schur_assemble", "polya_setup_general", "polya_factor_solve_loopback"]
 
 
 class PolyaError(RuntimeError):
@@ -40,7 +40,7 @@ class _Dims(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("L0", "L", "M", "nblocks", "Ntil", "K", "nnz_beta", "nnz_H",
                                               "npairs", "pair0", "pair1", "item0", "item1")] + \
                [("useful_flops_schur", ctypes.c_double), ("tiles_bytes", ctypes.c_int64), ("b0", ctypes.c_int64),
-                ("b1", ctypes.c_int64), ("reduce_count", ctypes.c_int64)]
+                ("b1", ctypes.c_int64), ("reduce_count", ctypes.c_int64), ("npairs_local", ctypes.c_int64)]
 
 
 class _IpmState(ctypes.Structure):
@@ -79,6 +79,7 @@ def lib():
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
     L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
+    L.polya_factor_solve_loopback.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), vp, vp]
     L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
     L.polya_plan.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Dims)]
     L.polya_get_exponents.argtypes = [vp, ctypes.c_int, vp]
@@ -136,6 +137,20 @@ def nccl_unique_id():
     if st != 0:
         raise PolyaError(f"polya_nccl_unique_id: {lib().polya_strerror(st).decode()}")
     return bytes(buf.raw)
+
+
+def factor_solve_loopback(ctxs, G_local, x, stream=None):
+    """polya_factor_solve_loopback: the SHARD_CYCLIC distributed Cholesky + solve with all ranks'
+    contexts in this process (test hook; device copies in place of the NCCL broadcasts).
+    G_local[r]: rank r's pair tiles (overwritten by its factor tiles); x (K doubles) <- G^{-1} x."""
+    n = len(ctxs)
+    hs = (ctypes.c_void_p * n)(*[c._h.value for c in ctxs])
+    gs = (ctypes.c_void_p * n)(*[_dev_ptr(g, None, "G_local").value for g in G_local])
+    st = lib().polya_factor_solve_loopback(hs, n, gs, _dev_ptr(x, ctxs[0].K, "x"), _stream_ptr(stream))
+    if st != 0:
+        raise PolyaError(f"polya_factor_solve_loopback: {lib().polya_strerror(st).decode()} "
+                         f"({lib().polya_last_error(ctxs[0]._h).decode()})")
+    return x
 
 
 def homogenize(terms, l):
@@ -289,7 +304,7 @@ class Polya:
             elif self.shard == SHARD_BLOCKS:   # flat partial-G buffer: all pair tiles + zero padding
                 G = torch.zeros(self.nranks * self.dims["reduce_count"], dtype=torch.float64, device=X.device)
             else:
-                npl = self.dims["pair1"] - self.dims["pair0"]
+                npl = self.dims["npairs_local"]
                 G = torch.zeros((npl, self.Ntil, self.Ntil), dtype=torch.float64, device=X.device)
         nbn = self.nblocks * self.n ** 2
         self._check(lib().polya_schur(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"), _dev_ptr(G, None, "G"),
@@ -315,7 +330,8 @@ class Polya:
         return {k: getattr(stats, k) for k, _ in _IpmStats._fields_}
 
     def nccl_init(self, uid):
-        """polya_nccl_init: collective over the nranks contexts (SHARD_BLOCKS combine)."""
+        """polya_nccl_init: collective over the nranks contexts (SHARD_BLOCKS combine, SHARD_CYCLIC
+        distributed factorisation)."""
         buf = ctypes.create_string_buffer(bytes(uid), 128)
         self._check(lib().polya_nccl_init(self._h, buf), "polya_nccl_init")
 

@@ -74,6 +74,44 @@ extern "C" polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart, doub
 }
 
 namespace polya {
+// Collectives of the distributed factorisation (SHARD_CYCLIC).  With one rank they are no-ops (the
+// root's buffer is every rank's buffer); with more they need polya_nccl_init.
+cudaError_t comm_bcast(Ctx& c, void* buf, size_t count, bool is_int, int root, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (!c.nccl) return c.cfg.nranks == 1 ? cudaSuccess : cudaErrorNotReady;   // one rank: nothing to send
+  ncclResult_t r = ncclBroadcast(buf, buf, count, is_int ? ncclInt32 : ncclFloat64, root, (ncclComm_t)c.nccl, s);
+  if (r != ncclSuccess) {
+    c.last_error = std::string("ncclBroadcast: ") + ncclGetErrorString(r);
+    return cudaErrorUnknown;
+  }
+  return cudaSuccess;
+}
+// tile q of buf (count doubles each, q < ntiles) broadcast from rank q mod nranks, as one NCCL group
+cudaError_t comm_bcast_tiles(Ctx& c, double* buf, size_t count, int64_t ntiles, cudaStream_t s) {
+  if (count == 0 || ntiles == 0) return cudaSuccess;
+  if (!c.nccl) return c.cfg.nranks == 1 ? cudaSuccess : cudaErrorNotReady;
+  ncclResult_t r = ncclGroupStart();
+  for (int64_t q = 0; q < ntiles && r == ncclSuccess; ++q)
+    r = ncclBroadcast(buf + q * count, buf + q * count, count, ncclFloat64, (int)(q % c.cfg.nranks), (ncclComm_t)c.nccl, s);
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) {
+    c.last_error = std::string("ncclBroadcast (tiles): ") + ncclGetErrorString(r);
+    return cudaErrorUnknown;
+  }
+  return cudaSuccess;
+}
+cudaError_t comm_allreduce_sum(Ctx& c, double* buf, size_t count, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (!c.nccl) return c.cfg.nranks == 1 ? cudaSuccess : cudaErrorNotReady;
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c.nccl, s);
+  if (r != ncclSuccess) {
+    c.last_error = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
+    return cudaErrorUnknown;
+  }
+  return cudaSuccess;
+}
+
 void nccl_free(Ctx& c) {
   if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
   c.nccl = nullptr;

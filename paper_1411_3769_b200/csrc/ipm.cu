@@ -429,6 +429,9 @@ struct Ipm {
   int* fail = nullptr;
   int lwork = 0;
   bool tiled = false;          // G held as pair tiles (lower block triangle in column-major view)
+  bool dist = false;           // SHARD_CYCLIC: this rank's pair tiles only, factorised across the ranks
+  double* panel = nullptr;     // dist, nranks > 1: the broadcast panel of step k ((L0-1) tiles)
+  double* lkk = nullptr;       // dist, nranks > 1: the broadcast diagonal factor L_kk (one tile)
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
   cudaEvent_t ev[6] = {};
@@ -445,7 +448,7 @@ void polya_ipm_free(polya::Ctx& c) {
   Ipm* w = (Ipm*)c.ipm;
   if (!w) return;
   double* ps[] = {w->W, w->Rd, w->T1, w->T2, w->dX1, w->dZ1, w->dX2, w->dZ2, w->G, w->O1, w->O2,
-                  w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work};
+                  w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work, w->panel, w->lkk};
   for (double* p : ps)
     if (p) cudaFree(p);
   if (w->info) cudaFree(w->info);
@@ -482,6 +485,7 @@ struct IpmFail {
   } while (0)
 
 bool want_tiled(const Ctx& c) {
+  if (c.cfg.shard == POLYA_SHARD_CYCLIC) return true;   // the distributed factorisation works on tiles
   if (c.fact_mode == 1) return false;
   if (c.fact_mode == 2) return true;
   size_t fr = 0, tot = 0;
@@ -501,7 +505,13 @@ Ipm* ipm_ws(Ctx& c) {
   for (double** p : stacks) CK(cudaMalloc(p, st));
   double** vecs[] = {&w->O1, &w->O2, &w->dy1, &w->dy2, &w->tmpK};
   for (double** p : vecs) CK(cudaMalloc(p, kv));
-  CK(cudaMalloc(&w->G, (w->tiled ? (size_t)c.npairs * c.Ntil * c.Ntil : (size_t)c.K * c.K) * sizeof(double)));
+  w->dist = c.cfg.shard == POLYA_SHARD_CYCLIC;
+  CK(cudaMalloc(&w->G, (w->tiled ? (size_t)std::max<int64_t>(c.npairs_local, 1) * c.Ntil * c.Ntil : (size_t)c.K * c.K) *
+                           sizeof(double)));
+  if (w->dist && c.cfg.nranks > 1 && c.L0 > 1) {
+    CK(cudaMalloc(&w->panel, (size_t)(c.L0 - 1) * c.Ntil * c.Ntil * sizeof(double)));
+    CK(cudaMalloc(&w->lkk, (size_t)c.Ntil * c.Ntil * sizeof(double)));
+  }
   CK(cudaMalloc(&w->tb, (size_t)c.nb * sizeof(double)));
   CK(cudaMalloc(&w->part, (size_t)kScalarBlocks * 3 * sizeof(double)));
   CK(cudaMalloc(&w->dc, (size_t)std::max<int64_t>(c.L, 1) * sizeof(double)));
@@ -565,10 +575,13 @@ double step_len(Ctx& c, Ipm* w, const double* S, const double* dS, cudaStream_t 
 // ---- blocked Cholesky on the pair tiles --------------------------------------------------------
 // Tile of pair (h <= h') holds G[h-block][h'-block] row-major = the block B_{h'h} of the LOWER block
 // triangle in column-major view (N = Ntil).  G = L L^T, right-looking, L overwriting B.
-inline double* tile(const Ctx& c, Ipm* w, int64_t h, int64_t h2) {
+// The tiles are this rank's pairs in pair order (all pairs on one rank; SHARD_CYCLIC: pair rows
+// h = rank mod nranks), so the local index comes from the set-up's pair_local table.
+inline double* tile(const Ctx& c, double* G, int64_t h, int64_t h2) {
   const int64_t p = h * c.L0 - h * (h - 1) / 2 + (h2 - h);
-  return w->G + p * c.Ntil * c.Ntil;
+  return G + (int64_t)c.pair_local[p] * c.Ntil * c.Ntil;
 }
+inline double* tile(const Ctx& c, Ipm* w, int64_t h, int64_t h2) { return tile(c, w->G, h, h2); }
 
 void tiled_potrf(Ctx& c, Ipm* w, cudaStream_t s) {
   const int N = (int)c.Ntil;
@@ -620,8 +633,162 @@ void tiled_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
   c.launches += 2 * T * (T + 1) / 2 + 2 * T;
 }
 
+// ---- distributed blocked Cholesky (SHARD_CYCLIC) -------------
+// Block column k of the lower factor is pair row k (tiles (k, i), i >= k), held by rank k mod N
+// (column-cyclic: the trailing-update work sum_{j = r mod N} j (L0 - j) is balanced to a few %).
+// Step k: the owner factors L_kk and broadcasts it with the raw panel B_ik (i > k, contiguous in
+// its pair order); the ranks split the panel solves B_ik <- B_ik L_kk^{-T} (tile q = i-k-1 on rank
+// q mod N: one rank doing all of them would put ~3.6 s of serial trsm on config 5's critical path)
+// and broadcast the solved tiles back; every rank then updates its own block columns j > k,
+// B_ij -= B_ik B_jk^T (k < j <= i).  Each tile sees the same cuBLAS / cuSOLVER calls in the same
+// order as in tiled_potrf, so the factor is the single-GPU one bit for bit.
+inline int owner(const Ctx& c, int64_t k) { return (int)(k % c.cfg.nranks); }
+
+int dist_potrf_kk(Ctx& c, Ipm* w, double* G, int64_t k, cudaStream_t s) {   // owner of column k only
+  const int N = (int)c.Ntil;
+  CS(cusolverDnSetStream(w->sol, s));
+  CS(cusolverDnDpotrf(w->sol, CUBLAS_FILL_MODE_LOWER, N, tile(c, G, k, k), N, w->work, w->lwork, w->info));
+  ++c.launches;
+  int hinfo = 0;
+  CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return hinfo;
+}
+
+// This rank's share of the panel solve B_ik <- B_ik L_kk^{-T}: panel tiles q = i - k - 1 with
+// q = rank mod nranks (all of them on one rank), in the rank's copy of the panel.
+void dist_trsm_share(Ctx& c, Ipm* w, int64_t k, const double* Lkk, double* panel, cudaStream_t s) {
+  const int N = (int)c.Ntil;
+  const int64_t NN = (int64_t)N * N;
+  const double one = 1.0;
+  CB(cublasSetStream(w->blas, s));
+  for (int64_t q = c.cfg.rank; q < c.L0 - k - 1; q += c.cfg.nranks) {
+    CB(cublasDtrsm(w->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, N, N, &one,
+                   Lkk, N, panel + q * NN, N));
+    ++c.launches;
+  }
+}
+
+// panel + (i - k - 1) N^2 = B_ik for i > k
+void dist_update(Ctx& c, Ipm* w, double* G, int64_t k, const double* panel, cudaStream_t s) {
+  const int N = (int)c.Ntil;
+  const int64_t NN = (int64_t)N * N;
+  const double one = 1.0, mone = -1.0;
+  CB(cublasSetStream(w->blas, s));
+  for (int64_t j = k + 1; j < c.L0; ++j) {
+    if (owner(c, j) != c.cfg.rank) continue;
+    const double* Bjk = panel + (j - k - 1) * NN;
+    CB(cublasDsyrk(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, N, N, &mone, Bjk, N, &one, tile(c, G, j, j), N));
+    ++c.launches;
+    for (int64_t i = j + 1; i < c.L0; ++i) {
+      CB(cublasDgemm(w->blas, CUBLAS_OP_N, CUBLAS_OP_T, N, N, N, &mone, panel + (i - k - 1) * NN, N, Bjk, N, &one,
+                     tile(c, G, j, i), N));
+      ++c.launches;
+    }
+  }
+}
+
+void comm(Ctx& c, cudaError_t e) {
+  if (e == cudaErrorNotReady) throw IpmFail{POLYA_ENCCL, "distributed factorisation before polya_nccl_init"};
+  if (e != cudaSuccess) throw IpmFail{POLYA_ENCCL, c.last_error};
+}
+
+// Collective over the ranks of the context (NCCL; no communication with one rank).
+bool dist_potrf(Ctx& c, Ipm* w, cudaStream_t s) {
+  const int64_t NN = c.Ntil * c.Ntil;
+  for (int64_t k = 0; k < c.L0; ++k) {
+    const int o = owner(c, k);
+    int info = 0;
+    if (c.cfg.rank == o) info = dist_potrf_kk(c, w, w->G, k, s);
+    if (c.cfg.nranks > 1) {   // every rank learns the owner's verdict on L_kk
+      CK(cudaMemcpyAsync(w->info, &info, sizeof(int), cudaMemcpyHostToDevice, s));
+      comm(c, comm_bcast(c, w->info, 1, true, o, s));
+      CK(cudaMemcpyAsync(&info, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    if (info != 0) return false;
+    if (k + 1 == c.L0) break;
+    const bool mine = c.cfg.rank == o;
+    double* Lkk = mine ? tile(c, w, k, k) : w->lkk;
+    double* panel = mine ? tile(c, w, k, k + 1) : w->panel;
+    const int64_t nq = c.L0 - k - 1;
+    comm(c, comm_bcast(c, Lkk, (size_t)NN, false, o, s));
+    comm(c, comm_bcast(c, panel, (size_t)(nq * NN), false, o, s));
+    dist_trsm_share(c, w, k, Lkk, panel, s);
+    comm(c, comm_bcast_tiles(c, panel, (size_t)NN, nq, s));   // tile q from rank q mod N
+    dist_update(c, w, w->G, k, panel, s);
+  }
+  return true;
+}
+
+// x <- G^{-1} x with the distributed factor: the owner of column k does its triangular solve and
+// its panel's matrix-vector updates, then broadcasts the part of x it changed.
+void dist_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
+  const int N = (int)c.Ntil;
+  const int64_t T = c.L0;
+  const double one = 1.0, mone = -1.0;
+  CB(cublasSetStream(w->blas, s));
+  for (int64_t k = 0; k < T; ++k) {
+    const int o = owner(c, k);
+    double* xk = x + k * N;
+    if (c.cfg.rank == o) {
+      CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, N, tile(c, w, k, k), N, xk, 1));
+      for (int64_t i = k + 1; i < T; ++i)
+        CB(cublasDgemv(w->blas, CUBLAS_OP_N, N, N, &mone, tile(c, w, k, i), N, xk, 1, &one, x + i * N, 1));
+      c.launches += T - k;
+    }
+    comm(c, comm_bcast(c, xk, (size_t)((T - k) * N), false, o, s));
+  }
+  for (int64_t k = T - 1; k >= 0; --k) {
+    const int o = owner(c, k);
+    double* xk = x + k * N;
+    if (c.cfg.rank == o) {
+      for (int64_t i = k + 1; i < T; ++i)
+        CB(cublasDgemv(w->blas, CUBLAS_OP_T, N, N, &mone, tile(c, w, k, i), N, x + i * N, 1, &one, xk, 1));
+      CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, N, tile(c, w, k, k), N, xk, 1));
+      c.launches += T - k;
+    }
+    comm(c, comm_bcast(c, xk, (size_t)N, false, o, s));
+  }
+}
+
+// G <- G + eps I, eps = 1e-12 tr(G) / K (the regularised retry) on this rank's diagonal tiles, the
+// trace summed over the ranks.  Returns eps.
+double dist_regularise(Ctx& c, Ipm* w, cudaStream_t s) {
+  std::vector<double> part(kScalarBlocks);
+  double tr = 0.0;
+  for (int64_t h = 0; h < c.L0; ++h) {
+    if (owner(c, h) != c.cfg.rank) continue;
+    k_diag_sum<<<kScalarBlocks, 256, 0, s>>>(tile(c, w, h, h), c.Ntil, c.Ntil, 1, 1, w->part);
+    ++c.launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(part.data(), w->part, kScalarBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (double v : part) tr += v;
+  }
+  CK(cudaMemcpyAsync(w->part, &tr, sizeof(double), cudaMemcpyHostToDevice, s));
+  comm(c, comm_allreduce_sum(c, w->part, 1, s));
+  CK(cudaMemcpyAsync(&tr, w->part, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const double eps = 1e-12 * std::fabs(tr) / (double)c.K;
+  for (int64_t h = 0; h < c.L0; ++h) {
+    if (owner(c, h) != c.cfg.rank) continue;
+    k_diag_shift<<<kScalarBlocks, 256, 0, s>>>(tile(c, w, h, h), c.Ntil, c.Ntil, 1, 1, eps);
+    ++c.launches;
+    CK(cudaGetLastError());
+  }
+  return eps;
+}
+
+void solveG(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
+  if (w->dist) dist_potrs(c, w, x, s);
+  else if (w->tiled) tiled_potrs(c, w, x, s);
+  else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, x, (int)c.K, w->info));
+}
+
 // Cholesky of the Schur complement (dense or tiled); false if not positive definite.
 bool factor(Ctx& c, Ipm* w, cudaStream_t s) {
+  if (w->dist) return dist_potrf(c, w, s);
   if (w->tiled) {
     try {
       tiled_potrf(c, w, s);
@@ -648,8 +815,8 @@ polya_status call(polya_status st, Ctx& c) {
 extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, polya_ipm_stats* stats, void* stream) {
   if (!ctx || !st || !st->X || !st->Z || !st->y) return POLYA_EINVAL;
   Ctx& c = ctx->c;
-  if (c.cfg.nranks != 1) {
-    c.last_error = "polya_ipm_step runs on a single rank (distributed factorisation is out of scope)";
+  if (c.cfg.nranks != 1 && c.cfg.shard != POLYA_SHARD_CYCLIC) {
+    c.last_error = "polya_ipm_step on several ranks needs SHARD_CYCLIC (the distributed factorisation)";
     return POLYA_EINVAL;
   }
   if ((c.n * c.n + c.n) * (int64_t)sizeof(double) > 227 * 1024) {
@@ -698,19 +865,24 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
       // G near-singular (it becomes ill-conditioned near convergence): one retry on G + eps I with
       // eps = 1e-12 tr(G) / K (SURVEY 8(b) ENOTPD).  potrf destroyed G: re-assemble it.
       call(polya_schur(ctx, X, w->W, w->G, glayout, s), c);
-      const int tiled = w->tiled ? 1 : 0;
-      k_diag_sum<<<kScalarBlocks, 256, 0, s>>>(w->G, c.K, c.Ntil, c.L0, tiled, w->part);
-      ++c.launches;
-      CK(cudaGetLastError());
-      std::vector<double> part(kScalarBlocks);
-      CK(cudaMemcpyAsync(part.data(), w->part, kScalarBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      double tr = 0.0;
-      for (double v : part) tr += v;
-      const double eps = 1e-12 * std::fabs(tr) / (double)c.K;
-      k_diag_shift<<<kScalarBlocks, 256, 0, s>>>(w->G, c.K, c.Ntil, c.L0, tiled, eps);
-      ++c.launches;
-      CK(cudaGetLastError());
+      double eps = 0.0;
+      if (w->dist) {
+        eps = dist_regularise(c, w, s);
+      } else {
+        const int tiled = w->tiled ? 1 : 0;
+        k_diag_sum<<<kScalarBlocks, 256, 0, s>>>(w->G, c.K, c.Ntil, c.L0, tiled, w->part);
+        ++c.launches;
+        CK(cudaGetLastError());
+        std::vector<double> part(kScalarBlocks);
+        CK(cudaMemcpyAsync(part.data(), w->part, kScalarBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double tr = 0.0;
+        for (double v : part) tr += v;
+        eps = 1e-12 * std::fabs(tr) / (double)c.K;
+        k_diag_shift<<<kScalarBlocks, 256, 0, s>>>(w->G, c.K, c.Ntil, c.L0, tiled, eps);
+        ++c.launches;
+        CK(cudaGetLastError());
+      }
       retries = 1;
       if (!(eps > 0.0) || !factor(c, w, s))
         throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite after one regularised retry"};
@@ -718,8 +890,7 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     CK(cudaEventRecord(w->ev[3], s));
     // dy^ = G^-1 O1
     CK(cudaMemcpyAsync(w->dy1, w->O1, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (w->tiled) tiled_potrs(c, w, w->dy1, s);
-    else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy1, (int)c.K, w->info));
+    solveG(c, w, w->dy1, s);
     // dZ^ = -Rd + B^T(dy^);  dX^ = sym(-X + W (Rd - B^T(dy^)) X)
     call(polya_apply(ctx, w->dy1, w->T1, s), c);
     axpby(c, -1.0, w->Rd, 1.0, w->T1, w->dZ1, nullptr, 0.0, s);          // dZ^
@@ -735,8 +906,7 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     call(polya_adjoint(ctx, w->T2, w->O2, s), c);
     vaxpby(c, mu, w->tmpK, -1.0, w->O2, w->O2, s);
     CK(cudaMemcpyAsync(w->dy2, w->O2, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (w->tiled) tiled_potrs(c, w, w->dy2, s);
-    else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, w->dy2, (int)c.K, w->info));
+    solveG(c, w, w->dy2, s);
     // dZ- = B^T(dy-);  dX- = sym(mu W - W dZ^ dX^ - W dZ- X)
     call(polya_apply(ctx, w->dy2, w->dZ2, s), c);
     bgemm(c, w->dZ2, 0, X, 0, w->T1, 1.0, 0.0, s);                         // dZ- X
@@ -786,6 +956,94 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     }
   } catch (const IpmFail& f) {
     c.last_error = f.msg;
+    return f.s;
+  }
+  return POLYA_OK;
+}
+
+// ---- the distributed factorisation with an in-process loopback in place of NCCL (tests) --------
+// All ranks' contexts live in this process on one device and run the SAME step functions as
+// dist_potrf / dist_potrs, one rank after another within each step; each broadcast is a device
+// copy from the owner's buffer into every other rank's.  This checks the partition, the local tile
+// indexing, the panel bookkeeping and the x exchange of the multi-rank path on one GPU (NCCL
+// refuses two ranks on one device); the NCCL calls themselves are the one-line comm_bcast.
+extern "C" polya_status polya_factor_solve_loopback(polya_ctx** ctxs, int32_t nranks, double* const* G_local, double* x,
+                                                    void* stream) {
+  if (!ctxs || nranks < 1 || !G_local || !x) return POLYA_EINVAL;
+  for (int32_t r = 0; r < nranks; ++r) {
+    if (!ctxs[r] || !G_local[r]) return POLYA_EINVAL;
+    const Ctx& c = ctxs[r]->c;
+    if (c.cfg.shard != POLYA_SHARD_CYCLIC || c.cfg.nranks != nranks || c.cfg.rank != r || c.K != ctxs[0]->c.K)
+      return POLYA_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  Ctx& c0 = ctxs[0]->c;
+  const int64_t T = c0.L0, N = c0.Ntil, NN = N * N, K = c0.K;
+  try {
+    std::vector<Ipm*> w(nranks);
+    for (int32_t r = 0; r < nranks; ++r) w[r] = ipm_ws(ctxs[r]->c);
+    for (int64_t k = 0; k < T; ++k) {
+      const int o = owner(c0, k);
+      if (dist_potrf_kk(ctxs[o]->c, w[o], G_local[o], k, s) != 0)
+        throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite (tile " + std::to_string(k) + ")"};
+      if (k + 1 == T) break;
+      const int64_t nq = T - k - 1;
+      std::vector<double*> Lkk(nranks), panel(nranks);
+      for (int32_t r = 0; r < nranks; ++r) {
+        Lkk[r] = r == o ? tile(ctxs[o]->c, G_local[o], k, k) : w[r]->lkk;
+        panel[r] = r == o ? tile(ctxs[o]->c, G_local[o], k, k + 1) : w[r]->panel;
+      }
+      for (int32_t r = 0; r < nranks; ++r) {
+        if (r == o) continue;   // the two broadcasts of the owner: L_kk and the raw panel
+        CK(cudaMemcpyAsync(Lkk[r], Lkk[o], (size_t)NN * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(panel[r], panel[o], (size_t)(nq * NN) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+      for (int32_t r = 0; r < nranks; ++r) dist_trsm_share(ctxs[r]->c, w[r], k, Lkk[r], panel[r], s);
+      for (int64_t q = 0; q < nq; ++q)   // solved tile q from rank q mod N to every other rank
+        for (int32_t r = 0; r < nranks; ++r)
+          if (r != q % nranks)
+            CK(cudaMemcpyAsync(panel[r] + q * NN, panel[q % nranks] + q * NN, (size_t)NN * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+      for (int32_t r = 0; r < nranks; ++r) dist_update(ctxs[r]->c, w[r], G_local[r], k, panel[r], s);
+    }
+    // the solves with one copy of x per rank (tmpK), exchanged like dist_potrs's broadcasts
+    const double one = 1.0, mone = -1.0;
+    for (int32_t r = 0; r < nranks; ++r) CK(cudaMemcpyAsync(w[r]->tmpK, x, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    auto send = [&](int o, int64_t off, int64_t cnt) {
+      for (int32_t r = 0; r < nranks; ++r)
+        if (r != o)
+          CK(cudaMemcpyAsync(w[r]->tmpK + off, w[o]->tmpK + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    };
+    for (int64_t k = 0; k < T; ++k) {
+      const int o = owner(c0, k);
+      Ctx& c = ctxs[o]->c;
+      Ipm* wo = w[o];
+      CB(cublasSetStream(wo->blas, s));
+      double* xo = wo->tmpK;
+      CB(cublasDtrsv(wo->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)N,
+                     tile(c, G_local[o], k, k), (int)N, xo + k * N, 1));
+      for (int64_t i = k + 1; i < T; ++i)
+        CB(cublasDgemv(wo->blas, CUBLAS_OP_N, (int)N, (int)N, &mone, tile(c, G_local[o], k, i), (int)N, xo + k * N, 1,
+                       &one, xo + i * N, 1));
+      send(o, k * N, (T - k) * N);
+    }
+    for (int64_t k = T - 1; k >= 0; --k) {
+      const int o = owner(c0, k);
+      Ctx& c = ctxs[o]->c;
+      Ipm* wo = w[o];
+      CB(cublasSetStream(wo->blas, s));
+      double* xo = wo->tmpK;
+      for (int64_t i = k + 1; i < T; ++i)
+        CB(cublasDgemv(wo->blas, CUBLAS_OP_T, (int)N, (int)N, &mone, tile(c, G_local[o], k, i), (int)N, xo + i * N, 1,
+                       &one, xo + k * N, 1));
+      CB(cublasDtrsv(wo->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)N,
+                     tile(c, G_local[o], k, k), (int)N, xo + k * N, 1));
+      send(o, k * N, N);
+    }
+    CK(cudaMemcpyAsync(x, w[nranks - 1]->tmpK, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  } catch (const IpmFail& f) {
+    c0.last_error = f.msg;
     return f.s;
   }
   return POLYA_OK;

@@ -424,18 +424,45 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     c.pair1 = std::upper_bound(c.pair_item_global.begin(), c.pair_item_global.end(), c.item1 - 1) -
               c.pair_item_global.begin();
   }
+  // local pairs and the kernel's item numbering: a contiguous pair range with the global item
+  // prefix (TILES, BLOCKS), or the pairs (h, h') with h = rank mod nranks numbered from 0 (CYCLIC)
+  c.local_pairs.clear();
+  c.local_item.clear();
+  c.pair_local.assign(c.npairs, -1);
+  if (g.shard == POLYA_SHARD_CYCLIC) {
+    c.local_item.push_back(0);
+    for (int64_t p = 0; p < c.npairs; ++p)
+      if (ph[p] % g.nranks == g.rank) {
+        c.pair_local[p] = (int32_t)c.local_pairs.size();
+        c.local_pairs.push_back(p);
+        c.local_item.push_back(c.local_item.back() + pItems[p]);
+      }
+    c.item0 = 0;
+    c.item1 = c.local_item.back();
+    c.pair0 = c.local_pairs.empty() ? 0 : c.local_pairs.front();
+    c.pair1 = c.local_pairs.empty() ? 0 : c.local_pairs.back() + 1;
+  } else {
+    for (int64_t p = c.pair0; p < c.pair1; ++p) {
+      c.pair_local[p] = (int32_t)c.local_pairs.size();
+      c.local_pairs.push_back(p);
+      c.local_item.push_back(c.pair_item_global[p]);
+    }
+    c.local_item.push_back(c.pair_item_global[c.pair1]);
+  }
   c.useful_flops_rank = 0;
-  for (int64_t p = c.pair0; p < c.pair1; ++p) {
-    int64_t a = std::max(c.item0, c.pair_item_global[p]), b = std::min(c.item1, c.pair_item_global[p + 1]);
+  for (size_t q = 0; q < c.local_pairs.size(); ++q) {
+    const int64_t p = c.local_pairs[q];
+    const int64_t lo = g.shard == POLYA_SHARD_CYCLIC ? c.local_item[q] : c.pair_item_global[p];
+    const int64_t a = std::max(c.item0, lo), b = std::min(c.item1, lo + pItems[p]);
     c.useful_flops_rank += (ph[p] == ph2[p] ? 1.0 : 2.0) * n4 * pK[p] * (double)(b - a) / (double)pItems[p];
   }
-  c.npairs_local = c.pair1 - c.pair0;
+  c.npairs_local = (int64_t)c.local_pairs.size();
   if (!device) return;  // polya_plan: host-side bookkeeping only
 
   // ---- arena layout --------------------------------------------------------------------------
   // Q, R: one per (local pair, Lyapunov block active for both rows)
   int64_t nQR = 0;
-  for (int64_t p = c.pair0; p < c.pair1; ++p) nQR += pMu[p];
+  for (int64_t p : c.local_pairs) nQR += pMu[p];
   c.nQR = nQR;
   int64_t id = 0;
   c.id_X = id; id += c.nb;
@@ -571,8 +598,9 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     std::vector<GemmTerm> tm;
     int64_t q = 0;
     kbeg.push_back(0);
-    pitem.push_back(c.pair_item_global[c.pair0]);
-    for (int64_t p = c.pair0; p < c.pair1; ++p) {
+    pitem.push_back(c.local_item.empty() ? 0 : c.local_item[0]);
+    for (size_t lp = 0; lp < c.local_pairs.size(); ++lp) {
+      const int64_t p = c.local_pairs[lp];
       const int64_t h = ph[p], h2 = ph2[p];
       qh.push_back((int32_t)h);
       qh2.push_back((int32_t)h2);
@@ -630,7 +658,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
         kL.push_back((int32_t)c.id_Zero); kR.push_back((int32_t)c.id_Zero);
       }
       kbeg.push_back((int64_t)kL.size());
-      pitem.push_back(c.pair_item_global[p + 1]);
+      pitem.push_back(c.local_item[lp + 1]);
     }
     c.nk_local = (int64_t)kL.size();
     c.n_items_QR = (int64_t)it.size();
@@ -767,7 +795,7 @@ extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_hos
   if (!cfg || !A_host) return POLYA_EINVAL;
   const polya_config& g = *cfg;
   if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
-      g.rank < 0 || g.rank >= g.nranks || (g.shard != POLYA_SHARD_TILES && g.shard != POLYA_SHARD_BLOCKS))
+      g.rank < 0 || g.rank >= g.nranks || (g.shard < POLYA_SHARD_TILES || g.shard > POLYA_SHARD_CYCLIC))
     return POLYA_EINVAL;
   polya_ctx* ctx = new (std::nothrow) polya_ctx();
   if (!ctx) return POLYA_ENOMEM;
@@ -798,7 +826,7 @@ extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nte
   if (!cfg || nterms < 1 || !deg_a || !deg_b || !At || !Bt) return POLYA_EINVAL;
   const polya_config& g = *cfg;
   if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
-      g.rank < 0 || g.rank >= g.nranks || (g.shard != POLYA_SHARD_TILES && g.shard != POLYA_SHARD_BLOCKS))
+      g.rank < 0 || g.rank >= g.nranks || (g.shard < POLYA_SHARD_TILES || g.shard > POLYA_SHARD_CYCLIC))
     return POLYA_EINVAL;
   for (int32_t i = 0; i < nterms; ++i)   // every term homogeneous of the one total degree cfg->da (R18)
     if (deg_a[i] < 0 || deg_b[i] < 0 || deg_a[i] + deg_b[i] != g.da) return POLYA_EINVAL;
@@ -834,13 +862,14 @@ static void fill_dims(const Ctx& c, polya_dims* o) {
   o->b1 = c.b1;
   const int64_t tot = c.npairs * c.Ntil * c.Ntil;
   o->reduce_count = c.cfg.shard == POLYA_SHARD_BLOCKS ? (tot + c.cfg.nranks - 1) / c.cfg.nranks : 0;
+  o->npairs_local = c.npairs_local;
 }
 
 extern "C" polya_status polya_plan(const polya_config* cfg, polya_dims* out) {
   if (!cfg || !out) return POLYA_EINVAL;
   const polya_config& g = *cfg;
   if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
-      g.rank < 0 || g.rank >= g.nranks || (g.shard != POLYA_SHARD_TILES && g.shard != POLYA_SHARD_BLOCKS))
+      g.rank < 0 || g.rank >= g.nranks || (g.shard < POLYA_SHARD_TILES || g.shard > POLYA_SHARD_CYCLIC))
     return POLYA_EINVAL;
   try {
     Ctx c;
@@ -1050,8 +1079,8 @@ extern "C" polya_status polya_schur_assemble(polya_ctx* ctx, double* G, int layo
   try {
     int64_t i0 = c.item0, i1 = c.item1;
     if (c.npairs_local > 0) {
-      i0 = std::max(c.item0, c.pair_item_global[c.pair0 + pair_begin]);
-      i1 = std::min(c.item1, c.pair_item_global[c.pair0 + pair_end]);
+      i0 = std::max(c.item0, c.local_item[pair_begin]);
+      i1 = std::min(c.item1, c.local_item[pair_end]);
     }
     CU(launch_schur(c, G, layout, i0, i1, s));
     if (c.timing) CU(cudaEventRecord(c.ev[2], s));

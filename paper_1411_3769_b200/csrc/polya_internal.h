@@ -76,6 +76,9 @@ struct Ctx {
   int64_t b0 = 0, b1 = 0;  // this rank's Polya blocks (SHARD_BLOCKS; all blocks otherwise)
   void* nccl = nullptr;    // ncclComm_t of polya_nccl_init (SHARD_BLOCKS combine)
   std::vector<int64_t> pair_item_global;  // [npairs + 1]
+  std::vector<int64_t> local_pairs;       // this rank's pairs (global indices, ascending)
+  std::vector<int64_t> local_item;        // [npairs_local + 1] item prefix of the local pairs (kernel numbering)
+  std::vector<int32_t> pair_local;        // [npairs] local index of a pair, or -1
   double useful_flops_total = 0, useful_flops_rank = 0;
   // arena (np x np matrices)
   int64_t mstride = 0, nmats = 0;
@@ -129,6 +132,10 @@ cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
 cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s);
 cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
 cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t item0, int64_t item1, cudaStream_t s);
+// collectives of the distributed factorisation (combine.cpp; no-ops with one rank)
+cudaError_t comm_bcast(Ctx& c, void* buf, size_t count, bool is_int, int root, cudaStream_t s);
+cudaError_t comm_allreduce_sum(Ctx& c, double* buf, size_t count, cudaStream_t s);
+cudaError_t comm_bcast_tiles(Ctx& c, double* buf, size_t count, int64_t ntiles, cudaStream_t s);
 
 }  // namespace polya
 

@@ -40,3 +40,22 @@ def test_block_partition(shape):
         # tiles mode: all blocks on every rank
         dt = pb.plan(*shape, rank=0, nranks=world)
         assert dt["b0"] == 0 and dt["b1"] == nb and dt["reduce_count"] == 0
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "n%d_l%d" % (s[0], s[1]))
+def test_cyclic_partition(shape):
+    """SHARD_CYCLIC (the distributed factorisation's layout): rank r holds the pair rows h = r mod N
+    completely -- local pairs of all ranks partition the pairs, their FLOPs add up to the total, and
+    the item numbering is per rank from 0."""
+    import paper_1411_3769_b200 as pb
+    total = pb.plan(*shape)["useful_flops_schur"]
+    for world in (1, 2, 3, 8):
+        ds = [pb.plan(*shape, rank=r, nranks=world, shard=pb.SHARD_CYCLIC) for r in range(world)]
+        L0 = ds[0]["L0"]
+        assert sum(d["npairs_local"] for d in ds) == ds[0]["npairs"]
+        for r, d in enumerate(ds):
+            rows = [h for h in range(L0) if h % world == r]
+            assert d["npairs_local"] == sum(L0 - h for h in rows)
+            assert d["item0"] == 0
+            assert d["tiles_bytes"] == d["npairs_local"] * d["Ntil"] ** 2 * 8
+        assert abs(sum(d["useful_flops_schur"] for d in ds) - total) <= 1e-9 * total
