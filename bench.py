@@ -8,15 +8,16 @@ on config 4 (n=100, l=4, dp=2, d1=d2=4; K=50,500, 204 Polya blocks) by default.
 value = W_G / t_step (TFLOP/s), W_G = n^4 (sum nu^2 + 4 sum mu^2) the algorithmic FP64 FLOPs
 of the Schur assembly; t_step is the max over ranks.
 
-Launch: python bench.py [--gpus N --steps K --warmup W --config 4|5 --shard tiles|blocks]
+Launch: python bench.py [--gpus N --steps K --warmup W --config 4|5 --shard tiles|blocks|cyclic]
         torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU; default output-tile
         sharding of G: no inter-GPU traffic on the data path, NCCL only for the barrier and the
         max-over-ranks timing; --shard blocks: the paper's Polya-block partition with the partial
-        G summed by NCCL ReduceScatter inside the step)
+        G summed by NCCL ReduceScatter inside the step; --shard cyclic: the column-cyclic pair
+        tiles of the distributed factorisation, whose IPM iteration is then timed at any N)
         python bench.py --impl reference ...   (the CPU oracle, rank 0 only)
 The JSON line also carries the roofline of the dominant kernel (K4), the CPU-oracle baseline,
 an end-to-end figure through the public API (pinned host inputs in, all of G back out, streamed
-during the assembly), the seconds per IPM iteration (N = 1) and the SM clocks sampled during
+during the assembly), the seconds per IPM iteration (N = 1, or any N with --shard cyclic) and the SM clocks sampled during
 the timed region.
 """
 from __future__ import annotations
@@ -240,10 +241,11 @@ def run_gpu(args, cfg, cid):
     A, X, W = synth.make_case(cfg, L + M, seed=0)
     t0 = time.perf_counter()
     blocks = args.shard == "blocks"
+    cyclic = args.shard == "cyclic"
     ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world,
-                   shard=pb.SHARD_BLOCKS if blocks else pb.SHARD_TILES)
+                   shard=pb.SHARD_BLOCKS if blocks else pb.SHARD_CYCLIC if cyclic else pb.SHARD_TILES)
     setup_s = time.perf_counter() - t0
-    if blocks:   # NCCL communicator of the library (id from rank 0, distributed over the process group)
+    if blocks or cyclic:   # NCCL communicator of the library (id from rank 0, distributed over the process group)
         uid = [pb.nccl_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(uid, src=0)
@@ -364,9 +366,9 @@ def run_gpu(args, cfg, cid):
                "d2h_overlap": f"G streamed back in {nch} pair chunks while later chunks are assembled"}
         del Gh, Gres
 
-    # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step; N=1 only) ----
+    # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step; N=1, or any N with --shard cyclic) ----
     ipm = None
-    if world == 1 and not blocks and not args.no_ipm:   # dense K x K factorisation, or tiled when it does not fit (cfg 5)
+    if ((world == 1 and not blocks) or cyclic) and not args.no_ipm:   # dense K x K, tiled (cfg 5) or distributed
         del G
         flush = None
         torch.cuda.empty_cache()
@@ -385,10 +387,13 @@ def run_gpu(args, cfg, cid):
             mu = st["mu"]
             runs.append((e0.elapsed_time(e1), st))
         ms, st = runs[-1]
+        ms = max_over_ranks(ms)
         tiled = ctx.K * ctx.K * 8 > 0.45 * torch.cuda.get_device_properties(dev).total_memory
         ipm = {"s_per_iteration": ms / 1e3, "ms_schur": st["ms_schur"], "ms_factorisation": st["ms_factor"],
                "ms_other": st["ms_other"],
-               "factorisation": ("blocked Cholesky on the pair tiles (cuSOLVER dpotrf on diagonal tiles, cuBLAS "
+               "factorisation": (f"distributed blocked Cholesky over {world} rank(s) (column-cyclic pair tiles, NCCL "
+                                 "panel broadcasts, split panel solves; DESIGN.md 7.1)" if cyclic else
+                                 "blocked Cholesky on the pair tiles (cuSOLVER dpotrf on diagonal tiles, cuBLAS "
                                  "dtrsm/dsyrk/dgemm) + blocked solves" if tiled else
                                  "cuSOLVER dpotrf + 2 dpotrs on the K x K SCM (FULL)"),
                "iteration_measured": 2, "gap": st["gap"], "tp": st["tp"], "td": st["td"]}
@@ -425,7 +430,8 @@ def run_gpu(args, cfg, cid):
                                + (" + polya_reduce_G (NCCL ReduceScatter)" if blocks else ""),
                        "layout": "G pair tiles (upper, row-panel ready)",
                        "parallelism": (f"Polya-block shards x{world} + NCCL ReduceScatter of partial G" if blocks
-                                       else f"output-tile shards x{world}"),
+                                       else f"column-cyclic pair-tile shards x{world} (distributed factorisation)"
+                                       if cyclic else f"output-tile shards x{world}"),
                        "l2": "256 MiB memset between timed steps (outside the events); G write alone is "
                              f"{npl * N * N * 8 / 1e9:.1f} GB/step"},
             "breakdown_ms": {"schur_precompute": t_pre, "schur_assembly": t_asm,
@@ -457,9 +463,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--shard", default="tiles", choices=["tiles", "blocks"],
+    ap.add_argument("--shard", default="tiles", choices=["tiles", "blocks", "cyclic"],
                     help="tiles: output-tile sharding, no data-path collective (default); blocks: the paper's "
-                         "Polya-block sharding with the partial G summed by NCCL ReduceScatter")
+                         "Polya-block sharding with the partial G summed by NCCL ReduceScatter; cyclic: "
+                         "column-cyclic pair tiles, the layout of the distributed factorisation (IPM leg at any N)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ipm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
