@@ -94,6 +94,32 @@ def test_loopback_factor_solve(pb, cfg):
         assert np.array_equal(xs[world], xs[1]), world
 
 
+def test_loopback_more_ranks_than_tile_rows(pb):
+    """N > L0: some ranks own no block column (no tiles, no work) and only relay broadcasts."""
+    cfg = synth.CONFIGS[1]          # L0 = 2
+    rng = np.random.default_rng(4)
+    A = synth.vertex_matrices(cfg, rng)
+    ctx0 = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A)
+    X, W = synth.spd_blocks(cfg.n, ctx0.nblocks, rng)
+    full = ctx0.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES).cpu().numpy()
+    L0, N, K = ctx0.L0, ctx0.Ntil, ctx0.K
+    ctx0.close()
+    b = rng.normal(size=K)
+    ref = np.linalg.solve(_dense(full, L0, N), b)
+    world = 5
+    ctxs = [pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=world, shard=pb.SHARD_CYCLIC)
+            for r in range(world)]
+    assert [c.dims["npairs_local"] for c in ctxs] == [2, 1, 0, 0, 0]
+    pairs = _pairs(L0)
+    Gs = [_dev(full[[p for p, (h, _) in enumerate(pairs) if h % world == r]]) if ctxs[r].dims["npairs_local"]
+          else torch.zeros(1, dtype=torch.float64, device="cuda") for r in range(world)]
+    x = _dev(b)
+    pb.factor_solve_loopback(ctxs, Gs, x)
+    assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
+    for c in ctxs:
+        c.close()
+
+
 def test_loopback_reports_indefinite_G(pb):
     cfg = synth.CONFIGS[2]
     rng = np.random.default_rng(2)
