@@ -39,9 +39,10 @@ __all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "g
 def C_blocks(P):
     """C = diag(c_1 I, ..., c_L I, 0, ..., 0) (Eq. C, Eq. Cj); the generalised form's constant term
     R puts (sum alpha)^{d2} R(alpha)'s coefficients on the Lyapunov blocks (reading R18)."""
-    C = np.zeros((P.nblocks, P.n, P.n))
+    C = np.zeros((P.nblocks, P.bn, P.bn))
     for j in range(P.L):
-        C[j] = P.c[j] * np.eye(P.n)
+        C[j] = -np.eye(P.bn)          # the padding of a P-block (non-square form, R19): slack Z = I there
+        C[j][:P.n, :P.n] = P.c[j] * np.eye(P.n)
     if P.CL is not None:
         C[P.L:] = P.CL
     return C
@@ -49,7 +50,7 @@ def C_blocks(P):
 
 def initial_state(P):
     """Algorithm 2 initialisation: X = Z = I, y = 0, mu = barrier(Z, X)."""
-    X = np.broadcast_to(np.eye(P.n), (P.nblocks, P.n, P.n)).copy()
+    X = np.broadcast_to(np.eye(P.bn), (P.nblocks, P.bn, P.bn)).copy()
     Z = X.copy()
     y = np.zeros(P.K)
     return X, Z, y, barrier(P, Z, X)
@@ -57,7 +58,7 @@ def initial_state(P):
 
 def barrier(P, Z, X):
     """Reading R4: mu = (1/3) sum_b tr(Z_b X_b) / ((L+M) n)."""
-    return sum(np.trace(Z[b] @ X[b]) for b in range(P.nblocks)) / (3.0 * P.nblocks * P.n)
+    return sum(np.trace(Z[b] @ X[b]) for b in range(P.nblocks)) / (3.0 * P.nblocks * P.bn)
 
 
 def _sym(M):

@@ -78,6 +78,20 @@ class Problem:
     pairs: list = None        # its (Atil_i, deg_a, Btil_i, deg_b) terms
     R: np.ndarray = None      # its constant term R(alpha), coefficients in W_{dp+e} order (or None)
     CL: np.ndarray = None     # C on the Lyapunov blocks: coefficients of (sum alpha)^{d2} R(alpha)
+    N: int = None             # block order (generalised form with N x n At_i: N > n, reading R19); None: n
+
+    @property
+    def bn(self):
+        """Order of every block of X, Z, C and B^T(y): n, or N for the non-square generalised form."""
+        return self.n if self.N is None else self.N
+
+    def embed(self, M):
+        """An n x n P-block quantity as the top-left corner of a bn x bn block (reading R19)."""
+        if self.bn == self.n:
+            return M
+        out = np.zeros((self.bn, self.bn))
+        out[:self.n, :self.n] = M
+        return out
 
     @property
     def nblocks(self):
@@ -104,6 +118,9 @@ def build_problem(A, n, l, dp, d1, d2, da=1, delta=1e-3) -> Problem:
 
 
 def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3, R=None) -> Problem:
+    """(Non-square: At_i coefficients N x n, Bt_i n x N, R N x N with N > n -- the bounded-real-lemma
+    shape -- make every block N x N, the P-blocks' n x n LMI sitting in the top-left corner with C
+    = -I on the rest, so that their slack Z is I there; reading R19.)"""
     """The generalised LMI form of PAPER.md:454-459, square case:
         P(alpha) > 0,   sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) + R(alpha) < 0,
     with pairs = [(At_i coefficients [f(l,a_i)][n][n] in W_{a_i} order, a_i, Bt_i coefficients, b_i)],
@@ -140,12 +157,13 @@ def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3, R=None) -> Proble
     c = polya.C_scalars(beta, l, dp, delta)
     CL = None
     if R is not None:
-        CL = np.zeros((M, n, n))
+        CL = np.zeros((M,) + np.asarray(R).shape[1:])
         for ri, rho in enumerate(enumerate_W(l, dp + e)):
             for e2, w in polya.poly_mul(S, {tuple(rho): 1}).items():
                 CL[idx[e2]] += float(w) * np.asarray(R[ri], dtype=float)
+    Nb = int(np.asarray(pairs[0][0]).shape[1])
     return Problem(n, l, dp, e, d1, d2, delta, L0, L, M, Ntil, L0 * Ntil, beta, np.zeros((L0, M, 0, 0)), c, None,
-                   basis(n), gen=gen, pairs=pairs, R=R, CL=CL)
+                   basis(n), gen=gen, pairs=pairs, R=R, CL=CL, N=None if Nb == n else Nb)
 
 
 def vmap(P: Problem, x, h: int):
@@ -175,9 +193,9 @@ def F_block(P: Problem, i: int, b: int):
     h, k = divmod(i, P.Ntil)
     E = E_matrix(P.n, P.E[k])
     if b < P.L:
-        return float(P.beta[h, b]) * E
+        return P.embed(float(P.beta[h, b]) * E)
     if P.gen is not None:
-        F = np.zeros((P.n, P.n))
+        F = np.zeros((P.bn, P.bn))
         for Aq, Bq in P.gen[h][b - P.L]:
             F -= Aq @ E @ Bq + Bq.T @ E @ Aq.T
         return F
@@ -193,7 +211,7 @@ def F_stack(P: Problem, b: int, rows=None):
 
 def apply_literal(P: Problem, y):
     """B^T(y) = sum_i y_i B_i (Eq. AT), blockwise, dense F."""
-    out = np.zeros((P.nblocks, P.n, P.n))
+    out = np.zeros((P.nblocks, P.bn, P.bn))
     for b in range(P.nblocks):
         for i in range(P.K):
             if y[i] != 0.0:
@@ -204,11 +222,11 @@ def apply_literal(P: Problem, y):
 def apply_vmap(P: Problem, y):
     """B^T(y) via Eq. (31) with e_i replaced by y (V is linear, Eq. 30):
     P-block j: sum_h beta_{h,j} V_h(y); Lyapunov block m: -sum_h (H^T V_h(y) + V_h(y) H)."""
-    out = np.zeros((P.nblocks, P.n, P.n))
+    out = np.zeros((P.nblocks, P.bn, P.bn))
     V = [vmap(P, y, h) for h in range(P.L0)]
     for j in range(P.L):
         for h in range(P.L0):
-            out[j] += float(P.beta[h, j]) * V[h]
+            out[j] += P.embed(float(P.beta[h, j]) * V[h])
     for m in range(P.M):
         for h in range(P.L0):
             if P.gen is not None:
@@ -238,7 +256,7 @@ def adjoint_trace(P: Problem, Xb):
             if b < P.L:
                 if P.beta[h, b] == 0:
                     continue
-                M = float(P.beta[h, b]) * Xb[b]
+                M = float(P.beta[h, b]) * Xb[b][:P.n, :P.n]
             elif P.gen is not None:
                 terms = P.gen[h][b - P.L]
                 if not terms:
@@ -260,7 +278,7 @@ def schur_literal(P: Problem, Xb, Wb, rows=None):
     tr(F_k Y_l) = sum_pq F_k[p,q] Y_l[q,p] (one library matmul over the flattened blocks)."""
     rows = list(range(P.K)) if rows is None else list(rows)
     G = np.zeros((len(rows), P.K))
-    n2 = P.n * P.n
+    n2 = P.bn * P.bn
     for b in range(P.nblocks):
         Fb = F_stack(P, b)
         Y = np.matmul(np.matmul(Wb[b], Fb), Xb[b])
@@ -311,8 +329,8 @@ def schur_structured(P: Problem, Xb, Wb, pairs=None):
         Ls, Rs = [], []
         for j in range(L):
             if P.beta[h, j] and P.beta[h2, j]:
-                Ls.append(float(P.beta[h, j] * P.beta[h2, j]) * Wb[j])
-                Rs.append(Xb[j])
+                Ls.append(float(P.beta[h, j] * P.beta[h2, j]) * Wb[j][:n, :n])
+                Rs.append(Xb[j][:n, :n])
         for m in range(P.M):
             W, X = Wb[L + m], Xb[L + m]
             if P.gen is not None:

@@ -22,7 +22,7 @@ import dataclasses
 import numpy as np
 
 __all__ = ["CONFIGS", "Config", "vertex_matrices", "spd_blocks", "make_case", "small_config",
-           "discrete_vertex_matrices", "discrete_time_terms", "random_terms"]
+           "discrete_vertex_matrices", "discrete_time_terms", "random_terms", "bounded_real_terms"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -161,3 +161,23 @@ def random_terms(n: int, l: int, degs, rng, counts):
     in by the caller (this module enumerates nothing)."""
     return [(rng.normal(0.0, 1.0, size=(counts(a), n, n)), a, rng.normal(0.0, 1.0, size=(counts(b), n, n)), b)
             for a, b in degs]
+
+
+def bounded_real_terms(A: np.ndarray, Bu: np.ndarray, Cy: np.ndarray, gamma: float):
+    """The bounded-real lemma for x' = A(alpha) x + Bu u, y = Cy x (A polytopic with vertices
+    A (l, n, n); Bu (n, m), Cy (p, n) constant):
+        [[A^T P + P A + Cy^T Cy, P Bu], [Bu^T P, -gamma^2 I]] < 0,  P > 0   <=>  ||G_alpha||_inf < gamma
+    as one generalised term (At, 0, Bt, 1) with At = [I; 0] (N x n, N = n + m) and
+    Bt(alpha) = [A(alpha), Bu] (n x N, vertex coefficients [A_i, Bu]), plus the constant
+    R0 = [[Cy^T Cy, 0], [0, -gamma^2 I]] -- returned as is: the caller homogenises it to the
+    degree dp + 1 of the term (each side with its own homogenisation)."""
+    l, n, _ = A.shape
+    m = Bu.shape[1]
+    N = n + m
+    At = np.zeros((1, N, n))
+    At[0, :n, :n] = np.eye(n)
+    Bt = np.array([np.hstack([a, Bu]) for a in A])
+    R0 = np.zeros((N, N))
+    R0[:n, :n] = Cy.T @ Cy
+    R0[n:, n:] = -gamma ** 2 * np.eye(m)
+    return [(At, 0, Bt, 1)], R0

@@ -134,3 +134,68 @@ def test_constant_term_polynomial_identity():
         assert np.abs(lhs - rhs).max() <= 1e-12 * np.abs(rhs).max()
     # and the P-blocks keep c_j I
     assert np.array_equal(C[0], P.c[0] * np.eye(n))
+
+
+# ---- non-square form (reading R19): the bounded-real lemma, N = n + m --------------------------------
+
+def _brl_problem(A, Bu, Cy, gamma, dp, d1, d2):
+    terms, R0 = synth.bounded_real_terms(A, Bu, Cy, gamma)
+    l, n = A.shape[0], A.shape[1]
+    _, R = polya.homogenize({tuple([dp + 1] + [0] * (l - 1)): 0.0 * R0, tuple([0] * l): R0}, l)
+    return sdp.build_problem_general(terms, n, l, dp, d1, d2, R=R)
+
+
+def _hinf(A, Bu, Cy, w=np.concatenate([[0.0], np.logspace(-3, 3, 2001)])):
+    """max over a frequency grid of sigma_max(Cy (jw I - A)^-1 Bu) (brute force)."""
+    n = A.shape[0]
+    return max(np.linalg.svd(Cy @ np.linalg.solve(1j * x * np.eye(n) - A, Bu), compute_uv=False)[0] for x in w)
+
+
+@pytest.mark.parametrize("a,b,c", [(1.0, 1.0, 1.0), (2.0, 3.0, 0.5), (0.5, 1.0, 2.0)])
+def test_bounded_real_scalar_closed_form(a, b, c):
+    """x' = -a x + b u, y = c x: ||G||_inf = |c b| / a.  Certified at 1.05 of it, not at 0.95: the
+    non-square blocks (N = 2 > n = 1), the padded P-blocks and R together."""
+    A, Bu, Cy = np.array([[[-a]]]), np.array([[b]]), np.array([[c]])
+    g = abs(c * b) / a
+    assert abs(_hinf(A[0], Bu, Cy) - g) <= 1e-6 * g
+    assert ipm.verdict(_brl_problem(A, Bu, Cy, 1.05 * g, 0, 0, 0), samples=10)
+    assert not ipm.verdict(_brl_problem(A, Bu, Cy, 0.95 * g, 0, 0, 0), samples=10)
+
+
+def test_bounded_real_polytope_bounds_the_worst_vertex():
+    """A certificate at gamma implies ||G_alpha||_inf < gamma for every alpha: never certified below
+    the brute-force worst case over the simplex; certified comfortably above it."""
+    rng = np.random.default_rng(6)
+    c = synth.small_config(2, 2, 1, 1, 1)
+    A = synth.vertex_matrices(c, rng)
+    Bu, Cy = rng.normal(size=(2, 1)), rng.normal(size=(1, 2))
+    worst = max(_hinf(t * A[0] + (1 - t) * A[1], Bu, Cy) for t in np.linspace(0, 1, 11))
+    assert not ipm.verdict(_brl_problem(A, Bu, Cy, 0.97 * worst, 1, 1, 1), samples=50)
+    assert ipm.verdict(_brl_problem(A, Bu, Cy, 1.5 * worst, 1, 1, 1), samples=50)
+
+
+def test_non_square_polynomial_identity_and_adjoint():
+    n, N, l, dp, d1, d2 = 2, 3, 2, 1, 1, 1
+    rng = np.random.default_rng(8)
+    f = _f(l)
+    terms = [(rng.normal(size=(f(1), N, n)), 1, rng.normal(size=(f(1), n, N)), 1),
+             (rng.normal(size=(f(2), N, n)), 2, rng.normal(size=(f(0), n, N)), 0)]
+    P = sdp.build_problem_general(terms, n, l, dp, d1, d2)
+    assert P.bn == N
+    y = rng.normal(size=P.K)
+    out = sdp.apply_vmap(P, y)
+    assert out.shape == (P.nblocks, N, N)
+    assert not np.any(out[:P.L, n:, :]) and not np.any(out[:P.L, :, n:])   # P-blocks: top-left only
+    Wp, Wm = enumerate_W(l, dp), enumerate_W(l, dp + 2 + d2)
+    V = [sdp.vmap(P, y, h) for h in range(P.L0)]
+    al = rng.uniform(0.2, 1.5, size=l)
+    mono = lambda e: math.prod(a ** k for a, k in zip(al, e))
+    Pa = sum(mono(h) * V[i] for i, h in enumerate(Wp))
+    lhs = sum(mono(g) * out[P.L + m] for m, g in enumerate(Wm))
+    S = sum(polya.evaluate(At, l, a, al) @ Pa @ polya.evaluate(Bt, l, b, al) for At, a, Bt, b in terms)
+    assert np.abs(lhs + sum(al) ** d2 * (S + S.T)).max() <= 1e-12 * np.abs(lhs).max()
+    X, W = synth.spd_blocks(N, P.nblocks, rng)
+    lhs = sum(np.sum(out[b] * X[b]) for b in range(P.nblocks))
+    assert abs(lhs - y @ sdp.adjoint_trace(P, X)) <= 1e-12 * abs(lhs)
+    assert np.abs(sdp.schur_structured(P, X, W) - sdp.schur_literal(P, X, W)).max() <= 1e-12 * np.abs(
+        sdp.schur_literal(P, X, W)).max()
