@@ -105,6 +105,8 @@ typedef struct {
                            buffer holds nranks*reduce_count doubles (zero padding at the end) */
   int64_t npairs_local; /* pair tiles held by this rank (PAIR_TILES layout: npairs_local tiles);
                            = pair1 - pair0 except with SHARD_CYCLIC (pairs not contiguous) */
+  int64_t block_n;      /* order of every block of X, Z, C, B^T(y): cfg->n, or the generalised
+                           form's N (polya_setup_general with nlmi > n) */
 } polya_dims;
 
 /* Output layouts of the Schur complement G (symmetric K x K):
@@ -129,20 +131,25 @@ polya_status polya_setup(const polya_config* cfg, const double* A_host, polya_ct
 
 /* The generalised form (reading R18):
  *     P(alpha) > 0,   sum_i (At_i(alpha) P(alpha) Bt_i(alpha) + Bt_i(alpha)^T P(alpha) At_i(alpha)^T) < 0,
- * square case (At_i, Bt_i n x n), R_i = 0.  Term i has At_i of degree deg_a[i] and Bt_i of degree
+ * nlmi = N: the order of the LMI (0 or cfg->n: the square case, At_i, Bt_i n x n; N > n: At_i is
+ * N x n, Bt_i n x N, R N x N -- e.g. the bounded-real lemma, N = n + m -- and every block of the SDP
+ * is N x N, a P-block's n x n LMI in its top-left corner with C = -I on the rest; reading R19:
+ * X, Z and B^T(y) stacks are then double[nblocks][N][N], see polya_dims.block_n).
+ * Term i has At_i of degree deg_a[i] and Bt_i of degree
  * deg_b[i] with deg_a[i] + deg_b[i] = cfg->da for every i (homogenise first; EINVAL otherwise).
- * At: the concatenation over i of double[f(l,deg_a[i])][n][n] (coefficients in W_{deg_a[i]} order),
- * Bt likewise; both copied.  The continuous-time polya_setup is the case nterms = 1,
+ * At: the concatenation over i of double[f(l,deg_a[i])][N][n] (coefficients in W_{deg_a[i]} order),
+ * Bt of double[f(l,deg_b[i])][n][N]; both copied.  The continuous-time polya_setup is the case nterms = 1,
  * (A^T, 1, I, 0); discrete time A^T P A - P < 0 is [(A^T/2, 1, A, 1), (-I/2 per vertex, 1, I per
  * vertex, 1)].  R_host (nullable = 0): the constant term sum_i R_i(alpha), homogeneous of degree
- * dp + da, double[f(l,dp+da)][n][n] symmetric, W_{dp+da} order; it becomes C on the Lyapunov blocks,
+ * dp + da, double[f(l,dp+da)][N][N] symmetric, W_{dp+da} order; it becomes C on the Lyapunov blocks,
  * C_{L+m} = sum_rho multinomial(d2; gamma_m - rho) R_rho (the dual constraint B^T(y) - C >= 0 is then
  * the LMI with "+ R < 0").  Lyapunov block gamma of the dual element (h, k) is
  *     -sum_{i,lambda,mu} multinomial(d2; gamma - h - lambda - mu) (At_{i,lambda} E_k Bt_{i,mu} + transpose);
  * every other entry point (apply, adjoint, Schur, IPM, solve, verdict, sharding) works unchanged
  * on the resulting context, except polya_get_H (EINVAL: no H table).  Errors as polya_setup. */
-polya_status polya_setup_general(const polya_config* cfg, int32_t nterms, const int32_t* deg_a, const int32_t* deg_b,
-                                 const double* At_host, const double* Bt_host, const double* R_host, polya_ctx** out);
+polya_status polya_setup_general(const polya_config* cfg, int32_t nlmi, int32_t nterms, const int32_t* deg_a,
+                                 const int32_t* deg_b, const double* At_host, const double* Bt_host, const double* R_host,
+                                 polya_ctx** out);
 
 polya_status polya_dims_get(const polya_ctx* ctx, polya_dims* out);
 

@@ -40,7 +40,8 @@ class _Dims(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("L0", "L", "M", "nblocks", "Ntil", "K", "nnz_beta", "nnz_H",
                                               "npairs", "pair0", "pair1", "item0", "item1")] + \
                [("useful_flops_schur", ctypes.c_double), ("tiles_bytes", ctypes.c_int64), ("b0", ctypes.c_int64),
-                ("b1", ctypes.c_int64), ("reduce_count", ctypes.c_int64), ("npairs_local", ctypes.c_int64)]
+                ("b1", ctypes.c_int64), ("reduce_count", ctypes.c_int64), ("npairs_local", ctypes.c_int64),
+                ("block_n", ctypes.c_int64)]
 
 
 class _IpmState(ctypes.Structure):
@@ -78,7 +79,7 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
-    L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
+    L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, i32, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
     L.polya_factor_solve_loopback.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), vp, vp]
     L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
     L.polya_plan.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Dims)]
@@ -233,7 +234,8 @@ class Polya:
             Bt = np.ascontiguousarray(np.concatenate([np.asarray(t[2], dtype=np.float64).reshape(-1) for t in terms]))
             cp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
             Rh = None if R is None else np.ascontiguousarray(np.asarray(R, dtype=np.float64))
-            st = L.polya_setup_general(ctypes.byref(cfg), len(terms), cp(dega), cp(degb), cp(At), cp(Bt),
+            nlmi = int(np.asarray(terms[0][0]).shape[1])   # At_0 is N x n
+            st = L.polya_setup_general(ctypes.byref(cfg), nlmi, len(terms), cp(dega), cp(degb), cp(At), cp(Bt),
                                        None if Rh is None else cp(Rh), ctypes.byref(h))
             what = "polya_setup_general"
         if st != 0:
@@ -246,6 +248,7 @@ class Polya:
         self.dims = {k: getattr(d, k) for k, _ in _Dims._fields_}
         for k in ("L0", "L", "M", "nblocks", "Ntil", "K"):
             setattr(self, k, int(self.dims[k]))
+        self.bn = int(self.dims["block_n"])   # order of every block (n, or the generalised form's N)
 
     def _check(self, st, what):
         if st != 0:
@@ -283,8 +286,8 @@ class Polya:
     def apply(self, y, out=None, stream=None):
         import torch
         if out is None:
-            out = torch.empty((self.nblocks, self.n, self.n), dtype=torch.float64, device=y.device)
-        self._check(lib().polya_apply(self._h, _dev_ptr(y, self.K, "y"), _dev_ptr(out, self.nblocks * self.n ** 2, "out"),
+            out = torch.empty((self.nblocks, self.bn, self.bn), dtype=torch.float64, device=y.device)
+        self._check(lib().polya_apply(self._h, _dev_ptr(y, self.K, "y"), _dev_ptr(out, self.nblocks * self.bn ** 2, "out"),
                                       _stream_ptr(stream)), "polya_apply")
         return out
 
@@ -292,7 +295,7 @@ class Polya:
         import torch
         if out is None:
             out = torch.empty(self.K, dtype=torch.float64, device=X.device)
-        self._check(lib().polya_adjoint(self._h, _dev_ptr(X, self.nblocks * self.n ** 2, "X"), _dev_ptr(out, self.K, "y"),
+        self._check(lib().polya_adjoint(self._h, _dev_ptr(X, self.nblocks * self.bn ** 2, "X"), _dev_ptr(out, self.K, "y"),
                                         _stream_ptr(stream)), "polya_adjoint")
         return out
 
@@ -306,13 +309,13 @@ class Polya:
             else:
                 npl = self.dims["npairs_local"]
                 G = torch.zeros((npl, self.Ntil, self.Ntil), dtype=torch.float64, device=X.device)
-        nbn = self.nblocks * self.n ** 2
+        nbn = self.nblocks * self.bn ** 2
         self._check(lib().polya_schur(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"), _dev_ptr(G, None, "G"),
                                       layout, _stream_ptr(stream)), "polya_schur")
         return G
 
     def schur_prepare(self, X, Zinv, stream=None):
-        nbn = self.nblocks * self.n ** 2
+        nbn = self.nblocks * self.bn ** 2
         self._check(lib().polya_schur_prepare(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"),
                                               _stream_ptr(stream)), "polya_schur_prepare")
 
@@ -349,7 +352,7 @@ class Polya:
     def ipm_solve(self, X=None, Z=None, y=None, eps=1e-8, tol=1e-8, maxit=60, init=True, stream=None):
         """polya_ipm_solve: Algorithm 2 to its stopping rule (state on the device, updated in place)."""
         import torch
-        nbn = (self.nblocks, self.n, self.n)
+        nbn = (self.nblocks, self.bn, self.bn)
         X = torch.empty(nbn, dtype=torch.float64, device="cuda") if X is None else X
         Z = torch.empty(nbn, dtype=torch.float64, device="cuda") if Z is None else Z
         y = torch.empty(self.K, dtype=torch.float64, device="cuda") if y is None else y

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(128) k_bgemm(int n, const double* __restrict__
 }
 
 // out = a X + b Y (+ c * C_b on the P-blocks' diagonals when cdiag != nullptr), elementwise
-__global__ void k_axpby(int64_t total, int n, int64_t Lp, double a, const double* __restrict__ X, double b,
+__global__ void k_axpby(int64_t total, int n, int nbas, int64_t Lp, double a, const double* __restrict__ X, double b,
                         const double* __restrict__ Y, double* __restrict__ out, const double* __restrict__ cdiag,
                         double cs, const double* __restrict__ cL) {
   const int64_t nn = (int64_t)n * n;
@@ -98,7 +98,7 @@ __global__ void k_axpby(int64_t total, int n, int64_t Lp, double a, const double
     double v = a * X[e] + (Y ? b * Y[e] : 0.0);
     if (cdiag) {   // C: c_j I on the P-blocks, the dense C_L (generalised form's R) on the Lyapunov blocks
       const int64_t blk = e / nn, r = e - blk * nn;
-      if (blk < Lp && (r / n) == (r % n)) v += cs * cdiag[blk];
+      if (blk < Lp && (r / n) == (r % n)) v += cs * ((r / n) < nbas ? cdiag[blk] : -1.0);   // -I: padding (R19)
       if (blk >= Lp && cL) v += cs * cL[e - Lp * nn];
     }
     out[e] = v;
@@ -205,7 +205,7 @@ __global__ void k_block_tmax(int n, const double* __restrict__ S, const double* 
 }
 
 // partial sums: out[0] = sum_b tr(Z_b X_b) = sum Z.*X^T, out[1] = sum_{j<L} c_j tr(X_j), out[2] = sum y
-__global__ void k_scalars(int64_t total, int n, int64_t Lp, const double* __restrict__ Z, const double* __restrict__ X,
+__global__ void k_scalars(int64_t total, int n, int nbas, int64_t Lp, const double* __restrict__ Z, const double* __restrict__ X,
                           const double* __restrict__ c, const double* __restrict__ y, int64_t K,
                           double* __restrict__ part, const double* __restrict__ cL) {
   __shared__ double red[3][256];
@@ -215,7 +215,7 @@ __global__ void k_scalars(int64_t total, int n, int64_t Lp, const double* __rest
     const int64_t blk = e / nn, r = e - blk * nn;
     const int i = (int)(r / n), j = (int)(r % n);
     s0 += Z[e] * X[blk * nn + (int64_t)j * n + i];
-    if (blk < Lp && i == j) s1 += c[blk] * X[e];
+    if (blk < Lp && i == j) s1 += (i < nbas ? c[blk] : -1.0) * X[e];
     if (blk >= Lp && cL) s1 += cL[e - Lp * nn] * X[blk * nn + (int64_t)j * n + i];   // tr(C_L X)
   }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x) s2 += y[e];
@@ -319,7 +319,7 @@ __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__
 // The same check for the generalised form (reading R18): -sum_i (At_i P Bt_i + transpose)(alpha) > 0.
 // Shared memory: P(alpha), the accumulator S = sum_i At_i P Bt_i, monomials; global scratch per point:
 // At_i(alpha), Bt_i(alpha), P Bt_i(alpha).
-__global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, int roff, const int32_t* __restrict__ Wp,
+__global__ void k_grid_gen(int n, int nbas, int l, int L0, int nterms, int ncoef, int roff, const int32_t* __restrict__ Wp,
                            const int32_t* __restrict__ cexp, const int32_t* __restrict__ aoff,
                            const int32_t* __restrict__ boff, const double* __restrict__ coef,
                            const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
@@ -389,7 +389,13 @@ __global__ void k_grid_gen(int n, int l, int L0, int nterms, int ncoef, int roff
   __syncthreads();
   const bool lmi = smem_chol(S, n);
   __syncthreads();
-  const bool pos = smem_chol(P, n);
+  if (nbas < n) {   // P(alpha) is the top-left nbas x nbas corner (R19): compact it for its test
+    for (int e = threadIdx.x; e < nbas * nbas; e += blockDim.x) Ae[e] = P[(e / nbas) * n + (e % nbas)];
+    __syncthreads();
+    for (int e = threadIdx.x; e < nbas * nbas; e += blockDim.x) P[e] = Ae[e];
+    __syncthreads();
+  }
+  const bool pos = smem_chol(P, nbas);
   if (threadIdx.x == 0 && !(lmi && pos)) atomicAdd(nfail, 1);
 }
 
@@ -539,7 +545,7 @@ void bgemm(Ctx& c, const double* A, int ta, const double* B, int tb, double* C, 
 void axpby(Ctx& c, double a, const double* X, double b, const double* Y, double* out, const double* cdiag, double cs,
            cudaStream_t s) {
   const int64_t total = c.nb * c.n * c.n;
-  k_axpby<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(total, (int)c.n, c.L, a, X, b, Y, out,
+  k_axpby<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, s>>>(total, (int)c.n, (int)c.nbas, c.L, a, X, b, Y, out,
                                                                                  cdiag, cs, c.d_CL);
   ++c.launches;
   CK(cudaGetLastError());
@@ -926,7 +932,7 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     vaxpby(c, 1.0, y, td, w->dy1, y, s);
     // step 4 scalars
     const int64_t total = c.nb * c.n * c.n;
-    k_scalars<<<kScalarBlocks, 256, 0, s>>>(total, (int)c.n, c.L, Z, X, w->dc, y, c.K, w->part, c.d_CL);
+    k_scalars<<<kScalarBlocks, 256, 0, s>>>(total, (int)c.n, (int)c.nbas, c.L, Z, X, w->dc, y, c.K, w->part, c.d_CL);
     ++c.launches;
     CK(cudaGetLastError());
     std::vector<double> part(kScalarBlocks * 3);
@@ -1160,7 +1166,7 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
       const int32_t* dexp = dgen;
       const int32_t* dao = dgen + c.coef_exp.size();
       CK(cudaFuncSetAttribute(k_grid_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      k_grid_gen<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, nt, (int)c.ncoef, (int)c.r_off, dWp, dexp, dao,
+      k_grid_gen<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.nbas, (int)c.l, (int)c.L0, nt, (int)c.ncoef, (int)c.r_off, dWp, dexp, dao,
                                                  dao + nt, c.d_coef, c.arena, c.mstride, (int)c.np, c.id_Vy, dpts,
                                                  dscr, dfail);
     } else {

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(128) k_gemm(double* __restrict__ arena, int64_
     }
 }
 
-// V_h(y) (Eq. 30) for every h into the arena.
+// V_h(y) (Eq. 30) for every h into the arena (n = order of P; zero beyond it, reading R19).
 __global__ void k_vmap(double* __restrict__ arena, int64_t ms, int np, int n, int64_t Ntil,
                        const double* __restrict__ y, int64_t id_Vy) {
   const int h = blockIdx.x;
@@ -190,8 +190,9 @@ __global__ void k_vmap(double* __restrict__ arena, int64_t ms, int np, int n, in
 }
 
 // B^T(y) blocks: P-block j: sum_h beta_{h,j} V_h(y); Lyapunov m: -(S_m + S_m^T), S_m = sum_h V_h H_{h,m}.
-__global__ void k_apply_out(const double* __restrict__ arena, int64_t ms, int np, int n, int64_t Ntil, int64_t L,
-                            const double* __restrict__ y, const int32_t* __restrict__ bP_beg,
+// (n = block order, nbas = order of P: a P-block's LMI is its top-left nbas x nbas corner, R19)
+__global__ void k_apply_out(const double* __restrict__ arena, int64_t ms, int np, int n, int nbas, int64_t Ntil,
+                            int64_t L, const double* __restrict__ y, const int32_t* __restrict__ bP_beg,
                             const int32_t* __restrict__ bP_h, const double* __restrict__ bP_w, int64_t id_S,
                             double* __restrict__ out) {
   const int64_t b = blockIdx.x;
@@ -200,9 +201,11 @@ __global__ void k_apply_out(const double* __restrict__ arena, int64_t ms, int np
     const int e0 = bP_beg[b], e1 = bP_beg[b + 1];
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
       const int i = e / n, j = e - i * n;
-      const int64_t k = svec_idx(min(i, j), max(i, j), n);
       double v = 0.0;
-      for (int q = e0; q < e1; ++q) v += bP_w[q] * y[(int64_t)bP_h[q] * Ntil + k];
+      if (i < nbas && j < nbas) {
+        const int64_t k = svec_idx(min(i, j), max(i, j), nbas);
+        for (int q = e0; q < e1; ++q) v += bP_w[q] * y[(int64_t)bP_h[q] * Ntil + k];
+      }
       o[e] = v;
     }
   } else {
@@ -291,13 +294,13 @@ cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, in
 }
 
 cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s) {
-  k_vmap<<<(unsigned)c.L0, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.Ntil, y, c.id_Vy);
+  k_vmap<<<(unsigned)c.L0, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.nbas, c.Ntil, y, c.id_Vy);
   ++c.launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s) {
-  k_apply_out<<<(unsigned)c.nb, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.Ntil, c.L, y, c.d_bP_beg,
+  k_apply_out<<<(unsigned)c.nb, 256, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, (int)c.nbas, c.Ntil, c.L, y, c.d_bP_beg,
                                               c.d_bP_h, c.d_bP_w, c.id_S, out);
   ++c.launches;
   return cudaGetLastError();
@@ -305,7 +308,7 @@ cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t 
 
 cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s) {
   dim3 grid((unsigned)((c.Ntil + 127) / 128), (unsigned)c.L0);
-  k_adjoint_reduce<<<grid, 128, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.n, c.Ntil, c.d_hP_beg, c.d_hP_j,
+  k_adjoint_reduce<<<grid, 128, 0, s>>>(c.arena, c.mstride, (int)c.np, (int)c.nbas, c.Ntil, c.d_hP_beg, c.d_hP_j,
                                          c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.id_Xt, c.id_T, y);
   ++c.launches;
   return cudaGetLastError();

@@ -113,22 +113,24 @@ struct GenInput {
   int32_t nterms;
   const int32_t *deg_a, *deg_b;
   const double *At, *Bt, *R;
+  int32_t N;   // block order (>= cfg.n; N > n: At_i is N x n, Bt_i n x N, R N x N)
 };
 
 void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi = nullptr) {
   const polya_config& g = c.cfg;
-  c.n = g.n;
+  c.nbas = g.n;
+  c.n = (gi && gi->N > g.n) ? gi->N : g.n;
   c.l = g.l;
   c.L0 = card(g.l, g.dp);
   c.L = card(g.l, (int64_t)g.dp + g.d1);
   c.M = card(g.l, (int64_t)g.dp + g.da + g.d2);
   c.nA = card(g.l, g.da);
   c.nb = add_chk(c.L, c.M);
-  c.Ntil = mul_chk(c.n, c.n + 1) / 2;
+  c.Ntil = mul_chk(c.nbas, c.nbas + 1) / 2;
   c.K = mul_chk(c.L0, c.Ntil);
   (void)mul_chk(c.K, c.K);  // K*K must be representable (FULL layout indexing)
   c.np = (c.n + kChunk - 1) / kChunk * kChunk;
-  c.r = c.np / kChunk;
+  c.r = (c.nbas + kChunk - 1) / kChunk;   // index chunks of the basis (K4 work items)
   c.ncls = c.r * (c.r + 1) / 2;
   c.mstride = mul_chk(c.np, c.np);
   if (c.mstride >= (int64_t)1 << 31) throw Fail{POLYA_EOVERFLOW, "n too large for 32-bit tile offsets"};
@@ -175,6 +177,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
   std::vector<double> w(c.nA);
   // generalised form: term t = (A_t, B_t) as weighted sums of coefficient matrices (src, weight)
   std::vector<std::vector<std::pair<int32_t, double>>> tA, tB;
+  std::vector<double> coefN;   // generalised form: the terms' coefficients padded to N x N
   c.gen = gi != nullptr;
   if (c.gen) {
     // coefficient layout: pair i's At coefficients (W_{a_i} order), then its Bt coefficients
@@ -195,26 +198,31 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     }
     c.r_off = off;
     c.r_cnt = 0;
-    // canonical coefficient ids: bitwise-equal coefficient matrices (an identity repeated per vertex,
-    // say) share the smallest id, so that the merges below see them as one matrix
-    std::vector<int32_t> canon(off);
+    // every coefficient as an N x N matrix (At: N x n in the left columns, Bt: n x N in the top rows,
+    // zero elsewhere -- reading R19), and canonical ids: bitwise-equal coefficient matrices (an
+    // identity repeated per vertex, say) share the smallest id, so the merges below see one matrix
+    const int64_t NB = c.n, nbs = c.nbas, NN = NB * NB;
+    coefN.assign((size_t)off * NN, 0.0);
     {
-      const int64_t nn = (int64_t)g.n * g.n;
-      std::vector<const double*> cptr(off);
       int64_t ua = 0, ub = 0;
       for (int32_t i = 0; i < gi->nterms; ++i) {
-        for (int64_t q = c.gp_aoff[i]; q < c.gp_boff[i]; ++q) cptr[q] = gi->At + (ua++) * nn;
+        for (int64_t q = c.gp_aoff[i]; q < c.gp_boff[i]; ++q, ++ua)
+          for (int64_t r = 0; r < NB; ++r)
+            for (int64_t col = 0; col < nbs; ++col) coefN[q * NN + r * NB + col] = gi->At[(ua * NB + r) * nbs + col];
         const int64_t bend = i + 1 < gi->nterms ? c.gp_aoff[i + 1] : off;
-        for (int64_t q = c.gp_boff[i]; q < bend; ++q) cptr[q] = gi->Bt + (ub++) * nn;
+        for (int64_t q = c.gp_boff[i]; q < bend; ++q, ++ub)
+          for (int64_t r = 0; r < nbs; ++r)
+            for (int64_t col = 0; col < NB; ++col) coefN[q * NN + r * NB + col] = gi->Bt[(ub * nbs + r) * NB + col];
       }
-      for (int64_t q = 0; q < off; ++q) {
-        canon[q] = (int32_t)q;
-        for (int64_t r = 0; r < q; ++r)
-          if (canon[r] == r && std::memcmp(cptr[q], cptr[r], (size_t)nn * sizeof(double)) == 0) {
-            canon[q] = (int32_t)r;
-            break;
-          }
-      }
+    }
+    std::vector<int32_t> canon(off);
+    for (int64_t q = 0; q < off; ++q) {
+      canon[q] = (int32_t)q;
+      for (int64_t r = 0; r < q; ++r)
+        if (canon[r] == r && std::memcmp(&coefN[q * NN], &coefN[r * NN], (size_t)NN * sizeof(double)) == 0) {
+          canon[q] = (int32_t)r;
+          break;
+        }
     }
     if (gi->R) {   // the constant term: coefficients in W_{dp+da} order (verdict) and C on Lyapunov blocks
       std::vector<int32_t> Wr;
@@ -392,7 +400,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
   }
   c.pair_item_global.assign(c.npairs + 1, 0);
   std::vector<double> cost_prefix(c.npairs + 1, 0.0);
-  double n4 = (double)c.n * c.n * c.n * c.n;
+  double n4 = (double)c.nbas * c.nbas * c.nbas * c.nbas;
   c.useful_flops_total = 0;
   for (int64_t p = 0; p < c.npairs; ++p) {
     c.pair_item_global[p + 1] = add_chk(c.pair_item_global[p], pItems[p]);
@@ -716,18 +724,8 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
 
   // ---- H on the device (kernel K1) ----------------------------------------------------------------
   if (c.gen) {   // A_t, A_t^T, B_t as weighted coefficient sums (k_wsum)
-    std::vector<double> coef;
     const int64_t nn = c.n * c.n;
-    coef.reserve(c.ncoef * nn);
-    int64_t ua = 0, ub = 0;   // running offsets into the caller's At / Bt concatenations
-    for (size_t i = 0; i < c.gp_da.size(); ++i) {
-      const int64_t na = c.gp_boff[i] - c.gp_aoff[i];
-      const int64_t nbm = (i + 1 < c.gp_da.size() ? c.gp_aoff[i + 1] : c.r_off) - c.gp_boff[i];
-      coef.insert(coef.end(), gi->At + ua * nn, gi->At + (ua + na) * nn);
-      coef.insert(coef.end(), gi->Bt + ub * nn, gi->Bt + (ub + nbm) * nn);
-      ua += na;
-      ub += nbm;
-    }
+    std::vector<double> coef(coefN);   // the padded N x N coefficients of the terms, then R's
     std::vector<WsumItem> wi;
     std::vector<WsumTerm> wt;
     auto add = [&](int64_t dst, const std::vector<std::pair<int32_t, double>>& sum, int trans) {
@@ -818,9 +816,9 @@ extern "C" polya_status polya_setup(const polya_config* cfg, const double* A_hos
   return POLYA_OK;
 }
 
-extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nterms, const int32_t* deg_a,
-                                           const int32_t* deg_b, const double* At, const double* Bt, const double* R,
-                                           polya_ctx** out) {
+extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nlmi, int32_t nterms,
+                                           const int32_t* deg_a, const int32_t* deg_b, const double* At,
+                                           const double* Bt, const double* R, polya_ctx** out) {
   if (!out) return POLYA_EINVAL;
   *out = nullptr;
   if (!cfg || nterms < 1 || !deg_a || !deg_b || !At || !Bt) return POLYA_EINVAL;
@@ -828,12 +826,13 @@ extern "C" polya_status polya_setup_general(const polya_config* cfg, int32_t nte
   if (g.n < 1 || g.l < 1 || g.dp < 0 || g.da < 0 || g.d1 < 0 || g.d2 < 0 || !(g.delta > 0) || g.nranks < 1 ||
       g.rank < 0 || g.rank >= g.nranks || (g.shard < POLYA_SHARD_TILES || g.shard > POLYA_SHARD_CYCLIC))
     return POLYA_EINVAL;
+  if (nlmi != 0 && nlmi < g.n) return POLYA_EINVAL;
   for (int32_t i = 0; i < nterms; ++i)   // every term homogeneous of the one total degree cfg->da (R18)
     if (deg_a[i] < 0 || deg_b[i] < 0 || deg_a[i] + deg_b[i] != g.da) return POLYA_EINVAL;
   polya_ctx* ctx = new (std::nothrow) polya_ctx();
   if (!ctx) return POLYA_ENOMEM;
   ctx->c.cfg = g;
-  const GenInput gi{nterms, deg_a, deg_b, At, Bt, R};
+  const GenInput gi{nterms, deg_a, deg_b, At, Bt, R, nlmi};
   try {
     if (cudaGetDevice(&ctx->c.device) != cudaSuccess) throw Fail{POLYA_ECUDA, "no CUDA device"};
     build(ctx->c, nullptr, true, &gi);
@@ -863,6 +862,7 @@ static void fill_dims(const Ctx& c, polya_dims* o) {
   const int64_t tot = c.npairs * c.Ntil * c.Ntil;
   o->reduce_count = c.cfg.shard == POLYA_SHARD_BLOCKS ? (tot + c.cfg.nranks - 1) / c.cfg.nranks : 0;
   o->npairs_local = c.npairs_local;
+  o->block_n = c.n;
 }
 
 extern "C" polya_status polya_plan(const polya_config* cfg, polya_dims* out) {

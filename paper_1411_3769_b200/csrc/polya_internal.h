@@ -51,6 +51,8 @@ struct Ctx {
   polya_config cfg{};
   int device = 0;
   int64_t n = 0, l = 0, L0 = 0, L = 0, M = 0, nb = 0, Ntil = 0, K = 0, nA = 0;
+  int64_t nbas = 0;      // order of P (the basis E_k); n is the order of every block (= nbas, or the
+                         // generalised form's N > nbas, reading R19)
   int64_t np = 0;        // padded matrix dimension (multiple of kChunk)
   int64_t r = 0;         // number of index chunks = np / kChunk
   int64_t ncls = 0;      // r (r+1) / 2 unordered chunk classes

@@ -653,7 +653,7 @@ cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, 
   per_sm = std::max(per_sm, 1);
   const int64_t want = std::min<int64_t>((int64_t)sms * per_sm, i1 - i0);
   SchurArgs a;
-  a.arena = c.arena; a.ms = c.mstride; a.ms32 = (unsigned)c.mstride; a.np = (int)c.np; a.n = (int)c.n; a.ncls = (int)c.ncls;
+  a.arena = c.arena; a.ms = c.mstride; a.ms32 = (unsigned)c.mstride; a.np = (int)c.np; a.n = (int)c.nbas; a.ncls = (int)c.ncls;
   a.npl = (int)c.npairs_local;
   a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
   a.pair_kbeg = c.st.pair_kbeg; a.pair_item = c.st.pair_item; a.kdesc = c.st.kdesc;

@@ -216,3 +216,87 @@ def test_discrete_time_terms_merge_to_l_plus_one(pb):
     assert _rel(ctx.apply(_dev(y)).cpu().numpy(), osdp.apply_vmap(P, y)) <= TOL
     assert _rel(ctx.schur(_dev(X), _dev(W)).cpu().numpy(), osdp.schur_structured(P, X, W)) <= TOL
     ctx.close()
+
+
+# ---- non-square form (reading R19): N x N blocks, the bounded-real lemma ------------------------------
+
+def _brl(pb, A, Bu, Cy, gamma, dp):
+    """Terms and R for the GPU side: R0 homogenised to degree dp + 1 by the library's own
+    polya_homogenize (the oracle side uses oracle.polya.homogenize)."""
+    terms, R0 = synth.bounded_real_terms(A, Bu, Cy, gamma)
+    l = A.shape[0]
+    _, R = pb.homogenize({tuple([dp + 1] + [0] * (l - 1)): 0.0 * R0, tuple([0] * l): R0}, l)
+    return terms, R
+
+
+def _brl_oracle(A, Bu, Cy, gamma, dp, d1, d2):
+    from oracle import polya as opolya
+    terms, R0 = synth.bounded_real_terms(A, Bu, Cy, gamma)
+    l, n = A.shape[0], A.shape[1]
+    _, R = opolya.homogenize({tuple([dp + 1] + [0] * (l - 1)): 0.0 * R0, tuple([0] * l): R0}, l)
+    return osdp.build_problem_general(terms, n, l, dp, d1, d2, R=R)
+
+
+@pytest.mark.parametrize("n,N,l,dp,d1,d2", [(3, 5, 2, 1, 1, 1), (9, 12, 2, 1, 1, 1), (4, 7, 3, 1, 1, 0)])
+def test_non_square_parity(pb, n, N, l, dp, d1, d2):
+    rng = np.random.default_rng(21)
+    f = lambda d: len(enumerate_W(l, d))
+    terms = [(rng.normal(size=(f(1), N, n)), 1, rng.normal(size=(f(1), n, N)), 1),
+             (rng.normal(size=(f(2), N, n)), 2, rng.normal(size=(f(0), n, N)), 0)]
+    Rr = rng.normal(size=(f(dp + 2), N, N))
+    Rr = Rr + Rr.transpose(0, 2, 1)
+    P = osdp.build_problem_general(terms, n, l, dp, d1, d2, R=Rr)
+    ctx = pb.Polya.general(terms, n, l, dp, d1, d2, R=Rr)
+    assert ctx.bn == N and (ctx.K, ctx.nblocks) == (P.K, P.nblocks)
+    y = rng.normal(size=P.K)
+    assert _rel(ctx.apply(_dev(y)).cpu().numpy(), osdp.apply_vmap(P, y)) <= TOL
+    X, W = synth.spd_blocks(N, P.nblocks, rng)
+    R = rng.normal(size=X.shape)
+    assert _rel(ctx.adjoint(_dev(R)).cpu().numpy(), osdp.adjoint_trace(P, R)) <= TOL
+    G = ctx.schur(_dev(X), _dev(W)).cpu().numpy()
+    assert _rel(G, osdp.schur_structured(P, X, W)) <= TOL
+    ctx.close()
+
+
+@pytest.mark.parametrize("a,b,c", [(1.0, 1.0, 1.0), (0.5, 1.0, 2.0)])
+def test_bounded_real_scalar_closed_form(pb, a, b, c):
+    from paper_1411_3769_b200 import robust
+    A, Bu, Cy = np.array([[[-a]]]), np.array([[b]]), np.array([[c]])
+    g = abs(c * b) / a
+    for fac, want in ((1.05, True), (0.95, False)):
+        terms, R = _brl(pb, A, Bu, Cy, fac * g, 0)
+        r = robust.certify(None, 1, 1, 0, 0, 0, terms=terms, R=R, samples=10)
+        assert r["certified"] == want, (fac, r)
+
+
+def test_bounded_real_polytope_and_ipm_parity(pb):
+    from paper_1411_3769_b200 import robust
+    from oracle import ipm as oipm
+    rng = np.random.default_rng(6)
+    c = synth.small_config(2, 2, 1, 1, 1)
+    A = synth.vertex_matrices(c, rng)
+    Bu, Cy = rng.normal(size=(2, 1)), rng.normal(size=(1, 2))
+    w = np.concatenate([[0.0], np.logspace(-3, 3, 2001)])
+    hinf = lambda M: max(np.linalg.svd(Cy @ np.linalg.solve(1j * x * np.eye(2) - M, Bu), compute_uv=False)[0] for x in w)
+    worst = max(hinf(t * A[0] + (1 - t) * A[1]) for t in np.linspace(0, 1, 11))
+    for fac, want in ((1.5, True), (0.97, False)):
+        terms, R = _brl(pb, A, Bu, Cy, fac * worst, 1)
+        r = robust.certify(None, 2, 2, 1, 1, 1, terms=terms, R=R, samples=50)
+        assert r["certified"] == want, (fac, r)
+    # three predictor-corrector steps against the oracle's
+    terms, R = _brl(pb, A, Bu, Cy, 1.5 * worst, 1)
+    P = _brl_oracle(A, Bu, Cy, 1.5 * worst, 1, 1, 1)
+    ctx = pb.Polya.general(terms, 2, 2, 1, 1, 1, R=R)
+    X, Z, y, mu = oipm.initial_state(P)
+    Xd, Zd, yd = (torch.from_numpy(v.copy()).cuda() for v in (X, Z, y))
+    mud = mu
+    for it in range(3):
+        X, Z, y, st = oipm.ipm_step(P, X, Z, y, mu)
+        mu = st["mu"]
+        s = ctx.ipm_step(Xd, Zd, yd, mud, it)
+        mud = s["mu"]
+        assert _rel(Xd.cpu().numpy(), X) <= 1e-8 and _rel(Zd.cpu().numpy(), Z) <= 1e-8
+        assert _rel(yd.cpu().numpy(), y) <= 1e-8, it
+        for k in ("tp", "td", "mu", "phi", "psi"):
+            assert abs(s[k] - st[k]) <= 1e-8 * max(1.0, abs(st[k])), (it, k)
+    ctx.close()
