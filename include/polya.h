@@ -207,13 +207,17 @@ polya_status polya_schur_assemble(polya_ctx* ctx, double* G_dev, int layout, int
                                   void* stream);
 
 /* One predictor-corrector iteration of Algorithm 2 with the
- * readings R3-R6, on a single rank (nranks must be 1).  State lives on the device:
- * X, Z: double[nblocks][n][n] (symmetric PD), y: double[K]; updated in place.
+ * readings R3-R6.  nranks must be 1, or the context SHARD_CYCLIC: then every rank calls it
+ * (collective) with identical replicated X, Z, y, assembles its pair tiles and the K x K
+ * factorisation and solves run distributed (NCCL, polya_nccl_init first); the
+ * ranks' X, Z, y stay bitwise identical.  State lives on the device:
+ * X, Z: double[nblocks][block_n][block_n] (symmetric PD), y: double[K]; updated in place.
  * mu is the barrier parameter of the previous step (Eq. mu).
  * The K x K factorisation uses cuSOLVER dpotrf/dpotrs (timed separately in stats); if G is not
  * numerically positive definite it is re-assembled and factorised once more as G + eps I,
  * eps = 1e-12 tr(G) / K, before ENOTPD is returned.
- * Synchronous (returns after the step).  Errors: ENOTPD, ESTEP, ECUDA, ENOMEM.   */
+ * Synchronous (returns after the step).  Errors: EINVAL (several ranks without SHARD_CYCLIC,
+ * block_n > 168), ENOTPD, ESTEP, ENCCL, ECUDA, ENOMEM.   */
 typedef struct { double* X; double* Z; double* y; double mu; int32_t iter; } polya_ipm_state;
 typedef struct {
   double gap;      /* |a^T y - tr(C X)| after the step (stopping rule) */
@@ -280,7 +284,7 @@ polya_status polya_simplex_map(int32_t l, int32_t d, int32_t n, const double* sc
  * result, not an error: res->converged = 1 iff the rule was met with every Z block positive
  * definite (reading R10); otherwise res->status says why (ENOTPD: a block or G lost definiteness,
  * ESTEP: no admissible step, EMAXIT).  The return value reports only misuse / CUDA failures.
- * Single rank (nranks = 1).  Synchronous.                                                   */
+ * Ranks as polya_ipm_step (collective with SHARD_CYCLIC).  Synchronous.                     */
 typedef struct {
   double eps, tol;
   int32_t maxit, init;
