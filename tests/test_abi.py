@@ -71,3 +71,20 @@ def test_setup_general_rejects_mixed_degrees_without_a_gpu():
     terms = [(np.zeros((2, n, n)), 1, np.zeros((2, n, n)), 1), (np.zeros((2, n, n)), 1, np.zeros((1, n, n)), 0)]
     with pytest.raises(pb.PolyaError, match="invalid argument"):
         pb.Polya.general(terms, n, l, 1, 1, 1)
+
+
+def test_setup_general_rejects_lmi_order_below_n_without_a_gpu():
+    """nlmi (the LMI order N) must be 0 (square) or >= n: EINVAL before any device call."""
+    import ctypes
+
+    import numpy as np
+    import paper_1411_3769_b200 as pb
+    L = pb.lib()
+    cfg = pb._Config(3, 2, 1, 1, 1, 1, 1e-3, 0, 1, 0)
+    At = np.zeros((2, 3, 3))
+    Bt = np.zeros((1, 3, 3))
+    da, db = np.array([1], dtype=np.int32), np.array([0], dtype=np.int32)
+    h = ctypes.c_void_p()
+    cp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    st = L.polya_setup_general(ctypes.byref(cfg), 2, 1, cp(da), cp(db), cp(At), cp(Bt), None, ctypes.byref(h))
+    assert st == 1 and not h.value    # POLYA_EINVAL, no context

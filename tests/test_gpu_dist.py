@@ -157,3 +157,29 @@ def test_cyclic_ipm_step_equals_tiled(pb, nccl):
     assert r["converged"]
     ref.close()
     cyc.close()
+
+
+def test_loopback_generalised_form(pb):
+    """The distributed factorisation on a generalised-form problem (discrete time, N = n): same x as
+    a dense solve of the one-rank G."""
+    A = synth.discrete_vertex_matrices(5, 3, 0.8, np.random.default_rng(3))
+    terms = synth.discrete_time_terms(A)
+    ref_ctx = pb.Polya.general(terms, 5, 3, 2, 1, 1)
+    rng = np.random.default_rng(4)
+    X, W = synth.spd_blocks(5, ref_ctx.nblocks, rng)
+    full = ref_ctx.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES).cpu().numpy()
+    L0, N, K = ref_ctx.L0, ref_ctx.Ntil, ref_ctx.K
+    ref_ctx.close()
+    b = rng.normal(size=K)
+    ref = np.linalg.solve(_dense(full, L0, N), b)
+    world = 3
+    ctxs = [pb.Polya.general(terms, 5, 3, 2, 1, 1, rank=r, nranks=world, shard=pb.SHARD_CYCLIC) for r in range(world)]
+    Gs = [c.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES) for c in ctxs]
+    pairs = _pairs(L0)
+    for r in range(world):
+        assert np.array_equal(Gs[r].cpu().numpy(), full[[p for p, (h, _) in enumerate(pairs) if h % world == r]])
+    x = _dev(b)
+    pb.factor_solve_loopback(ctxs, Gs, x)
+    assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
+    for c in ctxs:
+        c.close()
