@@ -304,7 +304,8 @@ polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, const polya_so
  * set-up's A, counts the points alpha = pts_host[p] (double[npts][l], host, points of the simplex)
  * where P(alpha) > 0 or -(A^T P + P A)(alpha) > 0 fails a Cholesky test, into *nfail_out
  * (generalised form: -sum_i (At_i P Bt_i + transpose)(alpha) > 0 instead).
- * One CTA per point on the device; n <= 118.  Synchronous.                                     */
+ * One CTA per point on the device (P(alpha), A(alpha) in a global scratch, each Cholesky test on
+ * a shared-memory copy); block order <= 168 (the IPM's limit).  Synchronous.                    */
 polya_status polya_verdict(polya_ctx* ctx, const double* y_dev, int32_t npts, const double* pts_host,
                            int32_t* nfail_out, void* stream);
 

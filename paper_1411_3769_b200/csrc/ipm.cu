@@ -271,18 +271,28 @@ __global__ void k_identity(int64_t total, int n, double* __restrict__ X, double*
 // Verdict grid check (O8, Theorem 1): at the point alpha = pts[blockIdx.x] of the simplex,
 //   P(alpha) = sum_h alpha^h V_h(y)   (reading R7; V_h in the arena after k_vmap)
 //   A(alpha) = sum_lambda alpha^lambda A_lambda
-// and the test P(alpha) > 0, -(A^T P + P A)(alpha) > 0 by in-shared-memory Cholesky.
-// Shared memory: P(alpha) and A(alpha) (2 n^2 doubles, n <= 118); -(A^T P + P A) is formed in a
-// per-point global scratch and copied over A for its Cholesky test.
+// and the test P(alpha) > 0, -(A^T P + P A)(alpha) > 0 by Cholesky.  P(alpha), A(alpha) and the
+// Lyapunov matrix live in a per-point global scratch (3 n^2); each Cholesky test runs on a copy in
+// shared memory (n^2 doubles: n <= 168, the IPM's limit).
+__device__ bool chol_copy(double* C, const double* src, int n, int ld) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) C[e] = src[(e / n) * ld + (e % n)];
+  __syncthreads();
+  const bool ok = smem_chol(C, n);
+  __syncthreads();
+  return ok;
+}
+
 __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__ Wp, const int32_t* __restrict__ Wa,
                        const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
                        const double* __restrict__ A, const double* __restrict__ pts, double* __restrict__ scratch,
                        int* __restrict__ nfail) {
   extern __shared__ double sm[];
-  double* P = sm;
-  double* Aa = sm + n * n;
-  double* mono = sm + 2 * n * n;   // [L0 + nA]
-  double* M = scratch + (int64_t)blockIdx.x * n * n;
+  double* C = sm;                  // n^2: Cholesky work matrix
+  double* mono = sm + n * n;       // [L0 + nA]
+  const int64_t nn = (int64_t)n * n;
+  double* P = scratch + (int64_t)blockIdx.x * 3 * nn;
+  double* Aa = P + nn;
+  double* M = Aa + nn;
   const double* al = pts + (int64_t)blockIdx.x * l;
   for (int q = threadIdx.x; q < L0 + nA; q += blockDim.x) {
     const int32_t* e = q < L0 ? Wp + (int64_t)q * l : Wa + (int64_t)(q - L0) * l;
@@ -308,28 +318,26 @@ __global__ void k_grid(int n, int l, int L0, int nA, const int32_t* __restrict__
     M[e] = -v;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) Aa[e] = M[e];
-  __syncthreads();
-  const bool lyap = smem_chol(Aa, n);
-  __syncthreads();
-  const bool pos = smem_chol(P, n);
+  const bool lyap = chol_copy(C, M, n, n);
+  const bool pos = chol_copy(C, P, n, n);
   if (threadIdx.x == 0 && !(lyap && pos)) atomicAdd(nfail, 1);
 }
 
-// The same check for the generalised form (reading R18): -sum_i (At_i P Bt_i + transpose)(alpha) > 0.
-// Shared memory: P(alpha), the accumulator S = sum_i At_i P Bt_i, monomials; global scratch per point:
-// At_i(alpha), Bt_i(alpha), P Bt_i(alpha).
+// The same check for the generalised form (reading R18): -sum_i (At_i P Bt_i + transpose)(alpha) - R > 0
+// (n = block order; the positivity test on P's nbas x nbas corner, R19).  Global scratch per point:
+// P(alpha), the accumulator S = sum_i At_i P Bt_i, At_i(alpha), Bt_i(alpha), P Bt_i(alpha).
 __global__ void k_grid_gen(int n, int nbas, int l, int L0, int nterms, int ncoef, int roff, const int32_t* __restrict__ Wp,
                            const int32_t* __restrict__ cexp, const int32_t* __restrict__ aoff,
                            const int32_t* __restrict__ boff, const double* __restrict__ coef,
                            const double* __restrict__ arena, int64_t ms, int np, int64_t id_Vy,
                            const double* __restrict__ pts, double* __restrict__ scratch, int* __restrict__ nfail) {
   extern __shared__ double sm[];
-  double* P = sm;
-  double* S = sm + n * n;
-  double* mono = sm + 2 * n * n;   // [L0 + ncoef]
+  double* C = sm;                  // n^2: Cholesky work matrix
+  double* mono = sm + n * n;       // [L0 + ncoef]
   const int64_t nn = (int64_t)n * n;
-  double* Ae = scratch + (int64_t)blockIdx.x * 3 * nn;
+  double* P = scratch + (int64_t)blockIdx.x * 5 * nn;
+  double* S = P + nn;
+  double* Ae = S + nn;
   double* Be = Ae + nn;
   double* PB = Be + nn;
   const double* al = pts + (int64_t)blockIdx.x * l;
@@ -346,7 +354,9 @@ __global__ void k_grid_gen(int n, int nbas, int l, int L0, int nterms, int ncoef
     double p = 0.0;
     for (int h = 0; h < L0; ++h) p += mono[h] * arena[(id_Vy + h) * ms + (int64_t)i * np + j];
     P[e] = p;
-    S[e] = 0.0;
+    double r = 0.0;   // the constant term R(alpha), coefficients [roff, ncoef)
+    for (int q = roff; q < ncoef; ++q) r += mono[L0 + q] * coef[q * nn + e];
+    S[e] = 0.5 * r;
   }
   __syncthreads();
   for (int t = 0; t < nterms; ++t) {
@@ -374,28 +384,13 @@ __global__ void k_grid_gen(int n, int nbas, int l, int L0, int nterms, int ncoef
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {   // the constant term R(alpha), coefficients [roff, ncoef)
-    double r = 0.0;
-    for (int q = roff; q < ncoef; ++q) r += mono[L0 + q] * coef[q * nn + e];
-    S[e] += 0.5 * r;
-  }
-  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
     Ae[e] = -(S[e] + S[j * n + i]);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[e] = Ae[e];
-  __syncthreads();
-  const bool lmi = smem_chol(S, n);
-  __syncthreads();
-  if (nbas < n) {   // P(alpha) is the top-left nbas x nbas corner (R19): compact it for its test
-    for (int e = threadIdx.x; e < nbas * nbas; e += blockDim.x) Ae[e] = P[(e / nbas) * n + (e % nbas)];
-    __syncthreads();
-    for (int e = threadIdx.x; e < nbas * nbas; e += blockDim.x) P[e] = Ae[e];
-    __syncthreads();
-  }
-  const bool pos = smem_chol(P, nbas);
+  const bool lmi = chol_copy(C, Ae, n, n);
+  const bool pos = chol_copy(C, P, nbas, n);   // P(alpha): the top-left nbas x nbas corner
   if (threadIdx.x == 0 && !(lmi && pos)) atomicAdd(nfail, 1);
 }
 
@@ -1133,13 +1128,15 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
   if (!ctx || !y || npts < 0 || (npts > 0 && !pts_host) || !nfail_out) return POLYA_EINVAL;
   Ctx& c = ctx->c;
   const int64_t nextra = c.gen ? c.ncoef : c.nA;
-  if ((2 * c.n * c.n + c.L0 + nextra) * (int64_t)sizeof(double) > 227 * 1024) {
-    c.last_error = "polya_verdict: n <= 118 (two n x n matrices per point in shared memory)";
+  if ((c.n * c.n + c.L0 + nextra) * (int64_t)sizeof(double) > 227 * 1024) {
+    c.last_error = "polya_verdict: n <= 168 (one n x n Cholesky matrix per point in shared memory)";
     return POLYA_EINVAL;
   }
   cudaStream_t s = (cudaStream_t)stream;
   *nfail_out = 0;
   if (npts == 0) return POLYA_OK;
+  const int64_t per = (c.gen ? 5 : 3) * c.n * c.n;          // scratch doubles per point
+  const int32_t chunk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(npts, (int64_t)(1u << 28) / per));
   int32_t *dWp = nullptr, *dWa = nullptr, *dgen = nullptr;
   double *dpts = nullptr, *dscr = nullptr;
   int* dfail = nullptr;
@@ -1149,33 +1146,41 @@ extern "C" polya_status polya_verdict(polya_ctx* ctx, const double* y, int32_t n
     CK(cudaMalloc(&dWa, c.Wa.size() * sizeof(int32_t)));
     CK(cudaMalloc(&dpts, (size_t)npts * c.l * sizeof(double)));
     CK(cudaMalloc(&dfail, sizeof(int)));
-    CK(cudaMalloc(&dscr, (size_t)npts * (c.gen ? 3 : 1) * c.n * c.n * sizeof(double)));
+    CK(cudaMalloc(&dscr, (size_t)chunk * per * sizeof(double)));
     CK(cudaMemcpyAsync(dWp, c.Wp.data(), c.Wp.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dWa, c.Wa.data(), c.Wa.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dpts, pts_host, (size_t)npts * c.l * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(dfail, 0, sizeof(int), s));
     CK(launch_vmap(c, y, s));   // V_h(y) -> arena slots id_Vy + h
-    const size_t sm = (2 * (size_t)c.n * c.n + c.L0 + nextra) * sizeof(double);
+    const size_t sm = ((size_t)c.n * c.n + c.L0 + nextra) * sizeof(double);
+    const int32_t* dexp = nullptr;
+    const int32_t* dao = nullptr;
+    const int nt = (int)c.gp_aoff.size();
     if (c.gen) {
-      const int nt = (int)c.gp_aoff.size();
       std::vector<int32_t> tab(c.coef_exp);   // [ncoef][l] exponents, then aoff[nt], boff[nt]
       tab.insert(tab.end(), c.gp_aoff.begin(), c.gp_aoff.end());
       tab.insert(tab.end(), c.gp_boff.begin(), c.gp_boff.end());
       CK(cudaMalloc(&dgen, tab.size() * sizeof(int32_t)));
       CK(cudaMemcpyAsync(dgen, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      const int32_t* dexp = dgen;
-      const int32_t* dao = dgen + c.coef_exp.size();
+      dexp = dgen;
+      dao = dgen + c.coef_exp.size();
       CK(cudaFuncSetAttribute(k_grid_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      k_grid_gen<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.nbas, (int)c.l, (int)c.L0, nt, (int)c.ncoef, (int)c.r_off, dWp, dexp, dao,
-                                                 dao + nt, c.d_coef, c.arena, c.mstride, (int)c.np, c.id_Vy, dpts,
-                                                 dscr, dfail);
     } else {
       CK(cudaFuncSetAttribute(k_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      k_grid<<<(unsigned)npts, 128, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, (int)c.nA, dWp, dWa, c.arena, c.mstride,
-                                            (int)c.np, c.id_Vy, c.dA, dpts, dscr, dfail);
     }
-    ++c.launches;
-    CK(cudaGetLastError());
+    for (int32_t p0 = 0; p0 < npts; p0 += chunk) {   // points in chunks (bounded scratch)
+      const int32_t cnt = std::min(chunk, npts - p0);
+      const double* pp = dpts + (int64_t)p0 * c.l;
+      if (c.gen)
+        k_grid_gen<<<(unsigned)cnt, 256, sm, s>>>((int)c.n, (int)c.nbas, (int)c.l, (int)c.L0, nt, (int)c.ncoef,
+                                                  (int)c.r_off, dWp, dexp, dao, dao + nt, c.d_coef, c.arena, c.mstride,
+                                                  (int)c.np, c.id_Vy, pp, dscr, dfail);
+      else
+        k_grid<<<(unsigned)cnt, 256, sm, s>>>((int)c.n, (int)c.l, (int)c.L0, (int)c.nA, dWp, dWa, c.arena, c.mstride,
+                                              (int)c.np, c.id_Vy, c.dA, pp, dscr, dfail);
+      ++c.launches;
+      CK(cudaGetLastError());
+    }
     int h = 0;
     CK(cudaMemcpyAsync(&h, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Full robust-stability certification on the GPU path for a BASELINE config: Algorithm 2 from its
 initial point to the stopping rule (polya_ipm_solve), then the certificate's grid check
-(polya_verdict, n <= 64) -- the whole method of the paper at that size, with per-iteration
+(polya_verdict, n <= 168) -- the whole method of the paper at that size, with per-iteration
 timings.  Usage: python scripts/full_solve.py CONFIG [maxit]"""
 import json
 import os
@@ -29,7 +29,7 @@ r = ctx.ipm_solve(eps=1e-8, tol=1e-8, maxit=maxit)
 torch.cuda.synchronize()
 solve_s = time.time() - t1
 nfail = None
-if r["converged"] and cfg.n <= 118:
+if r["converged"] and cfg.n <= 168:
     nfail = ctx.verdict(r["y"], robust.simplex_points(cfg.l, 1000, 0))
 out = {"config": cid, "n": cfg.n, "l": cfg.l, "dp": cfg.dp, "d1": cfg.d1, "d2": cfg.d2, "K": ctx.K,
        "nblocks": ctx.nblocks, "converged": bool(r["converged"]), "status": r["status"], "iterations": r["iterations"],
@@ -38,5 +38,5 @@ out = {"config": cid, "n": cfg.n, "l": cfg.l, "dp": cfg.dp, "d1": cfg.d1, "d2": 
        "setup_s": setup_s, "solve_s": solve_s, "s_per_iteration": solve_s / max(r["iterations"], 1),
        "ms_schur_total": r["ms_schur"], "ms_factor_total": r["ms_factor"], "ms_other_total": r["ms_other"],
        "history": [{k: h[k] for k in ("gap", "mu", "tp", "td", "ms_schur", "ms_factor", "ms_other")} for h in r["history"]],
-       "note": "grid check: polya_verdict at the simplex vertices, edge midpoints and 1000 Dirichlet(1) points (n <= 118)"}
+       "note": "grid check: polya_verdict at the simplex vertices, edge midpoints and 1000 Dirichlet(1) points (n <= 168)"}
 print(json.dumps(out))

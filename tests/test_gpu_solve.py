@@ -119,3 +119,25 @@ def test_example2_bounds_tighten_with_degree(pb):
     assert all(b > BOUNDARY for b in bounds)
     assert all(bounds[i + 1] <= bounds[i] + 1e-12 for i in range(len(bounds) - 1)), bounds
     assert bounds[-1] < bounds[0]
+
+
+def test_verdict_beyond_118_states(pb):
+    """polya_verdict at n = 130 (> the former 118 shared-memory limit; config 5 has n = 120): the
+    P = I certificate y* (P_h = multinomial(dp; h) I) of a system with A_i + A_i^T < 0 passes at every
+    point, -y* fails at every point; the oracle's grid check agrees."""
+    import math
+    from paper_1411_3769_b200 import robust
+    c = synth.small_config(130, 2, 1, 1, 1)
+    A = synth.vertex_matrices(c, np.random.default_rng(0))
+    P = osdp.build_problem(A, c.n, c.l, c.dp, c.d1, c.d2)
+    ystar = np.zeros(P.K)
+    from oracle.monomials import enumerate_W
+    for h, e in enumerate(enumerate_W(c.l, c.dp)):
+        ystar[h * P.Ntil:h * P.Ntil + c.n] = math.factorial(c.dp) / math.prod(math.factorial(k) for k in e)
+    ctx = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
+    pts = robust.simplex_points(c.l, 12, 0)
+    assert ctx.verdict(torch.from_numpy(ystar).cuda(), pts) == 0
+    assert oipm.grid_check(P, ystar, 12, 0)
+    assert ctx.verdict(torch.from_numpy(-ystar).cuda(), pts) == len(pts)
+    assert not oipm.grid_check(P, -ystar, 12, 0)
+    ctx.close()
