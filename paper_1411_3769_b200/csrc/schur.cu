@@ -13,11 +13,11 @@
 // every raw entry is added to exactly one G entry.
 //
 // Work item = (pair, row class {i<=j}, column class {k<=l}) of 8-index chunks.  A CTA (160
-// threads, 3 per SM) computes the <= 4 raw 64x64 sub-blocks of the item (one per orientation)
+// threads, 4 per SM) computes the <= 4 raw 64x64 sub-blocks of the item (one per orientation)
 // with FP64 DMMA (mma.sync m8n8k4 -> DMMA.8x8x4; sm_100a has no f64 tcgen05 kind):
 //  * a producer warp pulls items from an atomic counter (pair-major, so co-running CTAs share a
 //    pair's operands in L2), one item ahead, and streams each orientation's k-list in stages of
-//    8 terms (16 8x8 operand tiles, 16-byte cp.async) into a 4-slot mbarrier ring (tile stride
+//    8 terms (16 8x8 operand tiles, 16-byte cp.async) into a 2-slot mbarrier ring (tile stride
 //    68 doubles: conflict-free fragment loads);
 //  * 4 consumer warps split the valid M / N tiles 2 x 2 (4x4 DMMA tiles per warp, fewer for the
 //    ragged last chunk of n, whose rows are packed two x-values per tile), fold each orientation
@@ -48,7 +48,7 @@ constexpr int NT = NT_OVERRIDE;
 constexpr int NT = (NCW + 1) * 32;  // + one producer warp (cp.async into an mbarrier ring)
 #endif
 #ifndef SCHUR_NSTAGE
-#define SCHUR_NSTAGE 4
+#define SCHUR_NSTAGE 2   // v23: 2 slots so that 4 CTAs fit an SM (v20: 4 slots, 3 CTAs/SM; +2 % at cfg 4)
 #endif
 constexpr int NSTAGE = SCHUR_NSTAGE;  // ring depth
 constexpr int KS = 68;     // doubles per staged 8x8 tile: 64 + 4 pad (conflict-free LDS.64 fragments)
@@ -256,7 +256,7 @@ __device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int&
                       // 4 = no operand loads (results wrong by construction: never a bench value)
 #endif
 #ifndef SCHUR_MINB
-#define SCHUR_MINB 3
+#define SCHUR_MINB 4     // v23: 4 CTAs/SM (96 registers, a few spills outside the DMMA loop)
 #endif
 
 // One G entry of the item from the folded block: canonical summation order (direct, s-swap,
