@@ -87,87 +87,106 @@ __global__ void k_scale_copy(double* __restrict__ arena, int64_t ms, const int32
 }
 
 // Batched GEMM on np x np arena matrices: C[c_id] = sum_terms alpha A[a_id] op(B[b_id]).  CTA = one
-// 32x32 tile of one output matrix, 4 warps, each a 16x16 block = 2x2 DMMA m8n8 tiles.  The K
-// dimension of all terms is streamed in chunks of 8 through a 2-stage cp.async double buffer:
-// A as [i][k] (row stride 12 doubles), B as [k][j] (stride 36) or, transposed, [j][k] (stride 12),
-// so every fragment load of a half-warp hits 16 distinct bank slots.
-constexpr int GT = 32;
-constexpr int AS = 12;
-constexpr int BSN = 36;
-constexpr int BBUF = GT * AS > 8 * BSN ? GT * AS : 8 * BSN;
+// 64x64 tile of one output matrix, 8 warps, each a 32x16 block = 4x2 DMMA m8n8 tiles (8x8 tiles that
+// lie beyond np are skipped, warp-uniformly).  The K dimension of all terms is streamed in chunks
+// of 16 through a 3-stage cp.async ring with one CTA barrier per chunk: A as [i][k] (row stride
+// 20 doubles), B as [k][j] (stride 68) or, transposed, [j][k] (stride 20), so every fragment load
+// of a half-warp hits 16 distinct bank pairs; k beyond np is zero-filled.
+constexpr int GT = 64;               // output tile
+constexpr int GK = 16;               // k per chunk
+constexpr int GST = 3;               // ring stages
+constexpr int AS = 20;               // [i][k] row stride (doubles), = 4 mod 16
+constexpr int BSN = 68;              // [k][j] row stride, = 4 mod 16
+constexpr int ABUF = GT * AS;        // 1280
+constexpr int BBUF = GT * AS > GK * BSN ? GT * AS : GK * BSN;   // 1280 / 1088
+constexpr size_t kGemmSmem = (size_t)GST * (ABUF + BBUF) * sizeof(double);
 __device__ __forceinline__ void cp16z(void* dst, const void* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
 }
-__global__ void __launch_bounds__(128) k_gemm(double* __restrict__ arena, int64_t ms, int np,
+__global__ void __launch_bounds__(256) k_gemm(double* __restrict__ arena, int64_t ms, int np,
                                               const GemmItem* __restrict__ items,
                                               const GemmTerm* __restrict__ terms, int tiles) {
-  __shared__ __align__(16) double As[2][GT * AS];
-  __shared__ __align__(16) double Bs[2][BBUF];
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                        // [GST][ABUF]
+  double* Bs = gsm + GST * ABUF;           // [GST][BBUF]
   const GemmItem it = items[blockIdx.y];
   const int ti = blockIdx.x / tiles, tj = blockIdx.x - ti * tiles;
   const int i0 = ti * GT, j0 = tj * GT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 16;
-  const int nk = np / 8, total = (it.tend - it.tbeg) * nk;
+  const int wr = (warp >> 2) * 32, wc = (warp & 3) * 16;
+  const int nkc = (np + GK - 1) / GK, total = (it.tend - it.tbeg) * nkc;
   auto issue = [&](int c, int buf) {
-    const GemmTerm tm = terms[it.tbeg + c / nk];
+    const GemmTerm tm = terms[it.tbeg + c / nkc];
 #ifdef POLYA_BOUNDS_CHECK
     assert(tm.a_id >= 0 && tm.b_id >= 0 && it.c_id >= 0 && (int64_t)tm.a_id * ms >= 0);
 #endif
-    const int k0 = (c % nk) * 8;
+    const int k0 = (c % nkc) * GK;
     const double* A = arena + (int64_t)tm.a_id * ms;
     const double* B = arena + (int64_t)tm.b_id * ms;
-    {  // A rows i0..i0+31, columns k0..k0+7: one 16-byte copy per thread
-      const int i = tid >> 2, kc = (tid & 3) * 2;
-      const bool v = i0 + i < np;
-      cp16z(&As[buf][i * AS + kc], v ? A + (int64_t)(i0 + i) * np + k0 + kc : A, v);
-    }
-    if (!tm.transB) {  // B rows k0..k0+7, columns j0..j0+31
-      const int k = tid >> 4, jc = (tid & 15) * 2;
-      const bool v = j0 + jc < np;
-      cp16z(&Bs[buf][k * BSN + jc], v ? B + (int64_t)(k0 + k) * np + j0 + jc : B, v);
-    } else {           // op(B)[k][j] = B[j][k]: rows j0..j0+31 of B, columns k0..k0+7
-      const int j = tid >> 2, kc = (tid & 3) * 2;
-      const bool v = j0 + j < np;
-      cp16z(&Bs[buf][j * AS + kc], v ? B + (int64_t)(j0 + j) * np + k0 + kc : B, v);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  double acc[2][2][2] = {};
-  if (total > 0) issue(0, 0);
-  for (int c = 0; c < total; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < total) {
-      issue(c + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
-    __syncthreads();
-    const GemmTerm tm = terms[it.tbeg + c / nk];
+    double* as = As + buf * ABUF;
+    double* bs = Bs + buf * BBUF;
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      double a[2], b[2];
+    for (int r = 0; r < 2; ++r) {   // A rows i0..i0+63, columns k0..k0+15: two 16-byte copies per thread
+      const int q = tid + r * 256, i = q >> 3, kc = (q & 7) * 2;
+      const bool v = i0 + i < np && k0 + kc < np;
+      cp16z(&as[i * AS + kc], v ? A + (int64_t)(i0 + i) * np + k0 + kc : A, v);
+    }
+    if (!tm.transB) {  // B rows k0..k0+15, columns j0..j0+63
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) a[mi] = As[buf][(wr + mi * 8 + g) * AS + ks * 4 + t];
-      if (tm.alpha != 1.0) {
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) a[mi] *= tm.alpha;
+      for (int r = 0; r < 2; ++r) {
+        const int q = tid + r * 256, k = q >> 5, jc = (q & 31) * 2;
+        const bool v = k0 + k < np && j0 + jc < np;
+        cp16z(&bs[k * BSN + jc], v ? B + (int64_t)(k0 + k) * np + j0 + jc : B, v);
       }
+    } else {           // op(B)[k][j] = B[j][k]: rows j0..j0+63 of B, columns k0..k0+15
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int q = tid + r * 256, j = q >> 3, kc = (q & 7) * 2;
+        const bool v = j0 + j < np && k0 + kc < np;
+        cp16z(&bs[j * AS + kc], v ? B + (int64_t)(j0 + j) * np + k0 + kc : B, v);
+      }
+    }
+  };
+  // warp-uniform validity of the warp's 8x8 tiles (rows / columns beyond np are never formed)
+  bool mv[4], nv[2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) mv[mi] = i0 + wr + mi * 8 < np;
+#pragma unroll
+  for (int nj = 0; nj < 2; ++nj) nv[nj] = j0 + wc + nj * 8 < np;
+  double acc[4][2][2] = {};
+#pragma unroll
+  for (int p = 0; p < GST - 1; ++p) {
+    if (p < total) issue(p, p);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int c = 0; c < total; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GST - 2) : "memory");
+    __syncthreads();   // chunk c landed for every thread; the buffer of chunk c-1 is free
+    if (c + GST - 1 < total) issue(c + GST - 1, (c + GST - 1) % GST);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int buf = c % GST;
+    const double* as = As + buf * ABUF;
+    const double* bs = Bs + buf * BBUF;
+    const GemmTerm tm = terms[it.tbeg + c / nkc];
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      double a[4], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = as[(wr + mi * 8 + g) * AS + ks * 4 + t] * tm.alpha;
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj)
-        b[nj] = tm.transB ? Bs[buf][(wc + nj * 8 + g) * AS + ks * 4 + t] : Bs[buf][(ks * 4 + t) * BSN + wc + nj * 8 + g];
+        b[nj] = tm.transB ? bs[(wc + nj * 8 + g) * AS + ks * 4 + t] : bs[(ks * 4 + t) * BSN + wc + nj * 8 + g];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < 2; ++nj) dmma(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
+        for (int nj = 0; nj < 2; ++nj)
+          if (mv[mi] && nv[nj]) dmma(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
     }
-    __syncthreads();   // the buffer is refilled by the issue of chunk c + 2
   }
   double* C = arena + (int64_t)it.c_id * ms;
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int nj = 0; nj < 2; ++nj) {
       const int i = i0 + wr + mi * 8 + g, j = j0 + wc + nj * 8 + 2 * t;
@@ -284,10 +303,16 @@ cudaError_t launch_scale_copy(Ctx& c, cudaStream_t s) {
 cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, int64_t nitems, cudaStream_t s) {
   if (nitems == 0) return cudaSuccess;
   const int tiles = (int)((c.np + GT - 1) / GT);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   for (int64_t off = 0; off < nitems; off += 65535) {
     const int64_t cnt = std::min<int64_t>(65535, nitems - off);
     dim3 grid((unsigned)(tiles * tiles), (unsigned)cnt);
-    k_gemm<<<grid, 128, 0, s>>>(c.arena, c.mstride, (int)c.np, items + off, terms, tiles);
+    k_gemm<<<grid, 256, kGemmSmem, s>>>(c.arena, c.mstride, (int)c.np, items + off, terms, tiles);
     ++c.launches;
   }
   return cudaGetLastError();
