@@ -29,7 +29,8 @@ from .monomials import enumerate_W
 
 __all__ = ["basis", "trE", "Problem", "build_problem", "vmap", "F_block", "F_stack",
            "apply_literal", "apply_vmap", "adjoint_literal", "adjoint_trace",
-           "schur_literal", "schur_entries", "schur_probe", "schur_structured", "build_problem_general"]
+           "schur_literal", "schur_entries", "schur_probe", "schur_structured", "schur_structured_tile",
+           "build_problem_general"]
 
 
 def basis(n: int):
@@ -319,42 +320,50 @@ def schur_structured(P: Problem, Xb, Wb, pairs=None):
     Lyapunov block and (beta_hj beta_h'j W_j, X_j) of each P-block.  Per pair (h <= h') the sum over
     k is one library matmul Raw = [vec L_k]^T [vec R_k] (n^2 x n^2), folded by the four orientation
     gathers.  pairs: optional list of (h, h') to compute (the rest of G stays zero)."""
-    n, N, L = P.n, P.Ntil, P.L
-    ia, ib = _ab(n)
-    a, b = ia[:, None], ib[:, None]
-    c, d = ia[None, :], ib[None, :]
     G = np.zeros((P.K, P.K))
+    N = P.Ntil
     todo = pairs if pairs is not None else [(h, h2) for h in range(P.L0) for h2 in range(h, P.L0)]
     for h, h2 in todo:
-        Ls, Rs = [], []
-        for j in range(L):
-            if P.beta[h, j] and P.beta[h2, j]:
-                Ls.append(float(P.beta[h, j] * P.beta[h2, j]) * Wb[j][:n, :n])
-                Rs.append(Xb[j][:n, :n])
-        for m in range(P.M):
-            W, X = Wb[L + m], Xb[L + m]
-            if P.gen is not None:
-                # F = -sum_q (A_q E B_q + B_q^T E A_q^T): the same four terms per (q, q'), here
-                # (B W A', B' X A), (B W B'^T, A'^T X A), (A^T W A', B' X B^T), (A^T W B'^T, A'^T X B^T)
-                # (H^T, I) for (A, B) gives back the continuous-time terms below (reading R18)
-                for A1, B1 in P.gen[h][m]:
-                    for A2, B2 in P.gen[h2][m]:
-                        Ls += [B1 @ W @ A2, B1 @ W @ B2.T, A1.T @ W @ A2, A1.T @ W @ B2.T]
-                        Rs += [B2 @ X @ A1, A2.T @ X @ A1, B2 @ X @ B1.T, A2.T @ X @ B1.T]
-                continue
-            H, H2 = P.H[h, m], P.H[h2, m]
-            if not (np.any(H) and np.any(H2)):
-                continue
-            Ls += [W @ H2.T, W, H @ W @ H2.T, H @ W]
-            Rs += [X @ H.T, H2 @ X @ H.T, X, H2 @ X]
-        if not Ls:
-            continue
-        k = len(Ls)
-        R4 = (np.stack(Ls).reshape(k, n * n).T @ np.stack(Rs).reshape(k, n * n)).reshape(n, n, n, n)
-        sw, tw = a != b, c != d
-        blk = R4[b, c, d, a] + np.where(sw, R4[a, c, d, b], 0.0) + np.where(tw, R4[b, d, c, a], 0.0) \
-            + np.where(sw & tw, R4[a, d, c, b], 0.0)
+        blk = schur_structured_tile(P, Xb, Wb, h, h2)
         G[h * N:(h + 1) * N, h2 * N:(h2 + 1) * N] = blk
         if h2 != h:
             G[h2 * N:(h2 + 1) * N, h * N:(h + 1) * N] = blk.T
     return G
+
+
+def schur_structured_tile(P: Problem, Xb, Wb, h, h2):
+    """The (h, h') block G[h-rows, h'-columns] of ``schur_structured`` alone (Ntil x Ntil; the same
+    arithmetic, so large configurations can be checked pair by pair)."""
+    n, N, L = P.n, P.Ntil, P.L
+    ia, ib = _ab(n)
+    a, b = ia[:, None], ib[:, None]
+    c, d = ia[None, :], ib[None, :]
+    Ls, Rs = [], []
+    for j in range(L):
+        if P.beta[h, j] and P.beta[h2, j]:
+            Ls.append(float(P.beta[h, j] * P.beta[h2, j]) * Wb[j][:n, :n])
+            Rs.append(Xb[j][:n, :n])
+    for m in range(P.M):
+        W, X = Wb[L + m], Xb[L + m]
+        if P.gen is not None:
+            # F = -sum_q (A_q E B_q + B_q^T E A_q^T): the same four terms per (q, q'), here
+            # (B W A', B' X A), (B W B'^T, A'^T X A), (A^T W A', B' X B^T), (A^T W B'^T, A'^T X B^T)
+            # (H^T, I) for (A, B) gives back the continuous-time terms below (reading R18)
+            for A1, B1 in P.gen[h][m]:
+                for A2, B2 in P.gen[h2][m]:
+                    Ls += [B1 @ W @ A2, B1 @ W @ B2.T, A1.T @ W @ A2, A1.T @ W @ B2.T]
+                    Rs += [B2 @ X @ A1, A2.T @ X @ A1, B2 @ X @ B1.T, A2.T @ X @ B1.T]
+            continue
+        H, H2 = P.H[h, m], P.H[h2, m]
+        if not (np.any(H) and np.any(H2)):
+            continue
+        Ls += [W @ H2.T, W, H @ W @ H2.T, H @ W]
+        Rs += [X @ H.T, H2 @ X @ H.T, X, H2 @ X]
+    if not Ls:
+        return np.zeros((N, N))
+    k = len(Ls)
+    R4 = (np.stack(Ls).reshape(k, n * n).T @ np.stack(Rs).reshape(k, n * n)).reshape(n, n, n, n)
+    sw, tw = a != b, c != d
+    blk = R4[b, c, d, a] + np.where(sw, R4[a, c, d, b], 0.0) + np.where(tw, R4[b, d, c, a], 0.0) \
+        + np.where(sw & tw, R4[a, d, c, b], 0.0)
+    return blk
