@@ -303,12 +303,9 @@ cudaError_t launch_scale_copy(Ctx& c, cudaStream_t s) {
 cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, int64_t nitems, cudaStream_t s) {
   if (nitems == 0) return cudaSuccess;
   const int tiles = (int)((c.np + GT - 1) / GT);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // per call (cheap): the attribute is per device, and a process may drive contexts on several
+  cudaError_t e = cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+  if (e != cudaSuccess) return e;
   for (int64_t off = 0; off < nitems; off += 65535) {
     const int64_t cnt = std::min<int64_t>(65535, nitems - off);
     dim3 grid((unsigned)(tiles * tiles), (unsigned)cnt);
