@@ -44,6 +44,8 @@ struct SchurTables {
   int2* kdesc = nullptr;          // [nk] arena matrix ids (L_k, R_k) of the pair k-lists for K4
   int32_t* cls_a = nullptr;       // [ncls] chunk index i of class (i <= j)
   int32_t* cls_b = nullptr;       // [ncls] chunk index j
+  int2* item_full = nullptr;      // [ncls^2] (sc, tc) of the k-th item of an off-diagonal pair (item order)
+  int2* item_upper = nullptr;     // [ncls(ncls+1)/2] same for a diagonal pair (sc <= tc); null: row-major
   unsigned long long* counter = nullptr;  // dynamic work counter
 };
 

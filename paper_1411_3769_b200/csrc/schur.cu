@@ -62,6 +62,8 @@ struct SchurArgs {
   int np, n, ncls, npl;
   const int32_t* cls_a;
   const int32_t* cls_b;
+  const int2* item_full;    // optional item-order tables (POLYA_ITEM_ORDER experiment); null: row-major
+  const int2* item_upper;
   const int32_t* pair_h;
   const int32_t* pair_h2;
   const int64_t* pair_kbeg;
@@ -214,7 +216,11 @@ __device__ __forceinline__ ItemInfo decode_item(const SchurArgs& p, int64_t item
   it.h = __ldg(p.pair_h + lo);
   it.h2 = __ldg(p.pair_h2 + lo);
   const int64_t rem = item - __ldg(p.pair_item + lo);
-  if (it.h != it.h2) {
+  if (p.item_full) {
+    const int2 st = __ldg((it.h != it.h2 ? p.item_full : p.item_upper) + rem);
+    it.sc = st.x;
+    it.tc = st.y;
+  } else if (it.h != it.h2) {
     it.sc = (int)(rem / p.ncls);
     it.tc = (int)(rem - (int64_t)it.sc * p.ncls);
   } else {
@@ -655,7 +661,7 @@ cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, 
   SchurArgs a;
   a.arena = c.arena; a.ms = c.mstride; a.ms32 = (unsigned)c.mstride; a.np = (int)c.np; a.n = (int)c.nbas; a.ncls = (int)c.ncls;
   a.npl = (int)c.npairs_local;
-  a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
+  a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.item_full = c.st.item_full; a.item_upper = c.st.item_upper; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
   a.pair_kbeg = c.st.pair_kbeg; a.pair_item = c.st.pair_item; a.kdesc = c.st.kdesc;
   a.item0 = i0; a.item1 = i1; a.counter = c.st.counter;
   a.G = G; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil; a.nmats = c.nmats;
