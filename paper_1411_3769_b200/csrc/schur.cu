@@ -261,6 +261,9 @@ __device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int&
 #define SCHUR_EXP 0   // timing experiments only (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either,
                       // 4 = no operand loads (results wrong by construction: never a bench value)
 #endif
+#ifndef SCHUR_EARLY_REL
+#define SCHUR_EARLY_REL 0
+#endif
 #ifndef SCHUR_MINB
 #define SCHUR_MINB 4     // v23: 4 CTAs/SM (96 registers, a few spills outside the DMMA loop)
 #endif
@@ -318,6 +321,26 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
 #endif
     const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
     const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
+#if SCHUR_EARLY_REL
+    // experiment: every fragment of the stage into registers first, release the slot (the
+    // arrive's release semantics order the loads before the producer's refill), then the DMMAs
+    double a[KB / 4][MI], b[KB / 4][NJ];
+#pragma unroll
+    for (int k4 = 0; k4 < KB / 4; ++k4) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[k4][i] = fA[k4 * 4 * KS + i * AST];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[k4][j] = fB[k4 * 4 * KS + j * BST];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + slot);
+#pragma unroll
+    for (int k4 = 0; k4 < KB / 4; ++k4)
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[k4][i], b[k4][j]);
+#else
 #pragma unroll
     for (int k4 = 0; k4 < KB / 4; ++k4) {
       double a[MI], b[NJ];
@@ -332,6 +355,7 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + slot);
+#endif
     ++cnt;
   }
   if (SCHUR_EXP & 2) {   // timing experiment: no fold, no epilogue (a never-taken sink keeps the DMMAs)
