@@ -53,7 +53,10 @@ constexpr int NT = (NCW + 1) * 32;  // + one producer warp (cp.async into an mba
 constexpr int NSTAGE = SCHUR_NSTAGE;  // ring depth
 constexpr int KS = 68;     // doubles per staged 8x8 tile: 64 + 4 pad (conflict-free LDS.64 fragments)
 constexpr int STAGE = 2 * KB * KS;  // doubles per stage: L[8 k][8 x][8 y] + R[8 k][8 z][8 w]
-constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 2 * NSTAGE * sizeof(uint64_t);
+#ifndef SCHUR_SPLIT_FULL
+#define SCHUR_SPLIT_FULL 1   // v24: a second `full` barrier per slot: consumers start on the first half of a stage
+#endif
+constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 3 * NSTAGE * sizeof(uint64_t);
 
 struct SchurArgs {
   const double* arena;
@@ -343,6 +346,7 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
 #else
 #pragma unroll
     for (int k4 = 0; k4 < KB / 4; ++k4) {
+      if (SCHUR_SPLIT_FULL && k4 == KB / 8) mbar_wait(full + 2 * NSTAGE + slot, ph);   // second half landed
       double a[MI], b[NJ];
 #pragma unroll
       for (int i = 0; i < MI; ++i) a[i] = fA[k4 * 4 * KS + i * AST];
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
+      mbar_init(full + 2 * NSTAGE + i, 32);   // SCHUR_SPLIT_FULL: the second half's completions
       mbar_init(empty + i, NCW);
     }
     mbar_init(&s_pbar, NCW);
@@ -528,9 +533,17 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
               cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL, pol);
               cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR, pol);
             }
+            if (SCHUR_SPLIT_FULL && kk == KB / 2 - 1) {   // first half of the k-terms: consumers may start
+              cp_async_mbar_arrive(full + slot);
+              if (lane == 0) mbar_arrive(full + slot);   // releases s_info[slot]
+            }
           }
-          cp_async_mbar_arrive(full + slot);
-          if (lane == 0) mbar_arrive(full + slot);   // releases s_info[slot]
+          if (SCHUR_SPLIT_FULL) {
+            cp_async_mbar_arrive(full + 2 * NSTAGE + slot);
+          } else {
+            cp_async_mbar_arrive(full + slot);
+            if (lane == 0) mbar_arrive(full + slot);   // releases s_info[slot]
+          }
           dcur = dnext;
           ++cnt;
         }
