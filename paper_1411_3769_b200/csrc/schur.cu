@@ -56,7 +56,10 @@ constexpr int STAGE = 2 * KB * KS;  // doubles per stage: L[8 k][8 x][8 y] + R[8
 #ifndef SCHUR_SPLIT_FULL
 #define SCHUR_SPLIT_FULL 1   // v24: a second `full` barrier per slot: consumers start on the first half of a stage
 #endif
-constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 3 * NSTAGE * sizeof(uint64_t);
+#ifndef SCHUR_SPLIT_EMPTY
+#define SCHUR_SPLIT_EMPTY 0   // experiment (with SCHUR_SPLIT_FULL): release / refill a slot by halves
+#endif
+constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 4 * NSTAGE * sizeof(uint64_t);
 
 struct SchurArgs {
   const double* arena;
@@ -356,6 +359,10 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      if (SCHUR_SPLIT_EMPTY && k4 == KB / 8 - 1) {   // the first half is in registers: release it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full + 3 * NSTAGE + slot);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + slot);
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
       mbar_init(full + 2 * NSTAGE + i, 32);   // SCHUR_SPLIT_FULL: the second half's completions
+      mbar_init(full + 3 * NSTAGE + i, NCW);  // SCHUR_SPLIT_EMPTY: the first half consumed
       mbar_init(empty + i, NCW);
     }
     mbar_init(&s_pbar, NCW);
@@ -515,7 +523,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
           int2 dnext = dfirst;
           if (s + 1 < it.nstage && lane < KB) dnext = __ldg(p.kdesc + it.kb + (int64_t)(s + 1) * KB + lane);
           const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
-          mbar_wait(empty + slot, ph ^ 1);
+          mbar_wait((SCHUR_SPLIT_EMPTY ? full + 3 * NSTAGE : empty) + slot, ph ^ 1);
           if (first_stage && lane == 0) {
             SlotInfo si;
             si.item = item; si.pl = it.pl; si.h = it.h; si.h2 = it.h2; si.sc = it.sc; si.tc = it.tc;
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
             const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, kk);
             const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, kk);
             POLYA_ASSERT(idL < p.nmats && idR < p.nmats);
+            if (SCHUR_SPLIT_EMPTY && kk == KB / 2) mbar_wait(empty + slot, ph ^ 1);   // second half free
             if (!(SCHUR_EXP & 4)) {   // experiment bit 4: no operand loads (timing of the DMMA side only)
               cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL, pol);
               cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR, pol);
