@@ -183,3 +183,20 @@ def test_loopback_generalised_form(pb):
     assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
     for c in ctxs:
         c.close()
+
+
+def test_multi_rank_ipm_needs_cyclic_and_nccl(pb):
+    """polya_ipm_step on several ranks: EINVAL without SHARD_CYCLIC, ENCCL (not a hang) with
+    SHARD_CYCLIC but no communicator -- the distributed factorisation's first broadcast fails
+    cleanly."""
+    cfg = synth.CONFIGS[1]
+    A = synth.vertex_matrices(cfg, np.random.default_rng(0))
+    P = osdp.build_problem(A, cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)
+    from oracle import ipm as oipm
+    X, Z, y, mu = oipm.initial_state(P)
+    for shard, msg in ((pb.SHARD_TILES, "invalid argument"), (pb.SHARD_CYCLIC, "NCCL")):
+        ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=0, nranks=2, shard=shard)
+        st = [_dev(v.copy()) for v in (X, Z, y)]
+        with pytest.raises(pb.PolyaError, match=msg):
+            ctx.ipm_step(*st, mu, 0)
+        ctx.close()
