@@ -223,7 +223,10 @@ def run_gpu(args, cfg, cid):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1:   # NCCL INIT lines (comm nranks, NVLS / NVLink transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
@@ -366,37 +369,53 @@ def run_gpu(args, cfg, cid):
                "d2h_overlap": f"G streamed back in {nch} pair chunks while later chunks are assembled"}
         del Gh, Gres
 
-    # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step; N=1, or any N with --shard cyclic) ----
+    # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step) at every N: one rank uses the
+    # dense (or, for config 5, tiled) factorisation; N > 1 ranks factor G distributed (SHARD_CYCLIC:
+    # column-cyclic pair tiles, NCCL panel broadcasts) ----
     ipm = None
-    if ((world == 1 and not blocks) or cyclic) and not args.no_ipm:   # dense K x K, tiled (cfg 5) or distributed
+    if not args.no_ipm:
         del G
         flush = None
+        if blocks:
+            del Grecv
         torch.cuda.empty_cache()
-        Xi = torch.eye(cfg.n, dtype=torch.float64, device=dev).repeat(ctx.nblocks, 1, 1).contiguous()
+        ictx = ctx
+        if world > 1 and not cyclic:   # the IPM context of N ranks: the distributed factorisation
+            ictx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world, shard=pb.SHARD_CYCLIC)
+            uid = [pb.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ictx.nccl_init(uid[0])
+        elif blocks:                   # one rank, block-sharded context: a plain one for the IPM leg
+            ictx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A)
+        Xi = torch.eye(cfg.n, dtype=torch.float64, device=dev).repeat(ictx.nblocks, 1, 1).contiguous()
         Zi = Xi.clone()
         yi = torch.zeros(K, dtype=torch.float64, device=dev)
-        mu = float(ctx.nblocks * cfg.n) / (3.0 * ctx.nblocks * cfg.n)   # reading R4 at X = Z = I
+        mu = 1.0 / 3.0                                                 # reading R4 at X = Z = I
         runs = []
         for it in range(2):                                            # the first call allocates G
+            barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            st = ctx.ipm_step(Xi, Zi, yi, mu, it)
+            st = ictx.ipm_step(Xi, Zi, yi, mu, it)
             e1.record()
             e1.synchronize()
             mu = st["mu"]
             runs.append((e0.elapsed_time(e1), st))
         ms, st = runs[-1]
         ms = max_over_ranks(ms)
-        tiled = ctx.K * ctx.K * 8 > 0.45 * torch.cuda.get_device_properties(dev).total_memory
-        ipm = {"s_per_iteration": ms / 1e3, "ms_schur": st["ms_schur"], "ms_factorisation": st["ms_factor"],
-               "ms_other": st["ms_other"],
+        tiled = ictx.K * ictx.K * 8 > 0.45 * torch.cuda.get_device_properties(dev).total_memory
+        dist_f = world > 1 or cyclic
+        ipm = {"s_per_iteration": ms / 1e3, "n_ranks": world, "ms_schur": max_over_ranks(st["ms_schur"]),
+               "ms_factorisation": max_over_ranks(st["ms_factor"]), "ms_other": max_over_ranks(st["ms_other"]),
                "factorisation": (f"distributed blocked Cholesky over {world} rank(s) (column-cyclic pair tiles, NCCL "
-                                 "panel broadcasts, split panel solves; DESIGN.md 7.1)" if cyclic else
+                                 "panel broadcasts, split panel solves; DESIGN.md 7.1)" if dist_f else
                                  "blocked Cholesky on the pair tiles (cuSOLVER dpotrf on diagonal tiles, cuBLAS "
                                  "dtrsm/dsyrk/dgemm) + blocked solves" if tiled else
                                  "cuSOLVER dpotrf + 2 dpotrs on the K x K SCM (FULL)"),
                "iteration_measured": 2, "gap": st["gap"], "tp": st["tp"], "td": st["td"]}
+        if ictx is not ctx:
+            ictx.close()
 
     # ---- CPU oracle baseline (rank 0, N=1 only) ----
     cpu = None
@@ -404,7 +423,17 @@ def run_gpu(args, cfg, cid):
         P, fl, t_used, done, build_s = oracle_rate_structured(cfg, A, X, W, seconds=args.cpu_seconds)
         _, ent, t_lit, _ = oracle_rate(cfg, A, X, W, seconds=min(3.0, args.cpu_seconds), P=P)
         per_entry = wg_total / (K * (K + 1) / 2)
+        one = None
+        try:   # the same oracle on one host thread (1 thread and all threads)
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                _, fl1, t1, done1, _ = oracle_rate_structured(cfg, A, X, W, seconds=min(6.0, args.cpu_seconds), P=P,
+                                                              seed=321)
+            one = {"value": fl1 / t1 / 1e12, "cores": 1, "sample": f"{done1} pair tiles in {t1:.1f} s"}
+        except Exception as exc:   # threadpoolctl missing: say so
+            one = {"unavailable": str(exc)}
         cpu = {"value": fl / t_used / 1e12, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "one_thread": one,
                "sample": f"{done} pair tiles (h,h') of G by the oracle's structured assembly (oracle.sdp."
                          f"schur_structured: one library matmul per pair + orientation fold) in {t_used:.1f} s, "
                          f"credited (1|2) n^4 K_pair each; oracle set-up {build_s:.1f} s excluded",
@@ -476,7 +505,31 @@ def main():
     cfg = synth.CONFIGS[cid]
     if args.impl == "reference":
         return run_reference(args, cfg, cid)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)", file=sys.stderr)
+        return 2
     return run_gpu(args, cfg, cid)
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` outside torchrun: re-exec this script under torch.distributed.run with N
+    ranks on this node (one per GPU); fails loudly when fewer than N GPUs are visible."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -55,8 +55,16 @@ typedef enum {
   POLYA_ENCCL = 5,      /* NCCL error, or a collective called without polya_nccl_init */
   POLYA_ENOTPD = 6,     /* a Z block or the Schur complement is not positive definite */
   POLYA_ESTEP = 7,      /* line search found no admissible step                   */
-  POLYA_EMAXIT = 8      /* reserved (iteration limit of a driver)                 */
+  POLYA_EMAXIT = 8,     /* iteration limit of a driver (polya_ipm_solve outcome)  */
+  POLYA_EDIVERGED = 9   /* iterates left every bound (polya_ipm_solve outcome): max(|phi|, |psi|, mu)
+                           > POLYA_DIVERGENCE_BOUND or non-finite -- an unbounded primal, i.e. an
+                           infeasible LMI (reading R20) */
 } polya_status;
+
+/* Divergence exit of polya_ipm_solve (reading R20): the iteration stops with status
+ * EDIVERGED as soon as tr(CX), a^T y or mu exceeds this bound in magnitude.  The problems are scaled
+ * so that a = 1 and X = Z = I at the start (mu = 1/3); a converging run stays many orders below. */
+#define POLYA_DIVERGENCE_BOUND 1e12
 
 /* How the Schur complement is split across ranks:
  *  POLYA_SHARD_TILES   output-tile sharding: every rank holds all blocks' X, Z^{-1} and
@@ -283,7 +291,9 @@ polya_status polya_simplex_map(int32_t l, int32_t d, int32_t n, const double* sc
  * starts from Algorithm 2's initial point X = Z = I, y = 0.  The outcome is a
  * result, not an error: res->converged = 1 iff the rule was met with every Z block positive
  * definite (reading R10); otherwise res->status says why (ENOTPD: a block or G lost definiteness,
- * ESTEP: no admissible step, EMAXIT).  The return value reports only misuse / CUDA failures.
+ * ESTEP: no admissible step, EDIVERGED: the iterates left POLYA_DIVERGENCE_BOUND, EMAXIT).  The
+ * return value reports misuse and failures: EINVAL, ENOMEM, ECUDA and ENCCL from any iteration are
+ * returned as such (never folded into res->status).
  * Ranks as polya_ipm_step (collective with SHARD_CYCLIC).  Synchronous.                     */
 typedef struct {
   double eps, tol;

@@ -33,7 +33,7 @@ import numpy as np
 from . import sdp
 from .monomials import enumerate_W
 
-__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "grid_check", "solve", "verdict"]
+__all__ = ["initial_state", "barrier", "step_length", "ipm_step", "C_blocks", "grid_check", "solve", "verdict", "DIVERGENCE_BOUND"]
 
 
 def C_blocks(P):
@@ -137,22 +137,36 @@ def grid_check(P, y, samples=1000, seed=0):
     return True
 
 
-def solve(P, eps=1e-8, tol=1e-8, maxit=60):
+DIVERGENCE_BOUND = 1e12   # reading R20; the same bound as POLYA_DIVERGENCE_BOUND
+
+
+def solve(P, eps=1e-8, tol=1e-8, maxit=60, info=None):
     """Algorithm 2 iterated from its initial point until the duality gap is below eps
     (stopping rule) and the primal residual ||B(X) - a|| below tol.  Returns
-    (converged, X, Z, y, iterations); converged requires every Z block PD (reading R10)."""
+    (converged, X, Z, y, iterations); converged requires every Z block PD (reading R10).
+    Divergence exit (reading R20): when tr(CX), a^T y or mu leaves DIVERGENCE_BOUND in magnitude (an
+    unbounded primal iterate: the LMI is infeasible) the iteration stops, before any product can
+    overflow.  info (optional dict) receives "status": converged / notpd / diverged / maxit."""
+    info = {} if info is None else info
     X, Z, y, mu = initial_state(P)
     for it in range(1, maxit + 1):
         try:
             X, Z, y, st = ipm_step(P, X, Z, y, mu)
         except np.linalg.LinAlgError:
+            info["status"] = "notpd"
             return False, X, Z, y, it
         mu = st["mu"]
-        if not np.all(np.isfinite(y)):
+        vals = (st["phi"], st["psi"], mu)
+        if not all(np.isfinite(v) for v in vals) or max(abs(v) for v in vals) > DIVERGENCE_BOUND \
+                or not np.all(np.isfinite(y)):
+            info["status"] = "diverged"
             return False, X, Z, y, it
         pinf = np.linalg.norm(sdp.adjoint_trace(P, X) - 1.0)
         if st["gap"] <= eps and pinf <= tol:
-            return all(np.linalg.eigvalsh(z).min() > 0 for z in Z), X, Z, y, it
+            ok = all(np.linalg.eigvalsh(z).min() > 0 for z in Z)
+            info["status"] = "converged" if ok else "notpd"
+            return ok, X, Z, y, it
+    info["status"] = "maxit"
     return False, X, Z, y, maxit
 
 

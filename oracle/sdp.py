@@ -21,6 +21,7 @@ W_{dp+da+d2} order.  Dual index i = k + Ntil*h (0-based).
 from __future__ import annotations
 
 import dataclasses
+import functools
 
 import numpy as np
 
@@ -29,7 +30,7 @@ from .monomials import enumerate_W
 
 __all__ = ["basis", "trE", "Problem", "build_problem", "vmap", "F_block", "F_stack",
            "apply_literal", "apply_vmap", "adjoint_literal", "adjoint_trace",
-           "schur_literal", "schur_entries", "schur_probe", "schur_structured", "schur_structured_tile",
+           "schur_literal", "schur_rows", "schur_entries", "schur_probe", "schur_structured", "schur_structured_tile",
            "build_problem_general"]
 
 
@@ -168,25 +169,33 @@ def build_problem_general(pairs, n, l, dp, d1, d2, delta=1e-3, R=None) -> Proble
 
 
 def vmap(P: Problem, x, h: int):
-    """V_<h>(x) = sum_j E_j x_{j+Ntil h} (Eq. 30) as a dense symmetric n x n matrix."""
+    """V_<h>(x) = sum_j E_j x_{j+Ntil h} (Eq. 30) as a dense symmetric n x n matrix (x may carry
+    leading batch dimensions: (..., K) -> (..., n, n))."""
     ia, ib = _ab(P.n)
-    seg = np.asarray(x[P.Ntil * h:P.Ntil * (h + 1)], dtype=np.float64)
-    out = np.zeros((P.n, P.n))
-    out[ia, ib] += seg
+    x = np.asarray(x, dtype=np.float64)
+    seg = x[..., P.Ntil * h:P.Ntil * (h + 1)]
+    out = np.zeros(x.shape[:-1] + (P.n, P.n))
+    out[..., ia, ib] += seg
     off = ia != ib
-    out[ib[off], ia[off]] += seg[off]
+    out[..., ib[off], ia[off]] += seg[..., off]
     return out
 
 
+@functools.lru_cache(maxsize=None)
 def _ab(n):
+    """Index arrays (a_k, b_k) of the basis (cached, read-only)."""
     ab = np.array(basis(n), dtype=np.int64).reshape(-1, 2)
-    return ab[:, 0], ab[:, 1]
+    ia, ib = ab[:, 0].copy(), ab[:, 1].copy()
+    ia.flags.writeable = False
+    ib.flags.writeable = False
+    return ia, ib
 
 
 def trE_all(n, M):
-    """[tr(E_k M)]_k for every basis element at once (same rule as ``trE``)."""
+    """[tr(E_k M)]_k for every basis element at once (same rule as ``trE``); M may carry leading
+    batch dimensions."""
     ia, ib = _ab(n)
-    return np.where(ia == ib, M[ia, ia], M[ia, ib] + M[ib, ia])
+    return np.where(ia == ib, M[..., ia, ia], M[..., ia, ib] + M[..., ib, ia])
 
 
 def F_block(P: Problem, i: int, b: int):
@@ -205,9 +214,32 @@ def F_block(P: Problem, i: int, b: int):
 
 
 def F_stack(P: Problem, b: int, rows=None):
-    """(len(rows), n, n) stack of B_{i,b} for i in rows (default all K)."""
-    rows = range(P.K) if rows is None else rows
-    return np.array([F_block(P, i, b) for i in rows])
+    """(len(rows), bn, bn) stack of B_{i,b} for i in rows (default all K): Eq. (31) for every row at
+    once -- the same dense products as ``F_block`` (E_k built densely, then H^T E + E H or the
+    generalised terms), batched over the rows that share h."""
+    rows = np.arange(P.K) if rows is None else np.asarray(list(rows), dtype=np.int64)
+    out = np.zeros((len(rows), P.bn, P.bn))
+    if len(rows) == 0:
+        return out
+    ia, ib = _ab(P.n)
+    hs, ks = np.divmod(rows, P.Ntil)
+    for h in np.unique(hs):
+        sel = np.nonzero(hs == h)[0]
+        E = np.zeros((len(sel), P.n, P.n))
+        r = np.arange(len(sel))
+        E[r, ia[ks[sel]], ib[ks[sel]]] = 1.0
+        E[r, ib[ks[sel]], ia[ks[sel]]] = 1.0
+        if b < P.L:
+            out[sel, :P.n, :P.n] = float(P.beta[h, b]) * E
+        elif P.gen is not None:
+            F = np.zeros((len(sel), P.bn, P.bn))
+            for Aq, Bq in P.gen[h][b - P.L]:
+                F -= Aq @ E @ Bq + Bq.T @ E @ Aq.T
+            out[sel] = F
+        else:
+            Hm = P.H[h, b - P.L]
+            out[sel] = -(Hm.T @ E + E @ Hm)
+    return out
 
 
 def apply_literal(P: Problem, y):
@@ -222,20 +254,27 @@ def apply_literal(P: Problem, y):
 
 def apply_vmap(P: Problem, y):
     """B^T(y) via Eq. (31) with e_i replaced by y (V is linear, Eq. 30):
-    P-block j: sum_h beta_{h,j} V_h(y); Lyapunov block m: -sum_h (H^T V_h(y) + V_h(y) H)."""
-    out = np.zeros((P.nblocks, P.bn, P.bn))
+    P-block j: sum_h beta_{h,j} V_h(y); Lyapunov block m: -sum_h (H^T V_h(y) + V_h(y) H)
+    (terms with a structurally zero beta_{h,j} / H_{h,m} add nothing and are skipped).
+    y may carry leading batch dimensions: (..., K) -> (..., nblocks, bn, bn)."""
+    y = np.asarray(y, dtype=np.float64)
+    out = np.zeros(y.shape[:-1] + (P.nblocks, P.bn, P.bn))
     V = [vmap(P, y, h) for h in range(P.L0)]
     for j in range(P.L):
         for h in range(P.L0):
-            out[j] += P.embed(float(P.beta[h, j]) * V[h])
+            if P.beta[h, j] == 0:
+                continue
+            out[..., j, :P.n, :P.n] += float(P.beta[h, j]) * V[h]
     for m in range(P.M):
         for h in range(P.L0):
             if P.gen is not None:
                 for Aq, Bq in P.gen[h][m]:
-                    out[P.L + m] -= Aq @ V[h] @ Bq + Bq.T @ V[h] @ Aq.T
+                    out[..., P.L + m, :, :] -= Aq @ V[h] @ Bq + Bq.T @ V[h] @ Aq.T
                 continue
             Hm = P.H[h, m]
-            out[P.L + m] -= Hm.T @ V[h] + V[h] @ Hm
+            if not np.any(Hm):
+                continue
+            out[..., P.L + m, :, :] -= Hm.T @ V[h] + V[h] @ Hm
     return out
 
 
@@ -250,26 +289,29 @@ def adjoint_literal(P: Problem, Xb):
 
 def adjoint_trace(P: Problem, Xb):
     """B(X)_i with tr(B_{i,b} X_b) expanded by cyclicity of the trace:
-    P-block: beta tr(E_k X); Lyapunov: -tr(H^T E X) - tr(E H X) = -tr(E_k (X H^T + H X))."""
-    y = np.zeros(P.K)
+    P-block: beta tr(E_k X); Lyapunov: -tr(H^T E X) - tr(E H X) = -tr(E_k (X H^T + H X)).
+    Xb: (nblocks, bn, bn), or a batch (..., nblocks, bn, bn) giving y of shape (..., K)."""
+    Xb = np.asarray(Xb)
+    y = np.zeros(Xb.shape[:-3] + (P.K,))
     for h in range(P.L0):
         for b in range(P.nblocks):
+            Xk = Xb[..., b, :, :]
             if b < P.L:
                 if P.beta[h, b] == 0:
                     continue
-                M = float(P.beta[h, b]) * Xb[b][:P.n, :P.n]
+                M = float(P.beta[h, b]) * Xk[..., :P.n, :P.n]
             elif P.gen is not None:
                 terms = P.gen[h][b - P.L]
                 if not terms:
                     continue
                 # tr(F X) with F = -sum (A E B + B^T E A^T) = tr(E_k M), M = -sum (B X A + A^T X B^T)
-                M = -sum(Bq @ Xb[b] @ Aq + Aq.T @ Xb[b] @ Bq.T for Aq, Bq in terms)
+                M = -sum(Bq @ Xk @ Aq + Aq.T @ Xk @ Bq.T for Aq, Bq in terms)
             else:
                 Hm = P.H[h, b - P.L]
                 if not np.any(Hm):
                     continue
-                M = -(Xb[b] @ Hm.T + Hm @ Xb[b])
-            y[P.Ntil * h:P.Ntil * (h + 1)] += trE_all(P.n, M)
+                M = -(Xk @ Hm.T + Hm @ Xk)
+            y[..., P.Ntil * h:P.Ntil * (h + 1)] += trE_all(P.n, M)
     return y
 
 
@@ -288,24 +330,44 @@ def schur_literal(P: Problem, Xb, Wb, rows=None):
     return G
 
 
-def schur_entries(P: Problem, Xb, Wb, pairs):
-    """lambda_{k,l} for an explicit list of (k, l) pairs, one trace product at a time,
-    skipping blocks where B_{k,b} or B_{l,b} is structurally zero."""
-    out = np.zeros(len(pairs))
-    for t, (k, l) in enumerate(pairs):
-        hk, hl = k // P.Ntil, l // P.Ntil
-        s = 0.0
+def schur_rows(P: Problem, Xb, Wb, rows, chunk=16):
+    """Whole rows lambda_{k,.} of Eq. T2 for k in rows.  By cyclicity,
+    lambda_{k,l} = sum_b tr(B_{k,b} Z_b^{-1} B_{l,b} X_b) = sum_b tr(B_{l,b} (X_b B_{k,b} Z_b^{-1})),
+    i.e. row k is B(.) (PAPER.md:318-324) applied to the blocks M_b = X_b B_{k,b} Z_b^{-1}, with B_{k,b}
+    the dense F of Eq. (31) (``F_stack``) and B(.) by ``adjoint_trace``.  Independent of the
+    rank-structured four-term route (``schur_structured``) the CUDA path follows."""
+    rows = list(rows)
+    G = np.zeros((len(rows), P.K))
+    for c0 in range(0, len(rows), chunk):
+        rr = rows[c0:c0 + chunk]
+        Mb = np.zeros((len(rr), P.nblocks, P.bn, P.bn))
         for b in range(P.nblocks):
-            if not (P.active(hk, b) and P.active(hl, b)):
-                continue
-            s += np.trace(F_block(P, k, b) @ Wb[b] @ F_block(P, l, b) @ Xb[b])
-        out[t] = s
+            Mb[:, b] = Xb[b] @ F_stack(P, b, rr) @ Wb[b]
+        G[c0:c0 + len(rr)] = adjoint_trace(P, Mb)
+    return G
+
+
+def schur_entries(P: Problem, Xb, Wb, pairs):
+    """lambda_{k,l} = sum_b tr(B_{k,b} Z_b^{-1} B_{l,b} X_b) (Eq. T2) for an explicit list of (k, l)
+    pairs: dense F (Eq. 31) and one trace of the four-matrix product per pair and block, blocks where
+    B_{k,b} or B_{l,b} is structurally zero skipped; batched over the pairs of a block."""
+    pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    out = np.zeros(len(pairs))
+    hk, hl = pairs[:, 0] // P.Ntil, pairs[:, 1] // P.Ntil
+    for b in range(P.nblocks):
+        act = np.array([P.active(h, b) for h in range(P.L0)], dtype=bool)
+        sel = np.nonzero(act[hk] & act[hl])[0]
+        for c0 in range(0, len(sel), 256):
+            s = sel[c0:c0 + 256]
+            FkW = F_stack(P, b, pairs[s, 0]) @ Wb[b]
+            FlX = F_stack(P, b, pairs[s, 1]) @ Xb[b]
+            out[s] += np.einsum("epq,eqp->e", FkW, FlX)
     return out
 
 
 def schur_probe(P: Problem, Xb, Wb, v):
     """(G v)_k = sum_l lambda_{k,l} v_l = sum_b tr(B_{k,b} W_b (sum_l v_l B_{l,b}) X_b)
-    = B(W B^T(v) X)_k by linearity of Eq. (T2) in B_l."""
+    = B(W B^T(v) X)_k by linearity of Eq. (T2) in B_l.  v: (K,) or a batch (p, K) of probes."""
     Fv = apply_vmap(P, v)
     Y = np.matmul(np.matmul(Wb, Fv), Xb)
     return adjoint_trace(P, Y)

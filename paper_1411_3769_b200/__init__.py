@@ -17,6 +17,7 @@ __all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "SHARD_TILES"
 # POLYA_LIB overrides the library path (timing-experiment variants built by tools/schur_exp.py)
 LIB_PATH = os.environ.get("POLYA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
 G_FULL, G_PAIR_TILES = 0, 1
+EDIVERGED, EMAXIT, ENOTPD, ESTEP = 9, 8, 6, 7
 SHARD_TILES, SHARD_BLOCKS, SHARD_CYCLIC = 0, 1, 2
 EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents", "polya_get_beta", "polya_get_H",
            "polya_get_C", "polya_apply", "polya_adjoint", "polya_schur", "polya_ipm_step", "polya_sync",
@@ -349,15 +350,20 @@ class Polya:
                                          _stream_ptr(stream)), "polya_reduce_G")
         return out
 
-    def ipm_solve(self, X=None, Z=None, y=None, eps=1e-8, tol=1e-8, maxit=60, init=True, stream=None):
-        """polya_ipm_solve: Algorithm 2 to its stopping rule (state on the device, updated in place)."""
+    def ipm_solve(self, X=None, Z=None, y=None, eps=1e-8, tol=1e-8, maxit=60, init=True, mu=None, it=0,
+                  stream=None):
+        """polya_ipm_solve: Algorithm 2 to its stopping rule (state on the device, updated in place).
+        init=True starts from X = Z = I, y = 0 (the library sets mu = 1/3); init=False resumes from the
+        given X, Z, y with the caller's barrier parameter mu (e.g. the last step's stats["mu"])."""
         import torch
+        if not init and (X is None or Z is None or y is None or mu is None):
+            raise PolyaError("ipm_solve(init=False) resumes a state: pass X, Z, y and mu")
         nbn = (self.nblocks, self.bn, self.bn)
         X = torch.empty(nbn, dtype=torch.float64, device="cuda") if X is None else X
         Z = torch.empty(nbn, dtype=torch.float64, device="cuda") if Z is None else Z
         y = torch.empty(self.K, dtype=torch.float64, device="cuda") if y is None else y
         st = _IpmState(_dev_ptr(X, None, "X").value, _dev_ptr(Z, None, "Z").value, _dev_ptr(y, self.K, "y").value,
-                       1.0 / 3.0, 0)
+                       1.0 / 3.0 if init else float(mu), 0 if init else int(it))
         hist = (_IpmStats * max(int(maxit), 1))()
         opt = _SolveOpts(float(eps), float(tol), int(maxit), int(bool(init)), hist)
         res = _SolveResult()

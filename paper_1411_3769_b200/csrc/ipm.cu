@@ -1076,8 +1076,16 @@ extern "C" polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, con
       const polya_status r = polya_ipm_step(ctx, st, &ps, stream);
       res->iterations = it + 1;
       if (opt->history) opt->history[it] = ps;
-      if (r != POLYA_OK) {   // an outcome, not an exception: Z or G lost definiteness, no step
+      if (r == POLYA_ENOTPD || r == POLYA_ESTEP) {   // an outcome, not an exception
         res->status = r;
+        return POLYA_OK;
+      }
+      if (r != POLYA_OK) return r;   // misuse, allocation, CUDA or NCCL failure: the caller's error
+      if (!std::isfinite(ps.phi) || !std::isfinite(ps.psi) || !std::isfinite(ps.mu) ||
+          std::max(std::fabs(ps.phi), std::max(std::fabs(ps.psi), ps.mu)) > POLYA_DIVERGENCE_BOUND) {
+        res->gap = ps.gap;   // reading R20: an unbounded iterate, the LMI is infeasible
+        res->mu = ps.mu;
+        res->status = POLYA_EDIVERGED;
         return POLYA_OK;
       }
       res->gap = ps.gap;

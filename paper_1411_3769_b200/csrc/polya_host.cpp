@@ -1173,6 +1173,7 @@ extern "C" const char* polya_strerror(polya_status s) {
     case POLYA_ENOTPD: return "matrix not positive definite";
     case POLYA_ESTEP: return "no admissible step";
     case POLYA_EMAXIT: return "iteration limit";
+    case POLYA_EDIVERGED: return "iterates diverged (infeasible LMI)";
   }
   return "unknown status";
 }

@@ -42,6 +42,33 @@ def test_solve_and_verdict_on_constructed_systems(pb, key, stable):
         assert r["gap"] <= 1e-8 and r["pinf"] <= 1e-8 and r["nfail"] == 0
 
 
+@pytest.mark.parametrize("case", ["scalar", "1u", "discrete"])
+def test_infeasible_exit_status_matches_oracle(pb, case):
+    """Reading R20: polya_ipm_solve stops an infeasible LMI with status EDIVERGED at the same
+    iteration as the oracle's divergence exit (the GPU steps match the oracle's to rounding)."""
+    if case == "scalar":
+        A = np.array([[[1.0]], [[-1.0]]])
+        P = osdp.build_problem(A, 1, 2, 1, 1, 1)
+        ctx = pb.Polya(1, 2, 1, 1, 1, A)
+    elif case == "1u":
+        c = synth.CONFIGS["1u"]
+        A = synth.vertex_matrices(c, np.random.default_rng(0))
+        P = osdp.build_problem(A, c.n, c.l, c.dp, c.d1, c.d2)
+        ctx = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
+    else:
+        A = synth.discrete_vertex_matrices(4, 3, 0.8, np.random.default_rng(3), unstable=True)
+        terms = synth.discrete_time_terms(A)
+        P = osdp.build_problem_general(terms, 4, 3, 1, 1, 1)
+        ctx = pb.Polya.general(terms, 4, 3, 1, 1, 1)
+    info = {}
+    ok, _, _, _, it = oipm.solve(P, info=info)
+    assert not ok and info["status"] == "diverged"
+    r = ctx.ipm_solve()
+    assert not r["converged"] and r["status"] == pb.EDIVERGED, r
+    assert r["iterations"] == it
+    ctx.close()
+
+
 def test_solve_matches_oracle_solution_config1(pb):
     """Same stopping iteration and the same certificate y to 1e-6 on config 1 (the GPU steps match
     the oracle's to ~1e-15 each, tests/test_gpu_ipm.py)."""

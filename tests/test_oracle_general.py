@@ -81,6 +81,10 @@ def test_adjoint_and_two_routes_to_G():
     Gs = sdp.schur_structured(P, X, W)      # the rank-structured route (used at larger sizes)
     assert np.abs(Gs - G).max() <= 1e-12 * np.abs(G).max()
     assert np.allclose(G, G.T, rtol=0, atol=1e-12 * np.abs(G).max())
+    rows = [0, 3, P.K - 1]
+    assert np.abs(sdp.schur_rows(P, X, W, rows) - G[rows]).max() <= 1e-12 * np.abs(G).max()
+    pairs = [(int(i), int(j)) for i, j in rng.integers(0, P.K, size=(9, 2))]
+    assert np.abs(sdp.schur_entries(P, X, W, pairs) - [G[i, j] for i, j in pairs]).max() <= 1e-12 * np.abs(G).max()
     Y = np.array([X[b] @ T[b] @ W[b] for b in range(P.nblocks)])
     Y = 0.5 * (Y + Y.transpose(0, 2, 1))
     Gy = sdp.adjoint_trace(P, Y)
@@ -197,5 +201,7 @@ def test_non_square_polynomial_identity_and_adjoint():
     X, W = synth.spd_blocks(N, P.nblocks, rng)
     lhs = sum(np.sum(out[b] * X[b]) for b in range(P.nblocks))
     assert abs(lhs - y @ sdp.adjoint_trace(P, X)) <= 1e-12 * abs(lhs)
-    assert np.abs(sdp.schur_structured(P, X, W) - sdp.schur_literal(P, X, W)).max() <= 1e-12 * np.abs(
-        sdp.schur_literal(P, X, W)).max()
+    G = sdp.schur_literal(P, X, W)
+    assert np.abs(sdp.schur_structured(P, X, W) - G).max() <= 1e-12 * np.abs(G).max()
+    rows = [1, P.K // 2, P.K - 1]
+    assert np.abs(sdp.schur_rows(P, X, W, rows) - G[rows]).max() <= 1e-12 * np.abs(G).max()

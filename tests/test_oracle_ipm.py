@@ -75,18 +75,8 @@ def test_theorem3_dense_shadow():
 
 
 def _solve(P, iters=60, eps=1e-8):
-    X, Z, y, mu = ipm.initial_state(P)
-    for _ in range(iters):
-        try:
-            X, Z, y, st = ipm.ipm_step(P, X, Z, y, mu)
-        except np.linalg.LinAlgError:
-            return False, y
-        mu = st["mu"]
-        pinf = np.linalg.norm(sdp.adjoint_trace(P, X) - 1.0)
-        if st["gap"] <= eps and pinf <= 1e-8:
-            zpd = all(np.linalg.eigvalsh(z).min() > 0 for z in Z)
-            return zpd, y
-    return False, y
+    ok, X, Z, y, it = ipm.solve(P, eps=eps, maxit=iters)
+    return ok, y
 
 
 def test_verdict_config1_stable_certified():
@@ -108,3 +98,48 @@ def test_verdict_scalar_spec_cases(a1, stable):
     P = sdp.build_problem(A, 1, 2, 1, 1, 1)
     ok, y = _solve(P)
     assert (ok and ipm.grid_check(P, y)) == stable
+
+
+def test_step_length_closed_form():
+    """Reading R5 ("standard line-search between 0 and 1"): for diagonal blocks the
+    distance to the PSD boundary is min_i S_ii / (-dS_ii) over the entries with dS_ii < 0, so
+    t = min(1, 0.98 * that); with no decreasing direction t = 1."""
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        nb, n = int(rng.integers(1, 4)), int(rng.integers(1, 6))
+        s = rng.uniform(0.1, 3.0, size=(nb, n))
+        ds = rng.normal(scale=rng.choice([0.05, 1.0, 20.0]), size=(nb, n))
+        S = np.array([np.diag(v) for v in s])
+        dS = np.array([np.diag(v) for v in ds])
+        neg = ds < 0
+        tmax = (s[neg] / -ds[neg]).min() if neg.any() else np.inf
+        want = min(1.0, 0.98 * tmax)
+        assert abs(ipm.step_length(S, dS) - want) <= 1e-13 * want
+        assert abs(ipm.step_length(S, dS, frac=0.5) - min(1.0, 0.5 * tmax)) <= 1e-13
+    # no decreasing direction: the full step
+    S = np.array([np.eye(3)])
+    assert ipm.step_length(S, np.array([np.diag([0.0, 1.0, 2.0])])) == 1.0
+    # a congruence leaves t unchanged (t depends on L^-1 dS L^-T only): S = Q D Q^T, dS = Q dD Q^T
+    Q, _ = np.linalg.qr(rng.normal(size=(4, 4)))
+    D, dD = np.diag([1.0, 2.0, 0.5, 4.0]), np.diag([-3.0, 1.0, -0.1, -1.0])
+    assert abs(ipm.step_length(np.array([Q @ D @ Q.T]), np.array([Q @ dD @ Q.T])) - 0.98 / 3.0) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["scalar", "1u", "discrete"])
+def test_infeasible_cases_exit_by_divergence(case):
+    """Reading R20: an infeasible LMI makes the primal iterate unbounded; the solve stops with
+    status "diverged" once tr(CX), a^T y or mu passes DIVERGENCE_BOUND -- with no floating-point
+    overflow on the way (warnings are errors here)."""
+    import warnings
+    if case == "scalar":
+        P = sdp.build_problem(np.array([[[1.0]], [[-1.0]]]), 1, 2, 1, 1, 1)
+    elif case == "1u":
+        P = _problem("1u")
+    else:
+        A = synth.discrete_vertex_matrices(4, 3, 0.8, np.random.default_rng(3), unstable=True)
+        P = sdp.build_problem_general(synth.discrete_time_terms(A), 4, 3, 1, 1, 1)
+    info = {}
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        ok, X, Z, y, it = ipm.solve(P, info=info)
+    assert not ok and info["status"] == "diverged", info

@@ -66,12 +66,15 @@ def test_H_closed_form_recursion_rowsums(l, dp, d1, d2):
     H = polya.H_table(A, l, dp, d2)
     Wp, WM = enumerate_W(l, dp), enumerate_W(l, dp + 1 + d2)
     for hi, h in enumerate(Wp):
+        Hrow = polya.H_row(A, l, dp, d2, hi)     # one row h alone (used at config 5's size)
+        assert Hrow.shape == (len(WM), n, n)
         for gi, g in enumerate(WM):
             want = np.zeros((n, n))
             for i in range(l):
                 parts = [g[j] - h[j] - (1 if j == i else 0) for j in range(l)]
                 want += mnom(d2, parts) * A[i]
             assert np.allclose(H[hi, gi], want, rtol=0, atol=1e-12 * max(1.0, np.abs(want).max()))
+            assert np.allclose(Hrow[gi], want, rtol=0, atol=1e-12 * max(1.0, np.abs(want).max()))
     assert np.allclose(H, polya.H_recursion(A, l, dp, d2), rtol=0, atol=1e-12)
     rs = H.sum(axis=1)
     for hi in range(len(Wp)):
@@ -90,6 +93,7 @@ def test_H_degree_two_A():
         for gi, g in enumerate(enumerate_W(l, dp + da + d2)):
             want = sum(mnom(d2, [g[j] - h[j] - lam[j] for j in range(l)]) * A[li] for li, lam in enumerate(Wa))
             assert np.allclose(H[hi, gi], want, atol=1e-12)
+            assert np.allclose(polya.H_row(A, l, dp, d2, hi, da)[gi], want, atol=1e-12)
 
 
 def test_C_spec_example_and_closed_form():

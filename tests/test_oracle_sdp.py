@@ -147,12 +147,22 @@ def test_schur_invariants(shape):
     for _ in range(3):
         u = rng.normal(size=P.K)
         assert np.linalg.norm(G @ u - sdp.schur_probe(P, X, W, u)) <= 1e-12 * np.linalg.norm(G @ u)
+    U = rng.normal(size=(3, P.K))      # a batch of probes
+    assert np.abs(sdp.schur_probe(P, X, W, U) - U @ G.T).max() <= 1e-12 * np.abs(U @ G.T).max()
     # sampled-entry route and row restriction
     pairs = [(int(i), int(j)) for i, j in rng.integers(0, P.K, size=(20, 2))]
     ent = sdp.schur_entries(P, X, W, pairs)
     assert np.allclose(ent, [G[i, j] for i, j in pairs], rtol=1e-12, atol=1e-13 * np.abs(G).max())
     rows = [0, P.K // 2, P.K - 1]
     assert np.array_equal(sdp.schur_literal(P, X, W, rows=rows), G[rows])
+    # whole-row route (row k = B(X F_k W), PAPER.md:318-324 applied to Eq. T2 by cyclicity)
+    rows2 = [int(i) for i in rng.integers(0, P.K, size=7)] + [P.K - 1]
+    Gr = sdp.schur_rows(P, X, W, rows2, chunk=3)
+    assert np.abs(Gr - G[rows2]).max() <= 1e-12 * np.abs(G).max()
+    # batched dense F equals the one-at-a-time Eq. (31)
+    for b in (0, P.L - 1, P.L, P.nblocks - 1):
+        want = np.array([sdp.F_block(P, i, b) for i in rows2])
+        assert np.array_equal(sdp.F_stack(P, b, rows2), want) or np.abs(sdp.F_stack(P, b, rows2) - want).max() <= 1e-15
 
 
 def test_config1_unstable_copy_no_certificate():
