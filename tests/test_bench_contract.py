@@ -20,3 +20,18 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert "workload" in line["config"]
+
+
+def test_gpus_flag_fails_loudly_without_enough_gpus():
+    """`bench.py --gpus 2` outside torchrun self-launches one rank per GPU -- and refuses (exit 2, a
+    message on stderr) when fewer GPUs are visible, instead of silently running one rank."""
+    import torch
+    if torch.cuda.device_count() >= 2:
+        import pytest
+        pytest.skip("two GPUs visible: the self-launch would run")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 2 and "visible GPUs" in out.stderr, (out.returncode, out.stderr[-500:])
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
+                         text=True, timeout=300, env={**os.environ, "WORLD_SIZE": "1"})
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr

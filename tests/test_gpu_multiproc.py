@@ -1,0 +1,115 @@
+"""Multi-GPU data path with real ranks (one process per GPU, NCCL over NVLink):
+skipped unless at least two GPUs are visible (every gpurun box of this build has one; the driver's
+scaling run has eight).
+
+Per rank, in its own process on its own GPU:
+* SHARD_BLOCKS: the rank's partial G over its Polya blocks, summed by polya_reduce_G
+  (ncclReduceScatter) into row-panel ranges -- the concatenated panels equal the one-rank G to 1e-12
+  and the literal oracle (Eq. T2) to 1e-10;
+* SHARD_TILES: each rank's work items written into a zeroed K x K G; the sum over ranks is the
+  one-rank G bit for bit (disjoint entries) and the oracle to 1e-10;
+* SHARD_CYCLIC: three polya_ipm_step iterations with the distributed factorisation match the
+  oracle's Algorithm 2 iterates to 1e-8.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import ipm as oipm
+from oracle import sdp as osdp
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+WORLD = 2
+
+
+def _rank_main(rank, world, q_uid, q_out, cid):
+    import torch
+
+    import paper_1411_3769_b200 as pb
+    torch.cuda.set_device(rank)
+    cfg = synth.CONFIGS[cid]
+    rng = np.random.default_rng(0)
+    A = synth.vertex_matrices(cfg, rng)
+    out = {"rank": rank}
+    # block sharding + NCCL ReduceScatter of the partial G
+    cb = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world, shard=pb.SHARD_BLOCKS)
+    X, W = synth.spd_blocks(cfg.n, cb.nblocks, rng)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    uids = []
+    for _ in range(2):   # two communicators: blocks and cyclic
+        if rank == 0:
+            u = pb.nccl_unique_id()
+            for _ in range(world - 1):
+                q_uid.put(u)
+        else:
+            u = q_uid.get()
+        uids.append(u)
+    cb.nccl_init(uids[0])
+    Gp = cb.schur(Xd, Wd, layout=pb.G_PAIR_TILES)
+    out["blocks_panel"] = cb.reduce_G(Gp).cpu().numpy()
+    torch.cuda.synchronize()
+    cb.close()
+    # output-tile sharding
+    ct = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world)
+    Gt = torch.zeros(ct.K, ct.K, dtype=torch.float64, device="cuda")
+    ct.schur(Xd, Wd, G=Gt)
+    out["tiles_G"] = Gt.cpu().numpy()
+    ct.close()
+    # distributed factorisation inside the IPM step
+    cc = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=rank, nranks=world, shard=pb.SHARD_CYCLIC)
+    cc.nccl_init(uids[1])
+    n, nb = cfg.n, cc.nblocks
+    Xi = torch.eye(n, dtype=torch.float64, device="cuda").repeat(nb, 1, 1).contiguous()
+    Zi = Xi.clone()
+    yi = torch.zeros(cc.K, dtype=torch.float64, device="cuda")
+    mu, iters = 1.0 / 3.0, []
+    for it in range(3):
+        st = cc.ipm_step(Xi, Zi, yi, mu, it)
+        mu = st["mu"]
+        iters.append((Xi.cpu().numpy(), Zi.cpu().numpy(), yi.cpu().numpy(), st))
+    out["ipm"] = iters
+    cc.close()
+    q_out.put(out)
+
+
+@pytest.mark.parametrize("cid", [2, 3])
+def test_two_ranks_blocks_tiles_cyclic(cid):
+    if torch.cuda.device_count() < WORLD:
+        pytest.skip(f"needs {WORLD} GPUs (found {torch.cuda.device_count()})")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q_uid, q_out = ctx.Queue(), ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, WORLD, q_uid, q_out, cid)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    outs = sorted([q_out.get(timeout=600) for _ in range(WORLD)], key=lambda o: o["rank"])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = synth.CONFIGS[cid]
+    rng = np.random.default_rng(0)
+    A = synth.vertex_matrices(cfg, rng)
+    P = osdp.build_problem(A, cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)
+    X, W = synth.spd_blocks(cfg.n, P.nblocks, rng)
+    Gref = osdp.schur_literal(P, X, W)
+    N = P.Ntil
+    tiles_ref = np.concatenate([Gref[h * N:(h + 1) * N, h2 * N:(h2 + 1) * N].ravel()
+                                for h in range(P.L0) for h2 in range(h, P.L0)])
+    panels = np.concatenate([o["blocks_panel"] for o in outs])[:tiles_ref.size]
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)   # noqa: E731
+    assert rel(panels, tiles_ref) <= 1e-10
+    Gt = sum(o["tiles_G"] for o in outs)
+    assert rel(Gt, Gref) <= 1e-10 and np.array_equal(Gt, Gt.T)
+    if cid != 2:      # the oracle's dense IPM step is minutes at config 3
+        return
+    Xo, Zo, yo, mu = oipm.initial_state(P)
+    for it in range(3):
+        Xo, Zo, yo, st = oipm.ipm_step(P, Xo, Zo, yo, mu)
+        mu = st["mu"]
+        for o in outs:
+            Xg, Zg, yg, sg = o["ipm"][it]
+            assert rel(Xg, Xo) <= 1e-8 and rel(Zg, Zo) <= 1e-8 and rel(yg, yo) <= 1e-8, (it, o["rank"])
