@@ -108,13 +108,19 @@ typedef struct {
                                  this rank (upper triangle) */
   int64_t tiles_bytes;  /* bytes of G in POLYA_G_PAIR_TILES layout on this rank   */
   int64_t b0, b1;       /* this rank's Polya blocks [b0, b1) (all blocks with SHARD_TILES) */
-  int64_t reduce_count; /* SHARD_BLOCKS: doubles each rank receives from polya_reduce_G in
-                           the PAIR_TILES layout = ceil(npairs*Ntil^2 / nranks); the partial-G
-                           buffer holds nranks*reduce_count doubles (zero padding at the end) */
+  int64_t reduce_count; /* SHARD_BLOCKS: doubles each rank receives from polya_reduce_G /
+                           polya_schur_reduce in the PAIR_TILES layout = groups * combine_tiles *
+                           Ntil^2 (see combine_tiles); a whole partial-G buffer for polya_reduce_G
+                           holds nranks*reduce_count doubles (zero tiles past npairs) */
   int64_t npairs_local; /* pair tiles held by this rank (PAIR_TILES layout: npairs_local tiles);
                            = pair1 - pair0 except with SHARD_CYCLIC (pairs not contiguous) */
   int64_t block_n;      /* order of every block of X, Z, C, B^T(y): cfg->n, or the generalised
                            form's N (polya_setup_general with nlmi > n) */
+  int64_t combine_tiles; /* SHARD_BLOCKS: t = pair tiles per rank and tile group of the combine.
+                           Group g = pair tiles [g*nranks*t, (g+1)*nranks*t) (pair order; zero tiles
+                           past npairs); rank r receives the summed tiles g*nranks*t + r*t + j
+                           (j < t) at Grecv + (g*t + j)*Ntil^2.  t is chosen so that a group is
+                           about 2 GiB (at least one tile).  0 for the other shardings. */
 } polya_dims;
 
 /* Output layouts of the Schur complement G (symmetric K x K):
@@ -258,15 +264,33 @@ polya_status polya_get_timing(polya_ctx* ctx, float* ms_pre, float* ms_assemble)
  * polya_nccl_init (every rank, collectively) creates the context's communicator with
  * cfg.rank / cfg.nranks on the context's device.
  * polya_reduce_G sums the ranks' partial G^(r) on `stream`:
- *   layout PAIR_TILES: ncclReduceScatter of the flattened tile buffer Gpart_dev
- *     (nranks*reduce_count doubles, as written by polya_schur + zero padding) into
- *     Grecv_dev (reduce_count doubles) = elements [rank*reduce_count, (rank+1)*reduce_count)
- *     of the summed tiles: a contiguous row-panel range, ready for a distributed factorisation;
+ *   layout PAIR_TILES: one ncclReduceScatter per tile group (polya_dims.combine_tiles) of the
+ *     tile buffer Gpart_dev (nranks*reduce_count doubles, as written by polya_schur + zero tiles
+ *     past npairs) into Grecv_dev (reduce_count doubles): this rank's whole summed tiles, in the
+ *     group order of polya_dims.combine_tiles;
  *   layout FULL: ncclAllReduce of the K x K matrix (Grecv_dev may equal Gpart_dev).
- * Errors: EINVAL (not SHARD_BLOCKS, null pointers), ENCCL (no communicator, NCCL failure). */
+ * Errors: EINVAL (not SHARD_BLOCKS, null pointers), ENCCL (no communicator, NCCL failure).
+ *
+ * polya_schur_reduce = polya_schur + polya_reduce_G(PAIR_TILES) pipelined: the
+ * precompute, then per tile group the K4 assembly of the group into one of two library-owned
+ * partial slots (2 x nranks*t tiles -- not the whole partial G) on `stream`, and the group's
+ * ncclReduceScatter on the context's own comm stream, ordered by events: the reduction of group g
+ * overlaps the assembly of group g+1.  Grecv_dev: reduce_count doubles, the same layout and values
+ * (bit for bit) as polya_schur + polya_reduce_G.  On return `stream` is ordered after every
+ * reduce-scatter.  One rank without a communicator: the reduce-scatter is a device copy.
+ * Assemblies on one context must be serialised on one stream (they share the work counter).
+ * Errors: EINVAL, ENCCL (several ranks without polya_nccl_init, NCCL failure), ENOMEM, ECUDA.
+ * polya_get_combine_timing: with polya_set_timing on, the milliseconds between the end of the last
+ * K4 launch and the end of the last reduce-scatter (the combine time NOT hidden under the assembly). */
 polya_status polya_nccl_unique_id(char out_id[128]);
 polya_status polya_nccl_init(polya_ctx* ctx, const char id[128]);
 polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart_dev, double* Grecv_dev, int layout, void* stream);
+polya_status polya_schur_reduce(polya_ctx* ctx, const double* X_dev, const double* Zinv_dev, double* Grecv_dev,
+                                void* stream);
+polya_status polya_get_combine_timing(polya_ctx* ctx, float* ms_exposed);
+/* polya_set_combine_tiles: override t (polya_dims.combine_tiles; 0 = automatic ~2 GiB groups), e.g.
+ * for a finer overlap; all ranks must use the same t.  SHARD_BLOCKS only.  Errors: EINVAL. */
+polya_status polya_set_combine_tiles(polya_ctx* ctx, int64_t tiles);
 
 /* ---- beyond one iteration: non-homogeneous systems, parameter boxes, solve, verdict ------------
  * (used by the bisection drivers of the paper's Examples 1-2.)

@@ -24,7 +24,8 @@ EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents",
            "polya_strerror", "polya_last_error", "polya_launch_count", "polya_destroy", "polya_set_timing",
            "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
            "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization", "polya_schur_prepare",
-           "polya_schur_assemble", "polya_setup_general", "polya_factor_solve_loopback"]
+           "polya_schur_assemble", "polya_setup_general", "polya_factor_solve_loopback", "polya_schur_reduce",
+           "polya_get_combine_timing", "polya_set_combine_tiles"]
 
 
 class PolyaError(RuntimeError):
@@ -42,7 +43,7 @@ class _Dims(ctypes.Structure):
                                               "npairs", "pair0", "pair1", "item0", "item1")] + \
                [("useful_flops_schur", ctypes.c_double), ("tiles_bytes", ctypes.c_int64), ("b0", ctypes.c_int64),
                 ("b1", ctypes.c_int64), ("reduce_count", ctypes.c_int64), ("npairs_local", ctypes.c_int64),
-                ("block_n", ctypes.c_int64)]
+                ("block_n", ctypes.c_int64), ("combine_tiles", ctypes.c_int64)]
 
 
 class _IpmState(ctypes.Structure):
@@ -100,6 +101,9 @@ def lib():
     L.polya_nccl_unique_id.argtypes = [vp]
     L.polya_nccl_init.argtypes = [vp, vp]
     L.polya_reduce_G.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+    L.polya_schur_reduce.argtypes = [vp, vp, vp, vp, vp]
+    L.polya_get_combine_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+    L.polya_set_combine_tiles.argtypes = [vp, i64]
     L.polya_homogenize.argtypes = [i32, i32, i32, vp, vp, vp, vp]
     L.polya_simplex_map.argtypes = [i32, i32, i32, vp, vp, vp, vp]
     L.polya_ipm_solve.argtypes = [vp, ctypes.POINTER(_IpmState), ctypes.POINTER(_SolveOpts), ctypes.POINTER(_SolveResult),
@@ -349,6 +353,31 @@ class Polya:
         self._check(lib().polya_reduce_G(self._h, _dev_ptr(Gpart, None, "Gpart"), _dev_ptr(out, None, "Grecv"), layout,
                                          _stream_ptr(stream)), "polya_reduce_G")
         return out
+
+    def schur_reduce(self, X, Zinv, out=None, stream=None):
+        """polya_schur_reduce: the block-sharded partial G assembled tile group by tile group, each
+        group's NCCL reduce-scatter overlapping the next group's assembly; returns this rank's summed
+        tiles (reduce_count doubles, layout of polya_dims.combine_tiles)."""
+        import torch
+        if out is None:
+            out = torch.empty(self.dims["reduce_count"], dtype=torch.float64, device=X.device)
+        nbn = self.nblocks * self.bn ** 2
+        self._check(lib().polya_schur_reduce(self._h, _dev_ptr(X, nbn, "X"), _dev_ptr(Zinv, nbn, "Zinv"),
+                                             _dev_ptr(out, self.dims["reduce_count"], "Grecv"), _stream_ptr(stream)),
+                    "polya_schur_reduce")
+        return out
+
+    def set_combine_tiles(self, t):
+        """polya_set_combine_tiles: tiles per rank and group of the combine (0 = automatic)."""
+        self._check(lib().polya_set_combine_tiles(self._h, int(t)), "polya_set_combine_tiles")
+        d = _Dims()
+        self._check(lib().polya_dims_get(self._h, ctypes.byref(d)), "polya_dims_get")
+        self.dims = {k: getattr(d, k) for k, _ in _Dims._fields_}
+
+    def combine_timing(self):
+        a = ctypes.c_float()
+        self._check(lib().polya_get_combine_timing(self._h, ctypes.byref(a)), "polya_get_combine_timing")
+        return float(a.value)
 
     def ipm_solve(self, X=None, Z=None, y=None, eps=1e-8, tol=1e-8, maxit=60, init=True, mu=None, it=0,
                   stream=None):

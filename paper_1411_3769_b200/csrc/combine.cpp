@@ -6,6 +6,7 @@
 // one NCCL collective instead of the paper's root gather.
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "polya_internal.h"
@@ -60,10 +61,15 @@ extern "C" polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart, doub
   ncclComm_t comm = (ncclComm_t)c.nccl;
   cudaStream_t s = (cudaStream_t)stream;
   ncclResult_t r;
-  if (layout == POLYA_G_PAIR_TILES) {
-    const int64_t tot = c.npairs * c.Ntil * c.Ntil;
-    const size_t rc = (size_t)((tot + c.cfg.nranks - 1) / c.cfg.nranks);
-    r = ncclReduceScatter(Gpart, Grecv, rc, ncclFloat64, ncclSum, comm, s);
+  if (layout == POLYA_G_PAIR_TILES) {   // one reduce-scatter per tile group (combine_shape), fused
+    int64_t t = 0, groups = 0;
+    combine_shape(c, &t, &groups);
+    const int64_t NN = c.Ntil * c.Ntil, N = c.cfg.nranks;
+    r = ncclGroupStart();
+    for (int64_t g = 0; g < groups && r == ncclSuccess; ++g)
+      r = ncclReduceScatter(Gpart + g * N * t * NN, Grecv + g * t * NN, (size_t)(t * NN), ncclFloat64, ncclSum, comm, s);
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
   } else if (layout == POLYA_G_FULL) {
     r = ncclAllReduce(Gpart, Grecv, (size_t)(c.K * c.K), ncclFloat64, ncclSum, comm, s);
   } else {
@@ -73,7 +79,102 @@ extern "C" polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart, doub
   return POLYA_OK;
 }
 
+// The pipelined block-sharded Schur complement: the rank's partial G is assembled one
+// tile group at a time into one of two ping-pong slots on `stream`, and each group's reduce-scatter
+// runs on the context's comm stream as soon as its K4 launch has finished (event), overlapping the
+// assembly of the next group; a slot is reused only after its previous reduce-scatter has read it.
+// With one rank and no communicator the "reduce-scatter" is the identity (a device copy).
+extern "C" polya_status polya_schur_reduce(polya_ctx* ctx, const double* X, const double* Zinv, double* Grecv,
+                                           void* stream) {
+  if (!ctx || !X || !Zinv || !Grecv) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (c.cfg.shard != POLYA_SHARD_BLOCKS) {
+    c.last_error = "polya_schur_reduce needs SHARD_BLOCKS";
+    return POLYA_EINVAL;
+  }
+  if (!c.nccl && c.cfg.nranks > 1) {
+    c.last_error = "polya_schur_reduce before polya_nccl_init";
+    return POLYA_ENCCL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t t = 0, groups = 0;
+  combine_shape(c, &t, &groups);
+  const int64_t NN = c.Ntil * c.Ntil, N = c.cfg.nranks, gt = N * t;   // tiles per group
+  auto cuda = [&](cudaError_t e) {
+    if (e != cudaSuccess) {
+      c.last_error = std::string("polya_schur_reduce: ") + cudaGetErrorString(e);
+      return false;
+    }
+    return true;
+  };
+  if (!c.comm_stream) {
+    if (!cuda(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking))) return POLYA_ECUDA;
+    for (auto& e : c.comb_ev)
+      if (!cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return POLYA_ECUDA;
+  }
+  for (int q = 0; q < 2; ++q)
+    if (!c.comb_slot[q]) {
+      cudaError_t e = cudaMalloc(&c.comb_slot[q], (size_t)(gt * NN) * sizeof(double));
+      if (e == cudaErrorMemoryAllocation) {
+        c.last_error = "polya_schur_reduce: partial-tile slots";
+        return POLYA_ENOMEM;
+      }
+      if (!cuda(e)) return POLYA_ECUDA;
+    }
+  polya_status st = polya_schur_prepare(ctx, X, Zinv, stream);
+  if (st != POLYA_OK) return st;
+  for (int64_t g = 0; g < groups; ++g) {
+    const int q = (int)(g & 1);
+    double* slot = c.comb_slot[q];
+    const int64_t p0 = g * gt, p1 = std::min(c.npairs, p0 + gt);
+    if (g >= 2 && !cuda(cudaStreamWaitEvent(s, c.comb_ev[2 + q], 0))) return POLYA_ECUDA;   // slot read
+    if (p1 - p0 < gt && !cuda(cudaMemsetAsync(slot + (p1 - p0) * NN, 0, (size_t)((gt - (p1 - p0)) * NN) * sizeof(double), s)))
+      return POLYA_ECUDA;   // zero tiles past npairs in the last group
+    // K4 writes pair p's tile at G + p Ntil^2: shift the base so that pair p0 lands at the slot start
+    const int64_t i0 = std::max(c.item0, c.local_item[p0]), i1 = std::min(c.item1, c.local_item[p1]);
+    if (!cuda(launch_schur(c, slot - p0 * NN, POLYA_G_PAIR_TILES, i0, i1, s))) return POLYA_ECUDA;
+    if (!cuda(cudaEventRecord(c.comb_ev[q], s))) return POLYA_ECUDA;
+    if (!cuda(cudaStreamWaitEvent(c.comm_stream, c.comb_ev[q], 0))) return POLYA_ECUDA;
+    if (c.nccl) {
+      ncclResult_t r = ncclReduceScatter(slot, Grecv + g * t * NN, (size_t)(t * NN), ncclFloat64, ncclSum,
+                                         (ncclComm_t)c.nccl, c.comm_stream);
+      if (r != ncclSuccess) return nccl_fail(ctx, "ncclReduceScatter (pipelined combine)", r);
+    } else if (!cuda(cudaMemcpyAsync(Grecv + g * t * NN, slot, (size_t)(t * NN) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     c.comm_stream))) {
+      return POLYA_ECUDA;
+    }
+    if (!cuda(cudaEventRecord(c.comb_ev[2 + q], c.comm_stream))) return POLYA_ECUDA;
+  }
+  if (c.timing && !cuda(cudaEventRecord(c.ev[2], s))) return POLYA_ECUDA;   // end of the assembly
+  for (int q = 0; q < 2 && q < groups; ++q)   // the caller's stream sees every group reduced
+    if (!cuda(cudaStreamWaitEvent(s, c.comb_ev[2 + q], 0))) return POLYA_ECUDA;
+  if (c.timing && !cuda(cudaEventRecord(c.ev[3], s))) return POLYA_ECUDA;
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_set_combine_tiles(polya_ctx* ctx, int64_t tiles) {
+  if (!ctx || tiles < 0) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (c.cfg.shard != POLYA_SHARD_BLOCKS) return POLYA_EINVAL;
+  polya::combine_free(c);   // the slots are sized by t
+  c.comb_t = tiles;
+  return POLYA_OK;
+}
+
 namespace polya {
+void combine_free(Ctx& c) {
+  for (auto& p : c.comb_slot) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  for (auto& e : c.comb_ev) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
+  if (c.comm_stream) cudaStreamDestroy(c.comm_stream);
+  c.comm_stream = nullptr;
+}
+
 // Collectives of the distributed factorisation (SHARD_CYCLIC).  With one rank they are no-ops (the
 // root's buffer is every rank's buffer); with more they need polya_nccl_init.
 cudaError_t comm_bcast(Ctx& c, void* buf, size_t count, bool is_int, int root, cudaStream_t s) {

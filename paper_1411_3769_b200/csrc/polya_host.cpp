@@ -885,10 +885,13 @@ static void fill_dims(const Ctx& c, polya_dims* o) {
   o->tiles_bytes = c.npairs_local * c.Ntil * c.Ntil * (int64_t)sizeof(double);
   o->b0 = c.b0;
   o->b1 = c.b1;
-  const int64_t tot = c.npairs * c.Ntil * c.Ntil;
-  o->reduce_count = c.cfg.shard == POLYA_SHARD_BLOCKS ? (tot + c.cfg.nranks - 1) / c.cfg.nranks : 0;
+  int64_t t = 0, groups = 0;
+  combine_shape(c, &t, &groups);
+  const bool blocks = c.cfg.shard == POLYA_SHARD_BLOCKS;
+  o->reduce_count = blocks ? groups * t * c.Ntil * c.Ntil : 0;
   o->npairs_local = c.npairs_local;
   o->block_n = c.n;
+  o->combine_tiles = blocks ? t : 0;
 }
 
 extern "C" polya_status polya_plan(const polya_config* cfg, polya_dims* out) {
@@ -1151,6 +1154,17 @@ extern "C" polya_status polya_get_timing(polya_ctx* ctx, float* ms_pre, float* m
   return POLYA_OK;
 }
 
+extern "C" polya_status polya_get_combine_timing(polya_ctx* ctx, float* ms_exposed) {
+  if (!ctx || !ms_exposed) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (!c.ev[0]) return POLYA_EINVAL;
+  if (cudaEventSynchronize(c.ev[3]) != cudaSuccess || cudaEventElapsedTime(ms_exposed, c.ev[2], c.ev[3]) != cudaSuccess) {
+    c.last_error = "combine timing events not recorded (polya_schur_reduce with timing on)";
+    return POLYA_ECUDA;
+  }
+  return POLYA_OK;
+}
+
 extern "C" polya_status polya_sync(polya_ctx* ctx) {
   if (!ctx) return POLYA_EINVAL;
   cudaError_t e = cudaDeviceSynchronize();
@@ -1188,6 +1202,7 @@ namespace polya { void nccl_free(Ctx& c); }  // combine.cpp
 extern "C" void polya_destroy(polya_ctx* ctx) {
   if (!ctx) return;
   polya_ipm_free(ctx->c);
+  combine_free(ctx->c);
   nccl_free(ctx->c);
   for (auto& e : ctx->c.ev)
     if (e) cudaEventDestroy(e);

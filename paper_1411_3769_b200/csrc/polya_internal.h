@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -119,10 +120,29 @@ struct Ctx {
   void* ipm = nullptr;
   bool timing = false;
   int fact_mode = 0;     // polya_set_factorization: 0 auto, 1 dense K x K, 2 tiled (pair tiles)
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // schur: start, after precompute, after K4, after combine
+  // pipelined block-sharded combine (polya_schur_reduce, combine.cpp): two partial-tile slots,
+  // a dedicated comm stream, slot events (allocated on first use)
+  double* comb_slot[2] = {nullptr, nullptr};
+  int64_t comb_t = 0;                  // polya_set_combine_tiles (0: automatic, ~2 GiB groups)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comb_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // assembled[2], reduced[2]
   std::string last_error;
   int64_t launches = 0;
 };
+
+// Tile groups of the block-sharded combine (SHARD_BLOCKS): group g holds pair tiles
+// [g N t, (g+1) N t) (N = nranks, zero tiles past npairs); its reduce-scatter hands rank r the t tiles
+// g N t + r t .. + t - 1, stored at Grecv + g t Ntil^2.  t = tiles per rank and group, sized so that
+// a group is ~2 GiB (at least one tile): the granularity of the overlap and of the partial buffers.
+inline void combine_shape(const Ctx& c, int64_t* t_out, int64_t* groups_out) {
+  const int64_t N = c.cfg.nranks, tile_bytes = c.Ntil * c.Ntil * (int64_t)sizeof(double);
+  int64_t t = c.comb_t > 0 ? c.comb_t : std::max<int64_t>(1, ((int64_t)2 << 30) / std::max<int64_t>(1, N * tile_bytes));
+  t = std::min<int64_t>(t, std::max<int64_t>(1, (c.npairs + N - 1) / N));
+  *t_out = t;
+  *groups_out = (c.npairs + N * t - 1) / (N * t);
+}
+void combine_free(Ctx& c);
 
 // ---- kernel launchers (kernels.cu / schur.cu) -------------------------------------------------
 cudaError_t launch_setup_H(Ctx& c, cudaStream_t s);

@@ -50,7 +50,10 @@ def _rank_main(rank, world, q_uid, q_out, cid):
         uids.append(u)
     cb.nccl_init(uids[0])
     Gp = cb.schur(Xd, Wd, layout=pb.G_PAIR_TILES)
-    out["blocks_panel"] = cb.reduce_G(Gp).cpu().numpy()
+    out["blocks_panel"] = cb.reduce_G(Gp).cpu().numpy()          # whole partial, then one combine
+    cb.set_combine_tiles(1)                                       # pipelined: one tile per rank and group
+    out["blocks_pipe"] = cb.schur_reduce(Xd, Wd).cpu().numpy()
+    out["combine_tiles"] = cb.dims["combine_tiles"]
     torch.cuda.synchronize()
     cb.close()
     # output-tile sharding
@@ -99,9 +102,24 @@ def test_two_ranks_blocks_tiles_cyclic(cid):
     N = P.Ntil
     tiles_ref = np.concatenate([Gref[h * N:(h + 1) * N, h2 * N:(h2 + 1) * N].ravel()
                                 for h in range(P.L0) for h2 in range(h, P.L0)])
-    panels = np.concatenate([o["blocks_panel"] for o in outs])[:tiles_ref.size]
     rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)   # noqa: E731
-    assert rel(panels, tiles_ref) <= 1e-10
+    NN = N * N
+
+    def tiles_of(key, t):   # rank r holds tiles g N t + r t + j at (g t + j) (polya_dims.combine_tiles)
+        got = np.zeros(tiles_ref.size)
+        for o in outs:
+            buf = o[key]
+            for slot in range(buf.size // NN):
+                g, j = divmod(slot, t)
+                p = g * WORLD * t + o["rank"] * t + j
+                if p < P.L0 * (P.L0 + 1) // 2:
+                    got[p * NN:(p + 1) * NN] = buf[slot * NN:(slot + 1) * NN]
+        return got
+    t_auto = -(-(P.L0 * (P.L0 + 1) // 2) // WORLD)     # small tiles: one group of ceil(npairs / N)
+    whole = tiles_of("blocks_panel", t_auto)
+    pipe = tiles_of("blocks_pipe", outs[0]["combine_tiles"])
+    assert rel(whole, tiles_ref) <= 1e-10 and rel(pipe, tiles_ref) <= 1e-10
+    assert np.array_equal(whole, pipe)          # same partials, same NCCL sums
     Gt = sum(o["tiles_G"] for o in outs)
     assert rel(Gt, Gref) <= 1e-10 and np.array_equal(Gt, Gt.T)
     if cid != 2:      # the oracle's dense IPM step is minutes at config 3

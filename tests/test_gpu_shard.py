@@ -125,3 +125,54 @@ def test_chunked_assembly_is_bitwise_the_full_call(pb, cfg, world):
         with pytest.raises(pb.PolyaError):
             ctx.schur_assemble(G, 0, npl + 1, layout=pb.G_FULL)
         ctx.close()
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS[2], synth.small_config(12, 3, 2, 1, 2), synth.CONFIGS[3]],
+                         ids=lambda c: c.name)
+@pytest.mark.parametrize("tiles", [1, 2, 4, 0])
+@pytest.mark.parametrize("with_nccl", [False, True])
+def test_pipelined_combine_is_bitwise_schur_plus_reduce(pb, cfg, tiles, with_nccl):
+    """polya_schur_reduce (the partial G assembled tile group by tile group into two ping-pong slots,
+    each group's reduce-scatter on the comm stream overlapping the next group's assembly) gives
+    exactly polya_schur + polya_reduce_G: one rank, with a one-rank NCCL communicator or the
+    communicator-less identity; t = 1, 2, 4 tiles per group (several groups, a zero-padded last
+    group) and the automatic t."""
+    A, X, W = _inputs(cfg)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, shard=pb.SHARD_BLOCKS)
+    if with_nccl:
+        ctx.nccl_init(pb.nccl_unique_id())
+    ctx.set_combine_tiles(tiles)
+    t = ctx.dims["combine_tiles"]
+    assert t == (tiles if tiles else t) and t >= 1
+    ref = ctx.schur(Xd, Wd, layout=pb.G_PAIR_TILES)          # whole partial (+ zero tiles)
+    assert ref.numel() == ctx.dims["reduce_count"]            # one rank: receives everything
+    ctx.set_timing(True)
+    for _ in range(2):                                        # the second call reuses the slots
+        out = torch.full((ctx.dims["reduce_count"],), float("nan"), dtype=torch.float64, device="cuda")
+        ctx.schur_reduce(Xd, Wd, out=out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    assert ctx.combine_timing() >= 0.0
+    N = ctx.Ntil
+    P = osdp.build_problem(A, cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)
+    if P.K <= 1000:
+        Gl = osdp.schur_literal(P, X, W)
+        tiles_ref = np.concatenate([Gl[h * N:(h + 1) * N, h2 * N:(h2 + 1) * N].ravel()
+                                    for h in range(P.L0) for h2 in range(h, P.L0)])
+        assert _rel(out.cpu().numpy()[:tiles_ref.size], tiles_ref) <= 1e-10
+    ctx.close()
+
+
+def test_pipelined_combine_needs_communicator_for_several_ranks(pb):
+    cfg = synth.CONFIGS[2]
+    A, X, W = _inputs(cfg)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    c = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=0, nranks=2, shard=pb.SHARD_BLOCKS)
+    with pytest.raises(pb.PolyaError):
+        c.schur_reduce(Xd, Wd)
+    c.close()
+    t = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A)
+    with pytest.raises(pb.PolyaError):
+        t.schur_reduce(Xd, Wd)                      # SHARD_TILES: nothing to combine
+    t.close()

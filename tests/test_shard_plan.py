@@ -33,8 +33,11 @@ def test_block_partition(shape):
             own = cost[d["b0"]:d["b1"]].sum()
             assert abs(d["useful_flops_schur"] - own) <= 1e-9 * max(own, 1.0)
             assert d["item0"] == 0 and d["item1"] == ds[0]["item1"]
-            npairs, Ntil = d["npairs"], d["Ntil"]
-            assert d["reduce_count"] * world >= npairs * Ntil * Ntil > (d["reduce_count"] - 1) * world
+            npairs, Ntil, t = d["npairs"], d["Ntil"], d["combine_tiles"]
+            groups = -(-npairs // (world * t))
+            assert t >= 1 and d["reduce_count"] == groups * t * Ntil * Ntil
+            assert (groups - 1) * world * t < npairs <= groups * world * t     # no empty group
+            assert t == 1 or world * t * Ntil * Ntil * 8 <= 2 << 30 or t == -(-npairs // world)
         mx = max(d["useful_flops_schur"] for d in ds)
         assert mx <= cost.sum() / world + cost.max() + 1e-6
         # tiles mode: all blocks on every rank
