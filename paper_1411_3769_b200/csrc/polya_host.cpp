@@ -681,45 +681,11 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
       for (size_t i = 0; i < kL.size(); ++i) kd[i] = make_int2(kL[i], kR[i]);
       c.st.kdesc = dupload(kd);
     }
-    std::vector<int32_t> ca, cb;
-#ifndef POLYA_CLS_ORDER
-#define POLYA_CLS_ORDER 0
-#endif
-    if (POLYA_CLS_ORDER == 1) {   // experiment: classes along class diagonals (i, i+d)
-      for (int64_t d = 0; d < c.r; ++d)
-        for (int64_t i = 0; i + d < c.r; ++i) { ca.push_back((int32_t)i); cb.push_back((int32_t)(i + d)); }
-    } else {
-      for (int64_t i = 0; i < c.r; ++i)
-        for (int64_t j = i; j < c.r; ++j) { ca.push_back((int32_t)i); cb.push_back((int32_t)j); }
-    }
+    std::vector<int32_t> ca, cb;   // chunk classes {i <= j}, row-major
+    for (int64_t i = 0; i < c.r; ++i)
+      for (int64_t j = i; j < c.r; ++j) { ca.push_back((int32_t)i); cb.push_back((int32_t)j); }
     c.st.cls_a = dupload(ca);
     c.st.cls_b = dupload(cb);
-#ifndef POLYA_ITEM_ORDER
-#define POLYA_ITEM_ORDER 0
-#endif
-    if (POLYA_ITEM_ORDER > 0) {   // experiment: items of a pair blocked by chunk groups of POLYA_ITEM_ORDER
-      // chunks, so that the items in flight touch few operand tiles (L2 reuse at large K_pair)
-      const int64_t B = POLYA_ITEM_ORDER, ncl = c.ncls;
-      auto grp = [&](int64_t cls) { return std::make_pair(ca[cls] / B, cb[cls] / B); };
-      std::vector<int64_t> ord(ncl);
-      for (int64_t q = 0; q < ncl; ++q) ord[q] = q;
-      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return grp(x) < grp(y); });
-      std::vector<int64_t> gstart{0};   // class-group boundaries in ord
-      for (int64_t q = 1; q < ncl; ++q)
-        if (grp(ord[q]) != grp(ord[q - 1])) gstart.push_back(q);
-      gstart.push_back(ncl);
-      std::vector<int2> full, upper;
-      for (size_t g1 = 0; g1 + 1 < gstart.size(); ++g1)
-        for (size_t g2 = 0; g2 + 1 < gstart.size(); ++g2)
-          for (int64_t u = gstart[g1]; u < gstart[g1 + 1]; ++u)
-            for (int64_t v = gstart[g2]; v < gstart[g2 + 1]; ++v) {
-              const int32_t sc = (int32_t)ord[u], tc = (int32_t)ord[v];
-              full.push_back(make_int2(sc, tc));
-              if (sc <= tc) upper.push_back(make_int2(sc, tc));
-            }
-      c.st.item_full = dupload(full);
-      c.st.item_upper = dupload(upper);
-    }
     c.st.counter = dalloc<unsigned long long>(1);
   }
 
@@ -798,7 +764,7 @@ void free_ctx(Ctx& c) {
                 c.d_items_T, c.d_terms_T, c.d_sc_dst, c.d_sc_src, c.d_sc_w, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
                 c.st.pair_kbeg, c.st.pair_item, c.st.kdesc,
-                c.st.cls_a, c.st.cls_b, c.st.item_full, c.st.item_upper, c.st.counter, c.d_coef, c.d_ws_items, c.d_ws_terms, c.d_items_T0,
+                c.st.cls_a, c.st.cls_b, c.st.counter, c.d_coef, c.d_ws_items, c.d_ws_terms, c.d_items_T0,
                 c.d_terms_T0, c.d_items_S0, c.d_terms_S0, c.d_CL};
   for (void* p : ps)
     if (p) cudaFree(p);

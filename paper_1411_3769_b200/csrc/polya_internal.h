@@ -45,8 +45,6 @@ struct SchurTables {
   int2* kdesc = nullptr;          // [nk] arena matrix ids (L_k, R_k) of the pair k-lists for K4
   int32_t* cls_a = nullptr;       // [ncls] chunk index i of class (i <= j)
   int32_t* cls_b = nullptr;       // [ncls] chunk index j
-  int2* item_full = nullptr;      // [ncls^2] (sc, tc) of the k-th item of an off-diagonal pair (item order)
-  int2* item_upper = nullptr;     // [ncls(ncls+1)/2] same for a diagonal pair (sc <= tc); null: row-major
   unsigned long long* counter = nullptr;  // dynamic work counter
 };
 
@@ -129,6 +127,7 @@ struct Ctx {
   cudaEvent_t comb_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // assembled[2], reduced[2]
   std::string last_error;
   int64_t launches = 0;
+  int64_t k4_ctas = 0;   // resident K4 CTAs on the device (computed at the first assembly)
 };
 
 // Tile groups of the block-sharded combine (SHARD_BLOCKS): group g holds pair tiles

@@ -36,30 +36,34 @@ namespace polya {
 namespace {
 
 constexpr int Q = kChunk;  // 8
-#ifndef SCHUR_KB
-#define SCHUR_KB 8
-#endif
-constexpr int KB = SCHUR_KB;   // k terms per pipeline stage (a multiple of 4 dividing kKStage)
-static_assert(KB % 4 == 0 && kKStage % KB == 0, "stage size");
+constexpr int KB = 8;      // k terms per pipeline stage (= kKStage: the k-lists are padded to whole stages)
+static_assert(KB % 8 == 0 && kKStage % KB == 0, "stage size: two halves of whole k4 steps");
 constexpr int NCW = 4;     // consumer (DMMA) warps: each a 4x4 grid of 8x8 tiles of the 64x64 sub-block
-#ifdef NT_OVERRIDE
-constexpr int NT = NT_OVERRIDE;
-#else
 constexpr int NT = (NCW + 1) * 32;  // + one producer warp (cp.async into an mbarrier ring)
-#endif
-#ifndef SCHUR_NSTAGE
-#define SCHUR_NSTAGE 2   // v23: 2 slots so that 4 CTAs fit an SM (v20: 4 slots, 3 CTAs/SM; +2 % at cfg 4)
-#endif
-constexpr int NSTAGE = SCHUR_NSTAGE;  // ring depth
-constexpr int KS = 68;     // doubles per staged 8x8 tile: 64 + 4 pad (conflict-free LDS.64 fragments)
-constexpr int STAGE = 2 * KB * KS;  // doubles per stage: L[8 k][8 x][8 y] + R[8 k][8 z][8 w]
-#ifndef SCHUR_SPLIT_FULL
-#define SCHUR_SPLIT_FULL 1   // v24: a second `full` barrier per slot: consumers start on the first half of a stage
-#endif
-#ifndef SCHUR_SPLIT_EMPTY
-#define SCHUR_SPLIT_EMPTY 0   // experiment (with SCHUR_SPLIT_FULL): release / refill a slot by halves
-#endif
-constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 4 * NSTAGE * sizeof(uint64_t);
+constexpr int NSTAGE = 2;  // ring depth: 2 slots so that 4 CTAs fit an SM (v20: 4 slots at 3 CTAs/SM, 2 % slower)
+constexpr int kMinBlocks = 4;   // v23: 4 CTAs/SM (96 registers, a few spills outside the DMMA loop)
+// Stage layout (v25): per operand (L, then R) 8 k-terms x 8 x 8 doubles, dense (4 KB).  Each tile is
+// split into its 4 row pairs p = x >> 1 (128 bytes); k-term t's row pair p sits at byte
+//   2048 (t >> 2) + 512 p + 128 (t & 3),   inside it row x & 1 at + 64, the 16-byte column pair
+//   y >> 1 at + 16 ((y >> 1) ^ (t & 3)) (an XOR swizzle: the same pattern as TMA's 64-byte swizzle,
+//   whose phase is address bits 7-8 = t & 3 here),
+// so that (i) the 4 k-terms of a DMMA k-step and the 4 (x & 1, y & 1) rows of a half-warp's fragment
+// loads hit 16 distinct bank slots, (ii) each producer copy instruction (one tile) fills 4 whole
+// 128-byte bank rows, and (iii) a warp's M-tiles (which differ in p only, see orient<>) sit at constant
+// 512-byte offsets: one address register per operand.  v24's padded 68-double tiles were conflict-free
+// for the fragment loads only: its 544-byte tile starts made every cp.async take 2-3x the wavefronts.
+constexpr int OPB = KB * 64 * 8;         // bytes per operand per stage (4096)
+constexpr int STAGEB = 2 * OPB;          // bytes per stage (8192)
+constexpr int STAGE = STAGEB / 8;        // doubles per stage
+__host__ __device__ constexpr int stage_byte(int t, int x, int y) {
+  return 2048 * (t >> 2) + 512 * (x >> 1) + 128 * (t & 3) + 64 * (x & 1) + 16 * ((y >> 1) ^ (t & 3)) + 8 * (y & 1);
+}
+// per slot: full (first half of the stage's k-terms landed), full2 (second half), empty (consumed)
+constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 3 * NSTAGE * sizeof(uint64_t);
+
+#ifndef SCHUR_EXP
+#define SCHUR_EXP 0   // tools-only timing variants (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either
+#endif                // (results wrong by construction: never a bench value)
 
 struct SchurArgs {
   const double* arena;
@@ -68,8 +72,6 @@ struct SchurArgs {
   int np, n, ncls, npl;
   const int32_t* cls_a;
   const int32_t* cls_b;
-  const int2* item_full;    // optional item-order tables (POLYA_ITEM_ORDER experiment); null: row-major
-  const int2* item_upper;
   const int32_t* pair_h;
   const int32_t* pair_h2;
   const int64_t* pair_kbeg;
@@ -103,49 +105,30 @@ __device__ __forceinline__ int64_t svec_idx(int a, int b, int n) {
   return (int64_t)n + (int64_t)(o - 1) * n - (int64_t)(o - 1) * o / 2 + a;
 }
 
-// Shared G-block address of local (a,b,c,d): 16-double groups indexed by (a, b, c>>1), the low
-// 4 bits (c&1, d) XOR-swizzled by a GF(2)-linear function of (a, b, c>>1), chosen by search
-// so that the 32 lanes of every fold orientation hit distinct bank pairs.
-// Every field is a bit field or an XOR, so the address splits into per-coordinate terms:
-//   gs(a,b,c,d) = Ta(a) ^ Tb(b) ^ Tc(c) ^ d.
-__device__ __forceinline__ int Ta(int a) {
-  const int a0 = a & 1, a1 = (a >> 1) & 1, a2 = a >> 2;
-  return (a << 9) ^ ((a0 ^ a1) | (a2 << 1) | ((a0 ^ a2) << 2) | ((a0 ^ a1 ^ a2) << 3));
+// Shared G-block address of local (a,b,c,d): a GF(2)-linear bijection of the 12 coordinate bits onto
+// [0, 4096), gs = Ta(a) ^ Tb(b) ^ Tc(c) ^ Td(d), each T a linear map of its 3 bits (columns below).
+// 64-bit shared accesses are served per half-warp (16 lanes x 8 bytes = one 128-byte bank row), so the
+// low 4 address bits (the 8-byte bank slot) must differ across the 16 lanes of each half of every
+// fold store / load: for each orientation, the 4 coordinate bits that vary across a half-warp (x0, y0,
+// w0, w1 with the tile rows of orient<>) have linearly independent low-4-bit columns (v24's swizzle
+// met this for 4 of its 8 (orientation, packing) patterns only).
+// Columns found by search; tests/test_layout_banks.py re-checks the folds, the bijection and bounds
+// the epilogue's read conflicts.
+__device__ __forceinline__ int lin3(int v, int c0, int c1, int c2) {
+  return ((v & 1) ? c0 : 0) ^ ((v & 2) ? c1 : 0) ^ ((v & 4) ? c2 : 0);
 }
-__device__ __forceinline__ int Tb(int b) {
-  const int b0 = b & 1, b1 = (b >> 1) & 1, b2 = b >> 2;
-  return (b << 6) ^ ((b1 ^ b2) | ((b0 ^ b1 ^ b2) << 1) | (b2 << 2) | ((b0 ^ b1 ^ b2) << 3));
-}
-__device__ __forceinline__ int Tc(int c) {
-  const int c1 = c >> 1, e0 = c1 & 1, e1 = c1 >> 1;
-  return (c1 << 4) ^ ((c & 1) << 3) ^ (e1 | ((e0 ^ e1) << 1) | (e0 << 2));
-}
+__device__ __forceinline__ int Ta(int a) { return lin3(a, 11, 3, 10); }
+__device__ __forceinline__ int Tb(int b) { return lin3(b, 7, 21, 32); }
+__device__ __forceinline__ int Tc(int c) { return lin3(c, 65, 135, 264); }
+__device__ __forceinline__ int Td(int d) { return lin3(d, 525, 1027, 2048); }
 
-// Operand tiles are re-read by every item of a pair: keep them in L2 (evict_last), while the
-// 11+ GB of G streamed out per call is stored evict-first (st.global.cs) so it does not flush them.
-#ifndef SCHUR_CA
-#define SCHUR_CA 0   // experiment: L1-allocating cp.async (.ca) instead of .cg
-#endif
-#ifndef SCHUR_L2HINTS
-#define SCHUR_L2HINTS 0   // bit 1: evict-last operand loads, bit 2: evict-first G stores (v13: 3 = +0.5 ms)
-#endif
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, uint64_t pol) {
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  if (SCHUR_L2HINTS & 1)
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem_src), "l"(pol));
-  else if (SCHUR_CA)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
-  else
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void st_g(double* p, double v) {
   POLYA_ASSERT(p != nullptr);
-  if (SCHUR_L2HINTS & 2) __stcs(p, v); else *p = v;
+  *p = v;
 }
 __device__ __forceinline__ unsigned sptr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -158,32 +141,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(sptr(bar)) : "memory");
 }
-#ifndef SCHUR_WAIT_MODE
-#define SCHUR_WAIT_MODE 0   // 0: try_wait (hardware-chosen suspend), 1: test_wait spin, 2: try_wait with a
-#endif                      //    SCHUR_WAIT_NS suspend-time hint (timing experiments)
-#ifndef SCHUR_WAIT_NS
-#define SCHUR_WAIT_NS 100
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-#if SCHUR_WAIT_MODE == 1
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          sptr(bar)),
-      "r"(parity)
-      : "memory");
-#elif SCHUR_WAIT_MODE == 2
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          sptr(bar)),
-      "r"(parity), "n"(SCHUR_WAIT_NS)
-      : "memory");
-#else
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
           sptr(bar)),
       "r"(parity)
       : "memory");
-#endif
 }
 // Consumer phases (each fold of an orientation, each item's epilogue) are ordered by one mbarrier
 // with one arrival per consumer warp: a warp arrives when its part of a phase is done and waits
@@ -222,11 +185,7 @@ __device__ __forceinline__ ItemInfo decode_item(const SchurArgs& p, int64_t item
   it.h = __ldg(p.pair_h + lo);
   it.h2 = __ldg(p.pair_h2 + lo);
   const int64_t rem = item - __ldg(p.pair_item + lo);
-  if (p.item_full) {
-    const int2 st = __ldg((it.h != it.h2 ? p.item_full : p.item_upper) + rem);
-    it.sc = st.x;
-    it.tc = st.y;
-  } else if (it.h != it.h2) {
+  if (it.h != it.h2) {
     it.sc = (int)(rem / p.ncls);
     it.tc = (int)(rem - (int64_t)it.sc * p.ncls);
   } else {
@@ -263,17 +222,6 @@ __device__ __forceinline__ void roles(int o, const I& it, int& cX, int& cY, int&
   cZ = (o & 1) ? it.ck : it.cl;
 }
 
-#ifndef SCHUR_EXP
-#define SCHUR_EXP 0   // timing experiments only (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either,
-                      // 4 = no operand loads (results wrong by construction: never a bench value)
-#endif
-#ifndef SCHUR_EARLY_REL
-#define SCHUR_EARLY_REL 0
-#endif
-#ifndef SCHUR_MINB
-#define SCHUR_MINB 4     // v23: 4 CTAs/SM (96 registers, a few spills outside the DMMA loop)
-#endif
-
 // One G entry of the item from the folded block: canonical summation order (direct, s-swap,
 // t-swap, both) so that an entry and its mirror image are bitwise equal.  Table entries are
 // {svec index, Gs term direct, Gs term swapped, has swap}.
@@ -290,23 +238,23 @@ __device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
 
 // One orientation of an item on the consumer warps: the raw sub-block
 // Raw[(x,y),(z,w)] = sum_k L_k[x,y] R_k[z,w] (x in cX, y in cY, z in cZ, w in cW) over the
-// item's nstage ring stages, then folded into Gs.  The valid (x, y) rows form MT M-tiles of 8
-// and the valid (z, w) columns NT N-tiles; the 4 warps split both in halves (2 x 2), so each warp
-// owns MI = MT/2 M-tiles and NJ = NT/2 N-tiles whatever the raggedness:
-//   PY = 0: M-tile m is x = m with rows y = 0..7 (MT = 8, or 4 when cX is a ragged chunk with <= 4
-//           valid x -- the 4 invalid x are not computed at all);
-//   PY = 1: cY is ragged (<= 4 valid y): M-tile m packs x = 2m + (g>>2) with y = g&3 (MT = 4 or 2);
-// and likewise on the N side (z, w) with PW, where the accumulator column 2t+e is w = 2t+e
-// (PW = 0) or z = 2n+(t>>1), w = 2(t&1)+e (PW = 1).
-template <int MI, int NJ, int PY, int PW>
+// item's nstage ring stages, then folded into Gs.  MMA rows are M-tiles (p, q) of 8 rows
+// g -> (x, y) = (2p + (g & 1), 4q + (g >> 1)), columns N-tiles (p', q') the same way over (z, w).
+// Full chunks: 8 M-tiles, warp row wm (of the 2 x 2 warp grid) takes q = wm, p = 0..3; a ragged x
+// chunk (<= 4 valid x) needs p < 2 only (q = wm, p = 0..1), a ragged y chunk (<= 4 valid y) q = 0
+// only (p = 2 wm + 0..1), both one tile (q = 0, p = wm) -- invalid rows are never multiplied.  A
+// warp's tiles differ in p only, so their fragments sit at +512-byte steps of one lane offset.
+template <int MI, int NJ, int RY, int RW>
 __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
                                        uint64_t* empty, uint32_t& cnt, int nstage, int o, bool first,
                                        uint64_t* pbar, uint32_t& nph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int m0 = MI * (warp >> 1), n0 = NJ * (warp & 1);   // the warp's first M-tile and N-tile
-  constexpr int AST = PY ? 2 * Q : Q, BST = PW ? 2 * Q : Q;   // fragment strides per tile
-  const int aoff = PY ? (2 * m0 + (g >> 2)) * Q + (g & 3) : m0 * Q + g;
-  const int boff = PW ? (2 * n0 + (g >> 2)) * Q + (g & 3) : n0 * Q + g;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int qm = RY ? 0 : wm, pm = RY ? MI * wm : 0;   // the warp's M-tiles: (pm + i, qm)
+  const int qn = RW ? 0 : wn, pn = RW ? NJ * wn : 0;   // N-tiles: (pn + j, qn)
+  // lane offsets (doubles, k-step 0, tile 0) of A[g][k=t] and B[k=t][n=g] in a stage
+  const int oa = stage_byte(t, 2 * pm + (g & 1), 4 * qm + (g >> 1)) / 8;
+  const int ob = (OPB + stage_byte(t, 2 * pn + (g & 1), 4 * qn + (g >> 1))) / 8;
   double acc[MI][NJ][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
@@ -314,59 +262,24 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int s = 0; s < nstage; ++s) {
     const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
-#if SCHUR_EXP & 64   // experiment: histogram of consumer waits on `full` by stage index (warp 0, lane 0)
-    const long long w0 = clock64();
     mbar_wait(full + slot, ph);
-    if (tid == 0) {
-      const int bkt = s < 4 ? s : (s == nstage - 1 ? 5 : 4);
-      atomicAdd(p.G + (int64_t)p.npl * p.Ntil * p.Ntil + bkt, (double)(clock64() - w0));
-      atomicAdd(p.G + (int64_t)p.npl * p.Ntil * p.Ntil + 8 + bkt, 1.0);
-    }
-#else
-    mbar_wait(full + slot, ph);
-#endif
-    const double* fA = smem + slot * STAGE + t * KS + aoff;             // A[m][k=t]
-    const double* fB = smem + slot * STAGE + KB * KS + t * KS + boff;   // B[k=t][n]
-#if SCHUR_EARLY_REL
-    // experiment: every fragment of the stage into registers first, release the slot (the
-    // arrive's release semantics order the loads before the producer's refill), then the DMMAs
-    double a[KB / 4][MI], b[KB / 4][NJ];
+    const double* fA = smem + slot * STAGE + oa;
+    const double* fB = smem + slot * STAGE + ob;
 #pragma unroll
     for (int k4 = 0; k4 < KB / 4; ++k4) {
-#pragma unroll
-      for (int i = 0; i < MI; ++i) a[k4][i] = fA[k4 * 4 * KS + i * AST];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) b[k4][j] = fB[k4 * 4 * KS + j * BST];
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + slot);
-#pragma unroll
-    for (int k4 = 0; k4 < KB / 4; ++k4)
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[k4][i], b[k4][j]);
-#else
-#pragma unroll
-    for (int k4 = 0; k4 < KB / 4; ++k4) {
-      if (SCHUR_SPLIT_FULL && k4 == KB / 8) mbar_wait(full + 2 * NSTAGE + slot, ph);   // second half landed
+      if (k4 == KB / 8) mbar_wait(full + 2 * NSTAGE + slot, ph);   // the stage's second half has landed
       double a[MI], b[NJ];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = fA[k4 * 4 * KS + i * AST];
+      for (int i = 0; i < MI; ++i) a[i] = fA[k4 * 256 + i * 64];   // + 2048 bytes per k-step, 512 per tile
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) b[j] = fB[k4 * 4 * KS + j * BST];
+      for (int j = 0; j < NJ; ++j) b[j] = fB[k4 * 256 + j * 64];
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      if (SCHUR_SPLIT_EMPTY && k4 == KB / 8 - 1) {   // the first half is in registers: release it
-        __syncwarp();
-        if (lane == 0) mbar_arrive(full + 3 * NSTAGE + slot);
-      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + slot);
-#endif
     ++cnt;
   }
   if (SCHUR_EXP & 2) {   // timing experiment: no fold, no epilogue (a never-taken sink keeps the DMMAs)
@@ -379,23 +292,22 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
     return;
   }
   phase_wait_prev(pbar, nph);   // the previous fold / the previous item's epilogue is done with Gs
-  // fold: acc[i][j][e] = Raw(x, y, z, w) -> Gs[(a,b,c,d)(o)], gs = Ta(a)^Tb(b)^Tc(c)^d split into
-  // per-coordinate terms: x -> (o&2 ? Ta : Tb), w -> (o&2 ? Tb : Ta), y -> (o&1 ? id : Tc),
-  // z -> (o&1 ? Tc : id)   (o0: (a,b,c,d) = (w,x,y,z), o1: (w,x,z,y), o2: (x,w,y,z), o3: (x,w,z,y))
+  // fold: acc[i][j][e] = Raw(x, y, z, w) -> Gs[(a,b,c,d)(o)], gs = Ta(a)^Tb(b)^Tc(c)^Td(d) split into
+  // per-coordinate terms: x -> (o&2 ? Ta : Tb), w -> (o&2 ? Tb : Ta), y -> (o&1 ? Td : Tc),
+  // z -> (o&1 ? Tc : Td)   (o0: (a,b,c,d) = (w,x,y,z), o1: (w,x,z,y), o2: (x,w,y,z), o3: (x,w,z,y));
+  // accumulator column 2t+e of N-tile (p', q') is (z, w) = (2p' + e, 4q' + t)
   int bx[MI], bz[NJ][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
-    const int x = PY ? 2 * (m0 + i) + (g >> 2) : m0 + i;
-    const int y = PY ? (g & 3) : g;
-    bx[i] = ((o & 2) ? Ta(x) : Tb(x)) ^ ((o & 1) ? y : Tc(y));
+    const int x = 2 * (pm + i) + (g & 1), y = 4 * qm + (g >> 1);
+    bx[i] = ((o & 2) ? Ta(x) : Tb(x)) ^ ((o & 1) ? Td(y) : Tc(y));
   }
 #pragma unroll
   for (int j = 0; j < NJ; ++j)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int z = PW ? 2 * (n0 + j) + (t >> 1) : n0 + j;
-      const int w = PW ? 2 * (t & 1) + e : 2 * t + e;
-      bz[j][e] = ((o & 1) ? Tc(z) : z) ^ ((o & 2) ? Tb(w) : Ta(w));
+      const int z = 2 * (pn + j) + e, w = 4 * qn + t;
+      bz[j][e] = ((o & 1) ? Tc(z) : Td(z)) ^ ((o & 2) ? Tb(w) : Ta(w));
     }
   if (first) {
 #pragma unroll
@@ -421,21 +333,14 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
   phase_arrive(pbar, nph);
 }
 
-// (M side, N side) code -> instantiation: code 0: 8 full tiles (4 per warp), 1: 4 unpacked tiles
-// (ragged x / z), 2: 4 packed tiles (ragged y / w), 3: 2 packed tiles (both ragged).
-#define ORIENT_M(MC, MI, PY)                                                                          \
-  case MC * 4 + 0: orient<MI, 4, PY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
-  case MC * 4 + 1: orient<MI, 2, PY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
-  case MC * 4 + 2: orient<MI, 2, PY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
-  case MC * 4 + 3: orient<MI, 1, PY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break;
-#ifndef SCHUR_DISPATCH_INLINE
-#define SCHUR_DISPATCH_INLINE 1   // measured: the noinline call cost 1.7 ms (cfg 4) and 34 ms (cfg 5)
-#endif
-#if SCHUR_DISPATCH_INLINE
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
+// (M side, N side) code -> instantiation: code 0: 8 tiles (4 per warp), 1: 4 tiles of a ragged x / z
+// chunk, 2: 4 tiles of a ragged y / w chunk, 3: 2 tiles (both ragged).
+#define ORIENT_M(MC, MI, RY)                                                                          \
+  case MC * 4 + 0: orient<MI, 4, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 4 + 1: orient<MI, 2, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 4 + 2: orient<MI, 2, RY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 4 + 3: orient<MI, 1, RY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break;
+__device__ __forceinline__   // inlined: the out-of-line call cost 1.7 ms (cfg 4) and 34 ms (cfg 5)
 void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
                                              uint64_t* empty, uint32_t& cnt, int nstage, int o, bool first,
                                              uint64_t* pbar, uint32_t& nph) {
@@ -448,11 +353,12 @@ void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uin
 }
 #undef ORIENT_M
 
-__global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
+__global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
   extern __shared__ __align__(16) double smem[];
   double* Gs = smem + NSTAGE * STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Gs + Q * Q * Q * Q);   // stage landed (32 producer arrivals)
+  uint64_t* full = reinterpret_cast<uint64_t*>(Gs + Q * Q * Q * Q);   // first half landed (32 + 1 arrivals)
   uint64_t* empty = full + NSTAGE;                                      // stage consumed (NCW arrivals)
+  // full + 2 NSTAGE: second half landed (32 cp.async arrivals)
   __shared__ unsigned char s_diag[64][2];  // (lc, ld) of local pairs ordered by (ld-lc, lc)
   __shared__ int4 s_rt[2][64], s_ct[2][64];   // epilogue tables of the item's valid row / column pairs
   __shared__ int s_nrc[2][2];                  // their counts (double-buffered by item parity)
@@ -469,8 +375,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(full + i, 33);   // 32 cp.async completions + lane 0's release of s_info
-      mbar_init(full + 2 * NSTAGE + i, 32);   // SCHUR_SPLIT_FULL: the second half's completions
-      mbar_init(full + 3 * NSTAGE + i, NCW);  // SCHUR_SPLIT_EMPTY: the first half consumed
+      mbar_init(full + 2 * NSTAGE + i, 32);   // the second half's completions
       mbar_init(empty + i, NCW);
     }
     mbar_init(&s_pbar, NCW);
@@ -483,9 +388,9 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
   // already holds the index, decode and first k-descriptors of item i+1, so no stage waits on
   // an atomic, a table lookup or a descriptor load.  The consumers learn each item from s_info.
   if (warp == NCW) {
-    // ===== producer warp: 16-byte cp.async chunks (row sr, column pair sc2) of all 16 tiles ====
+    // ===== producer warp: 16-byte cp.async chunks (row sr, column pair sc2) of all 16 tiles into
+    // the swizzled stage layout (stage_byte) =====
     const int sr = lane >> 2, sc2 = lane & 3;
-    const uint64_t pol = l2_evict_last_policy();
     uint32_t cnt = 0;
     unsigned long long got = 0;
     if (lane == 0) got = atomicAdd(p.counter, 1ULL);
@@ -523,7 +428,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
           int2 dnext = dfirst;
           if (s + 1 < it.nstage && lane < KB) dnext = __ldg(p.kdesc + it.kb + (int64_t)(s + 1) * KB + lane);
           const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
-          mbar_wait((SCHUR_SPLIT_EMPTY ? full + 3 * NSTAGE : empty) + slot, ph ^ 1);
+          mbar_wait(empty + slot, ph ^ 1);
           if (first_stage && lane == 0) {
             SlotInfo si;
             si.item = item; si.pl = it.pl; si.h = it.h; si.h2 = it.h2; si.sc = it.sc; si.tc = it.tc;
@@ -531,28 +436,21 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
             s_info[slot] = si;
           }
           first_stage = false;
-          double* T = smem + slot * STAGE + sr * Q + 2 * sc2;
+          char* T = reinterpret_cast<char*>(smem + slot * STAGE);
 #pragma unroll
           for (int kk = 0; kk < KB; ++kk) {
             const unsigned idL = (unsigned)__shfl_sync(0xffffffffu, dcur.x, kk);
             const unsigned idR = (unsigned)__shfl_sync(0xffffffffu, dcur.y, kk);
             POLYA_ASSERT(idL < p.nmats && idR < p.nmats);
-            if (SCHUR_SPLIT_EMPTY && kk == KB / 2) mbar_wait(empty + slot, ph ^ 1);   // second half free
-            if (!(SCHUR_EXP & 4)) {   // experiment bit 4: no operand loads (timing of the DMMA side only)
-              cp_async16(T + kk * KS, p.arena + (uint64_t)idL * p.ms32 + offL, pol);
-              cp_async16(T + KB * KS + kk * KS, p.arena + (uint64_t)idR * p.ms32 + offR, pol);
-            }
-            if (SCHUR_SPLIT_FULL && kk == KB / 2 - 1) {   // first half of the k-terms: consumers may start
+            const int db = stage_byte(kk, sr, 2 * sc2);
+            cp_async16(T + db, p.arena + (uint64_t)idL * p.ms32 + offL);
+            cp_async16(T + OPB + db, p.arena + (uint64_t)idR * p.ms32 + offR);
+            if (kk == KB / 2 - 1) {   // first half of the k-terms: consumers may start on it
               cp_async_mbar_arrive(full + slot);
               if (lane == 0) mbar_arrive(full + slot);   // releases s_info[slot]
             }
           }
-          if (SCHUR_SPLIT_FULL) {
-            cp_async_mbar_arrive(full + 2 * NSTAGE + slot);
-          } else {
-            cp_async_mbar_arrive(full + slot);
-            if (lane == 0) mbar_arrive(full + slot);   // releases s_info[slot]
-          }
+          cp_async_mbar_arrive(full + 2 * NSTAGE + slot);
           dcur = dnext;
           ++cnt;
         }
@@ -606,7 +504,7 @@ __global__ void __launch_bounds__(NT, SCHUR_MINB) k_schur(const SchurArgs p) {
         if (valid) {
           const int pos = base + __popc(bal & ((1u << lane) - 1u));
           tab[pos] = rows ? make_int4((int)svec_idx(A, B, n), Ta(u1) ^ Tb(u2), Ta(u2) ^ Tb(u1), dg && u1 != u2)
-                          : make_int4((int)svec_idx(A, B, n), Tc(u1) ^ u2, Tc(u2) ^ u1, dg && u1 != u2);
+                          : make_int4((int)svec_idx(A, B, n), Tc(u1) ^ Td(u2), Tc(u2) ^ Td(u1), dg && u1 != u2);
         }
         base += __popc(bal);
       }
@@ -696,18 +594,19 @@ cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, 
   if (i1 <= i0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(c.st.counter, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur, NT, kSmemBytes);
-  per_sm = std::max(per_sm, 1);
-  const int64_t want = std::min<int64_t>((int64_t)sms * per_sm, i1 - i0);
+  if (c.k4_ctas == 0) {   // once per context: shared-memory attribute and resident CTAs (persistent grid)
+    e = cudaFuncSetAttribute(k_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur, NT, kSmemBytes);
+    c.k4_ctas = (int64_t)sms * std::max(per_sm, 1);
+  }
+  const int64_t want = std::min<int64_t>(c.k4_ctas, i1 - i0);
   SchurArgs a;
   a.arena = c.arena; a.ms = c.mstride; a.ms32 = (unsigned)c.mstride; a.np = (int)c.np; a.n = (int)c.nbas; a.ncls = (int)c.ncls;
   a.npl = (int)c.npairs_local;
-  a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.item_full = c.st.item_full; a.item_upper = c.st.item_upper; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
+  a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
   a.pair_kbeg = c.st.pair_kbeg; a.pair_item = c.st.pair_item; a.kdesc = c.st.kdesc;
   a.item0 = i0; a.item1 = i1; a.counter = c.st.counter;
   a.G = G; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil; a.nmats = c.nmats;
