@@ -147,7 +147,10 @@ __device__ bool smem_chol(double* S, int n) {
 // W_b = Z_b^{-1} via Cholesky Z = L L^T, X = L^{-1} in place (from X L = I, column by column from
 // the last: X_ij = -(sum_{k=j+1..i} X_ik L_kj) / L_jj), then W = X^T X; exactly symmetric.
 // Shared memory: n^2 + n doubles (n <= 168).
-__global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restrict__ W, int* __restrict__ fail) {
+// linv != 0: W_b = L^{-1} instead (lower triangle, zeros above; a NaN in W_b[0] if Z_b is not positive
+// definite), the congruence factor of the step length (step_len).
+__global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restrict__ W, int* __restrict__ fail,
+                            int linv = 0) {
   extern __shared__ double sm[];
   double* S = sm;           // n*n: L, then X = L^{-1} (lower)
   double* col = sm + n * n; // n: the column of X being formed
@@ -155,7 +158,10 @@ __global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restr
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[e] = Z[b * nn + e];
   __syncthreads();
   if (!smem_chol(S, n)) {
-    if (threadIdx.x == 0) atomicExch(fail, 1);
+    if (threadIdx.x == 0) {
+      if (fail) atomicExch(fail, 1);
+      if (linv) W[b * nn] = __longlong_as_double(0x7ff8000000000000LL);
+    }
     return;
   }
   for (int j = n - 1; j >= 0; --j) {
@@ -169,6 +175,13 @@ __global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restr
     if (threadIdx.x == 0) S[j * n + j] = 1.0 / S[j * n + j];
     __syncthreads();
   }
+  if (linv) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      W[b * nn + e] = j <= i ? S[e] : 0.0;
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
     if (i > j) continue;
@@ -179,12 +192,138 @@ __global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restr
   }
 }
 
-// Reading R5: t_b = sup{t in [0, tcap] : S_b + t dS_b positive definite}, by bisection on the
-// Cholesky test (60 halvings); t_b = tcap if S_b + tcap dS_b is positive definite.
+// Reading R5 as written: t_b = min(tcap, 1 / max(0, -lambda_min(M_b))), M_b = L_b^{-1} dS_b L_b^{-T}
+// (S_b = L_b L_b^T; M_b formed by k_block_inv(linv) + two k_bgemm).  One CTA per block: the symmetric
+// part of M_b, packed lower in shared memory ((n^2 + n)/2 + 4n doubles, n <= 168), is reduced to
+// tridiagonal form by Householder reflections (A <- H A H, H = I - tau v v^T; LAPACK dsytd2's
+// algorithm), then lambda_min by multisection on the Sturm count of the tridiagonal (256 trial points
+// per round, one per thread).  Non-finite M_b (S_b not positive definite, e.g. a singular X on the
+// boundary of the cone): t_b = -1, for which step_len runs the bisection kernel k_block_tmax.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int q = 0; q < nw; ++q) s += red[q];
+  return s;
+}
+__device__ __forceinline__ int sturm_count(int n, const double* d, const double* e, double lam) {
+  int cnt = 0;
+  double q = d[0] - lam;
+  for (int i = 0;; ++i) {
+    if (q == 0.0) q = -1e-300;
+    cnt += q < 0.0;
+    if (i + 1 == n) break;
+    q = (d[i + 1] - lam) - e[i] * e[i] / q;
+  }
+  return cnt;
+}
+__global__ void __launch_bounds__(256) k_block_lmin(int n, const double* __restrict__ M, double tcap,
+                                                    double* __restrict__ tout) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double* P = sm;                           // packed lower: (i, j <= i) at i (i + 1) / 2 + j
+  double* v = P + (n * (n + 1)) / 2;
+  double* w = v + n;
+  double* d = w + n;
+  double* e = d + n;
+  __shared__ double red[32];
+  __shared__ int s_j;
+  const int64_t b = blockIdx.x, nn = (int64_t)n * n;
+  const double* Mb = M + b * nn;
+  int bad = 0;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int i = idx / n, j = idx - i * n;
+    if (j > i) continue;
+    const double x = 0.5 * (Mb[(int64_t)i * n + j] + Mb[(int64_t)j * n + i]);
+    bad |= !isfinite(x);
+    P[i * (i + 1) / 2 + j] = x;
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) tout[b] = -1.0;   // S_b not positive definite: step_len falls back to k_block_tmax
+    return;
+  }
+  auto A = [&](int i, int j) -> double& { return i >= j ? P[i * (i + 1) / 2 + j] : P[j * (j + 1) / 2 + i]; };
+  for (int k = 0; k + 2 < n; ++k) {
+    // x = A[k+1.., k]; e_k = -sign(x_0) |x|; v = x - e_k e_1, tau = 2 / v^T v
+    double xs = 0.0;
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) xs += A(i, k) * A(i, k);
+    const double a2 = block_sum(xs, red);
+    const double x0 = A(k + 1, k);
+    const double alpha = sqrt(a2), ek = x0 >= 0.0 ? -alpha : alpha;
+    if (tid == 0) { d[k] = A(k, k); e[k] = ek; }
+    if (a2 == 0.0) continue;   // already reduced (uniform)
+    const double v0 = x0 - ek, tau = 2.0 / (a2 - x0 * x0 + v0 * v0);
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) v[i] = i == k + 1 ? v0 : A(i, k);
+    __syncthreads();
+    // p = tau A v (rows k+1.., a warp per row), then w = p - (tau / 2)(p^T v) v
+    for (int i = k + 1 + warp; i < n; i += nw) {
+      double acc = 0.0;
+      for (int j = k + 1 + lane; j < n; j += 32) acc += A(i, j) * v[j];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) w[i] = tau * acc;
+    }
+    __syncthreads();
+    double pv = 0.0;
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) pv += w[i] * v[i];
+    const double K = 0.5 * tau * block_sum(pv, red);
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) w[i] -= K * v[i];
+    __syncthreads();
+    // A <- A - v w^T - w v^T on the trailing lower triangle
+    for (int i = k + 1 + warp; i < n; i += nw)
+      for (int j = k + 1 + lane; j <= i; j += 32) P[i * (i + 1) / 2 + j] -= v[i] * w[j] + w[i] * v[j];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (n >= 2) { d[n - 2] = A(n - 2, n - 2); e[n - 2] = A(n - 1, n - 2); }
+    d[n - 1] = A(n - 1, n - 1);
+  }
+  __syncthreads();
+  // lambda_min >= 0: no bound on t (tcap); else multisection on [Gershgorin lower bound, 0]
+  if (sturm_count(n, d, e, 0.0) == 0) {
+    if (tid == 0) tout[b] = tcap;
+    return;
+  }
+  double lo = 0.0;
+  {
+    double g = 1e300;
+    for (int i = tid; i < n; i += blockDim.x)
+      g = fmin(g, d[i] - (i > 0 ? fabs(e[i - 1]) : 0.0) - (i + 1 < n ? fabs(e[i]) : 0.0));
+    for (int o = 16; o > 0; o >>= 1) g = fmin(g, __shfl_xor_sync(0xffffffffu, g, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = g;
+    __syncthreads();
+    for (int q = 0; q < nw; ++q) lo = fmin(lo, red[q]);
+    lo -= 1e-12 * fabs(lo) + 1e-300;
+  }
+  double hi = 0.0;
+  for (int round = 0; round < 12 && hi - lo > 4e-16 * fmax(fabs(lo), fabs(hi)); ++round) {
+    const double step = (hi - lo) / (double)(blockDim.x + 1);
+    const double lam = lo + step * (tid + 1);
+    const int below = sturm_count(n, d, e, lam) == 0;   // lam <= lambda_min
+    if (tid == 0) s_j = -1;
+    __syncthreads();
+    if (below) atomicMax(&s_j, tid);
+    __syncthreads();
+    const int j = s_j;
+    const double nlo = lo + step * (j + 1), nhi = j + 1 < (int)blockDim.x ? lo + step * (j + 2) : hi;
+    lo = nlo;
+    hi = nhi;
+    __syncthreads();
+  }
+  if (tid == 0) tout[b] = fmin(tcap, -1.0 / (0.5 * (lo + hi)));
+}
+
+// Fallback of step_len for a block with S_b only semidefinite (no L_b^{-1}): t_b = sup{t in [0, tcap] :
+// S_b + t dS_b positive definite} by bisection on the Cholesky test (60 halvings); blocks with
+// tout[b] >= 0 already are skipped.
 __global__ void k_block_tmax(int n, const double* __restrict__ S, const double* __restrict__ dS, double tcap,
                              double* __restrict__ tout) {
   extern __shared__ double sm[];
   const int64_t nn = (int64_t)n * n, b = blockIdx.x;
+  if (tout[b] >= 0.0) return;
   auto pd = [&](double tt) -> bool {
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) sm[e] = S[b * nn + e] + tt * dS[b * nn + e];
     __syncthreads();
@@ -201,6 +340,7 @@ __global__ void k_block_tmax(int n, const double* __restrict__ S, const double* 
       if (pd(mid)) lo = mid; else hi = mid;
     }
   }
+  __syncthreads();
   if (threadIdx.x == 0) tout[b] = lo;
 }
 
@@ -558,16 +698,34 @@ void vaxpby(Ctx& c, double a, const double* x, double b, const double* y, double
   CK(cudaGetLastError());
 }
 
+// Reading R5: t = min(1, 0.98 t_max), t_max = min_b 1 / max(0, -lambda_min(L_b^{-1} dS_b L_b^{-T})).
+// Scratch: T1 (L^{-1}), T2 (L^{-1} dS), dX2 (M) -- free at this point of the step.
 double step_len(Ctx& c, Ipm* w, const double* S, const double* dS, cudaStream_t s) {
   const double frac = 0.98, tcap = 1.0 / frac;
-  const size_t sm = (size_t)c.n * c.n * sizeof(double);
-  CK(cudaFuncSetAttribute(k_block_tmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_block_tmax<<<(unsigned)c.nb, 256, sm, s>>>((int)c.n, S, dS, tcap, w->tb);
+  const size_t smi = ((size_t)c.n * c.n + c.n) * sizeof(double);
+  CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
+  k_block_inv<<<(unsigned)c.nb, 128, smi, s>>>((int)c.n, S, w->T1, nullptr, 1);
+  ++c.launches;
+  CK(cudaGetLastError());
+  bgemm(c, w->T1, 0, dS, 0, w->T2, 1.0, 0.0, s);      // L^{-1} dS
+  bgemm(c, w->T2, 0, w->T1, 1, w->dX2, 1.0, 0.0, s);  // M = L^{-1} dS L^{-T}
+  const size_t sm = ((size_t)c.n * (c.n + 1) / 2 + 4 * (size_t)c.n) * sizeof(double);
+  CK(cudaFuncSetAttribute(k_block_lmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_block_lmin<<<(unsigned)c.nb, 256, sm, s>>>((int)c.n, w->dX2, tcap, w->tb);
   ++c.launches;
   CK(cudaGetLastError());
   std::vector<double> tb(c.nb);
   CK(cudaMemcpyAsync(tb.data(), w->tb, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (*std::min_element(tb.begin(), tb.end()) < 0.0) {   // a semidefinite S_b: bisection for those blocks
+    const size_t smb = (size_t)c.n * c.n * sizeof(double);
+    CK(cudaFuncSetAttribute(k_block_tmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+    k_block_tmax<<<(unsigned)c.nb, 256, smb, s>>>((int)c.n, S, dS, tcap, w->tb);
+    ++c.launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(tb.data(), w->tb, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
   double t = tcap;
   for (double v : tb) t = std::min(t, v);
   return std::min(1.0, frac * t);
