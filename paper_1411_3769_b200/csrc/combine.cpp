@@ -175,10 +175,88 @@ void combine_free(Ctx& c) {
   c.comm_stream = nullptr;
 }
 
-// Collectives of the distributed factorisation (SHARD_CYCLIC).  With one rank they are no-ops (the
-// root's buffer is every rank's buffer); with more they need polya_nccl_init.
+// ---- in-process loopback group (polya_factor_solve_loopback): the ranks are host threads of one
+// process on one device; a collective is stream sync -> publish the buffer -> barrier -> device
+// copies from the root's buffer -> sync -> barrier.  Same call sequence as the NCCL path; a rank that
+// fails aborts the group so the others leave their barriers with an error instead of hanging.
+bool loop_barrier(LoopGroup* g) {
+  std::unique_lock<std::mutex> lk(g->m);
+  if (g->abort) return false;
+  const int64_t my = g->gen;
+  if (++g->count == g->n) {
+    g->count = 0;
+    ++g->gen;
+    g->cv.notify_all();
+  } else {
+    g->cv.wait(lk, [&] { return g->gen != my || g->abort; });
+  }
+  return !g->abort;
+}
+void loop_abort(LoopGroup* g) {
+  std::lock_guard<std::mutex> lk(g->m);
+  g->abort = true;
+  g->cv.notify_all();
+}
+
+namespace {
+cudaError_t loop_fail(Ctx& c, const char* what) {
+  c.last_error = std::string(what) + ": loopback group aborted (another rank failed)";
+  return cudaErrorUnknown;
+}
+cudaError_t loop_bcast(Ctx& c, void* buf, size_t bytes, int root, cudaStream_t s) {
+  LoopGroup* g = (LoopGroup*)c.loop;
+  const int r = c.cfg.rank;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  g->ptr[r] = buf;
+  if (!loop_barrier(g)) return loop_fail(c, "broadcast");
+  if (r != root && bytes) {
+    e = cudaMemcpyAsync(buf, g->ptr[root], bytes, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+  }
+  if (!loop_barrier(g)) return loop_fail(c, "broadcast");
+  return cudaSuccess;
+}
+cudaError_t loop_bcast_tiles(Ctx& c, double* buf, size_t count, int64_t ntiles, cudaStream_t s) {
+  LoopGroup* g = (LoopGroup*)c.loop;
+  const int r = c.cfg.rank, n = c.cfg.nranks;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  g->ptr[r] = buf;
+  if (!loop_barrier(g)) return loop_fail(c, "tile broadcast");
+  for (int64_t q = 0; q < ntiles && e == cudaSuccess; ++q)
+    if (q % n != r)
+      e = cudaMemcpyAsync(buf + q * count, (const double*)g->ptr[q % n] + q * count, count * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  if (!loop_barrier(g)) return loop_fail(c, "tile broadcast");
+  return cudaSuccess;
+}
+cudaError_t loop_allreduce(Ctx& c, double* buf, size_t count, bool max, cudaStream_t s) {
+  LoopGroup* g = (LoopGroup*)c.loop;
+  const int r = c.cfg.rank;
+  g->host[r].resize(count);
+  cudaError_t e = cudaMemcpyAsync(g->host[r].data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  if (!loop_barrier(g)) return loop_fail(c, "all-reduce");
+  std::vector<double> acc(g->host[0]);
+  for (int q = 1; q < g->n; ++q)   // rank order: every rank forms the same value
+    for (size_t i = 0; i < count; ++i) acc[i] = max ? std::max(acc[i], g->host[q][i]) : acc[i] + g->host[q][i];
+  if (!loop_barrier(g)) return loop_fail(c, "all-reduce");   // everyone has read every host[q]
+  e = cudaMemcpyAsync(buf, acc.data(), count * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
+}
+}  // namespace
+
+// Collectives of the distributed factorisation (SHARD_CYCLIC): NCCL with polya_nccl_init, the loopback
+// group inside polya_factor_solve_loopback; no-ops with one rank.
 cudaError_t comm_bcast(Ctx& c, void* buf, size_t count, bool is_int, int root, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
+  if (c.loop) return loop_bcast(c, buf, count * (is_int ? sizeof(int32_t) : sizeof(double)), root, s);
   if (!c.nccl) return c.cfg.nranks == 1 ? cudaSuccess : cudaErrorNotReady;   // one rank: nothing to send
   ncclResult_t r = ncclBroadcast(buf, buf, count, is_int ? ncclInt32 : ncclFloat64, root, (ncclComm_t)c.nccl, s);
   if (r != ncclSuccess) {
@@ -190,6 +268,7 @@ cudaError_t comm_bcast(Ctx& c, void* buf, size_t count, bool is_int, int root, c
 // tile q of buf (count doubles each, q < ntiles) broadcast from rank q mod nranks, as one NCCL group
 cudaError_t comm_bcast_tiles(Ctx& c, double* buf, size_t count, int64_t ntiles, cudaStream_t s) {
   if (count == 0 || ntiles == 0) return cudaSuccess;
+  if (c.loop) return loop_bcast_tiles(c, buf, count, ntiles, s);
   if (!c.nccl) return c.cfg.nranks == 1 ? cudaSuccess : cudaErrorNotReady;
   ncclResult_t r = ncclGroupStart();
   for (int64_t q = 0; q < ntiles && r == ncclSuccess; ++q)
@@ -202,15 +281,22 @@ cudaError_t comm_bcast_tiles(Ctx& c, double* buf, size_t count, int64_t ntiles, 
   }
   return cudaSuccess;
 }
-cudaError_t comm_allreduce_sum(Ctx& c, double* buf, size_t count, cudaStream_t s) {
+static cudaError_t comm_allreduce(Ctx& c, double* buf, size_t count, bool max, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
+  if (c.loop) return loop_allreduce(c, buf, count, max, s);
   if (!c.nccl) return c.cfg.nranks == 1 ? cudaSuccess : cudaErrorNotReady;
-  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c.nccl, s);
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, max ? ncclMax : ncclSum, (ncclComm_t)c.nccl, s);
   if (r != ncclSuccess) {
     c.last_error = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
     return cudaErrorUnknown;
   }
   return cudaSuccess;
+}
+cudaError_t comm_allreduce_sum(Ctx& c, double* buf, size_t count, cudaStream_t s) {
+  return comm_allreduce(c, buf, count, false, s);
+}
+cudaError_t comm_allreduce_max(Ctx& c, double* buf, size_t count, cudaStream_t s) {
+  return comm_allreduce(c, buf, count, true, s);
 }
 
 void nccl_free(Ctx& c) {

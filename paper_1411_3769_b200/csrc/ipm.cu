@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "polya_internal.h"
@@ -571,10 +572,14 @@ struct Ipm {
   int lwork = 0;
   bool tiled = false;          // G held as pair tiles (lower block triangle in column-major view)
   bool dist = false;           // SHARD_CYCLIC: this rank's pair tiles only, factorised across the ranks
-  double* panel = nullptr;     // dist, nranks > 1: the broadcast panel of step k ((L0-1) tiles)
-  double* lkk = nullptr;       // dist, nranks > 1: the broadcast diagonal factor L_kk (one tile)
+  double* panel[2] = {};       // dist, nranks > 1: the broadcast panel of step k ((L0-1) tiles), by k parity
+  double* lkk[2] = {};         // dist, nranks > 1: the broadcast diagonal factor L_kk (one tile), by k parity
+  double* stat = nullptr;      // dist: {local error, potrf info} of a step, max-reduced over the ranks
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
+  cublasHandle_t blas_upd = nullptr;   // dist: the trailing update's handle (own workspace), on `upd`
+  cudaStream_t upd = nullptr;          // dist: look-ahead stream of the trailing updates
+  std::vector<cudaEvent_t> ev_pan, ev_col, ev_upd;   // dist: per step (panel solved / column k+1 / update done)
   cudaEvent_t ev[6] = {};
 };
 
@@ -589,13 +594,18 @@ void polya_ipm_free(polya::Ctx& c) {
   Ipm* w = (Ipm*)c.ipm;
   if (!w) return;
   double* ps[] = {w->W, w->Rd, w->T1, w->T2, w->dX1, w->dZ1, w->dX2, w->dZ2, w->G, w->O1, w->O2,
-                  w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work, w->panel, w->lkk};
+                  w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work, w->panel[0], w->panel[1],
+                  w->lkk[0], w->lkk[1], w->stat};
   for (double* p : ps)
     if (p) cudaFree(p);
   if (w->info) cudaFree(w->info);
   if (w->fail) cudaFree(w->fail);
   if (w->sol) cusolverDnDestroy(w->sol);
   if (w->blas) cublasDestroy(w->blas);
+  if (w->blas_upd) cublasDestroy(w->blas_upd);
+  if (w->upd) cudaStreamDestroy(w->upd);
+  for (auto* v : {&w->ev_pan, &w->ev_col, &w->ev_upd})
+    for (auto e : *v) cudaEventDestroy(e);
   for (auto& e : w->ev)
     if (e) cudaEventDestroy(e);
   delete w;
@@ -649,9 +659,18 @@ Ipm* ipm_ws(Ctx& c) {
   w->dist = c.cfg.shard == POLYA_SHARD_CYCLIC;
   CK(cudaMalloc(&w->G, (w->tiled ? (size_t)std::max<int64_t>(c.npairs_local, 1) * c.Ntil * c.Ntil : (size_t)c.K * c.K) *
                            sizeof(double)));
-  if (w->dist && c.cfg.nranks > 1 && c.L0 > 1) {
-    CK(cudaMalloc(&w->panel, (size_t)(c.L0 - 1) * c.Ntil * c.Ntil * sizeof(double)));
-    CK(cudaMalloc(&w->lkk, (size_t)c.Ntil * c.Ntil * sizeof(double)));
+  if (w->dist && c.cfg.nranks > 1 && c.L0 > 1)
+    for (int q = 0; q < 2; ++q) {
+      CK(cudaMalloc(&w->panel[q], (size_t)(c.L0 - 1) * c.Ntil * c.Ntil * sizeof(double)));
+      CK(cudaMalloc(&w->lkk[q], (size_t)c.Ntil * c.Ntil * sizeof(double)));
+    }
+  if (w->dist) {
+    CK(cudaMalloc(&w->stat, 2 * sizeof(double)));
+    CK(cudaStreamCreateWithFlags(&w->upd, cudaStreamNonBlocking));
+    for (auto* v : {&w->ev_pan, &w->ev_col, &w->ev_upd}) {
+      v->resize(c.L0 + 1);
+      for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
   }
   CK(cudaMalloc(&w->tb, (size_t)c.nb * sizeof(double)));
   CK(cudaMalloc(&w->part, (size_t)kScalarBlocks * 3 * sizeof(double)));
@@ -663,6 +682,7 @@ Ipm* ipm_ws(Ctx& c) {
   const int fdim = (int)(w->tiled ? c.Ntil : c.K);
   CS(cusolverDnDpotrf_bufferSize(w->sol, CUBLAS_FILL_MODE_LOWER, fdim, w->G, fdim, &w->lwork));
   CB(cublasCreate(&w->blas));
+  if (w->dist) CB(cublasCreate(&w->blas_upd));
   CK(cudaMalloc(&w->work, (size_t)std::max(w->lwork, 1) * sizeof(double)));
   for (auto& e : w->ev) CK(cudaEventCreate(&e));
   return w;
@@ -828,19 +848,20 @@ void dist_trsm_share(Ctx& c, Ipm* w, int64_t k, const double* Lkk, double* panel
   }
 }
 
-// panel + (i - k - 1) N^2 = B_ik for i > k
-void dist_update(Ctx& c, Ipm* w, double* G, int64_t k, const double* panel, cudaStream_t s) {
+// panel + (i - k - 1) N^2 = B_ik for i > k; this rank's block columns j in [j0, j1) (j > k)
+void dist_update(Ctx& c, cublasHandle_t h, double* G, int64_t k, const double* panel, int64_t j0, int64_t j1,
+                 cudaStream_t s) {
   const int N = (int)c.Ntil;
   const int64_t NN = (int64_t)N * N;
   const double one = 1.0, mone = -1.0;
-  CB(cublasSetStream(w->blas, s));
-  for (int64_t j = k + 1; j < c.L0; ++j) {
+  CB(cublasSetStream(h, s));
+  for (int64_t j = std::max(j0, k + 1); j < std::min(j1, c.L0); ++j) {
     if (owner(c, j) != c.cfg.rank) continue;
     const double* Bjk = panel + (j - k - 1) * NN;
-    CB(cublasDsyrk(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, N, N, &mone, Bjk, N, &one, tile(c, G, j, j), N));
+    CB(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, N, N, &mone, Bjk, N, &one, tile(c, G, j, j), N));
     ++c.launches;
     for (int64_t i = j + 1; i < c.L0; ++i) {
-      CB(cublasDgemm(w->blas, CUBLAS_OP_N, CUBLAS_OP_T, N, N, N, &mone, panel + (i - k - 1) * NN, N, Bjk, N, &one,
+      CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, N, N, N, &mone, panel + (i - k - 1) * NN, N, Bjk, N, &one,
                      tile(c, G, j, i), N));
       ++c.launches;
     }
@@ -852,37 +873,90 @@ void comm(Ctx& c, cudaError_t e) {
   if (e != cudaSuccess) throw IpmFail{POLYA_ENCCL, c.last_error};
 }
 
-// Collective over the ranks of the context (NCCL; no communication with one rank).
-bool dist_potrf(Ctx& c, Ipm* w, cudaStream_t s) {
-  const int64_t NN = c.Ntil * c.Ntil;
-  for (int64_t k = 0; k < c.L0; ++k) {
-    const int o = owner(c, k);
-    int info = 0;
-    if (c.cfg.rank == o) info = dist_potrf_kk(c, w, w->G, k, s);
-    if (c.cfg.nranks > 1) {   // every rank learns the owner's verdict on L_kk
-      CK(cudaMemcpyAsync(w->info, &info, sizeof(int), cudaMemcpyHostToDevice, s));
-      comm(c, comm_bcast(c, w->info, 1, true, o, s));
-      CK(cudaMemcpyAsync(&info, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+// Collective agreement on a step's outcome: every rank contributes {its first local failure (a
+// polya_status, 0 = none), the owner's potrf info}; the maxima come back to all ranks, so a failure on
+// one rank makes every rank leave dist_potrf with the same error instead of waiting in a broadcast.
+void dist_agree(Ctx& c, Ipm* w, polya_status& local, int& info, const std::string& msg, cudaStream_t s) {
+  if (c.cfg.nranks == 1) {
+    if (local != POLYA_OK) throw IpmFail{local, msg};
+    return;
+  }
+  double h[2] = {(double)local, (double)info};
+  CK(cudaMemcpyAsync(w->stat, h, sizeof(h), cudaMemcpyHostToDevice, s));
+  comm(c, comm_allreduce_max(c, w->stat, 2, s));
+  CK(cudaMemcpyAsync(h, w->stat, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h[0] != 0.0)
+    throw IpmFail{(polya_status)(int)h[0], local != POLYA_OK ? msg : "distributed factorisation: a peer rank failed"};
+  info = (int)h[1];
+}
+
+// Collective over the ranks of the context (NCCL, or the loopback group; nothing to send with one
+// rank).  With look-ahead: the panel work of step k (the owner's potrf, the broadcasts, the split
+// panel solves) runs on `s`, the trailing update on w->upd; the update of block column k+1 goes first
+// and releases step k+1's panel (event), so the next panel factorisation and its broadcasts overlap the
+// rest of step k's update.  Non-owners receive panels into two buffers by step parity (a buffer is
+// reused only after the update of step k-2 has read it).  Every tile still sees the same calls in the
+// same order as tiled_potrf: the factor is the one-rank factor bit for bit.
+bool dist_potrf(Ctx& c, Ipm* w, double* G, cudaStream_t s) {
+  const int64_t NN = c.Ntil * c.Ntil, T = c.L0;
+  polya_status pending = POLYA_OK;   // a local failure not yet agreed on
+  std::string pmsg;
+  auto local = [&](auto&& f) {
+    if (pending != POLYA_OK) return;
+    try {
+      f();
+    } catch (const IpmFail& e) {
+      pending = e.s;
+      pmsg = e.msg;
     }
-    if (info != 0) return false;
-    if (k + 1 == c.L0) break;
+  };
+  auto drain = [&]() { cudaStreamSynchronize(w->upd); };
+  CK(cudaEventRecord(w->ev_col[0], s));   // G assembled (on s): the first panel may start
+  CK(cudaStreamWaitEvent(w->upd, w->ev_col[0], 0));
+  for (int64_t k = 0; k < T; ++k) {
+    const int o = owner(c, k);
     const bool mine = c.cfg.rank == o;
-    double* Lkk = mine ? tile(c, w, k, k) : w->lkk;
-    double* panel = mine ? tile(c, w, k, k + 1) : w->panel;
-    const int64_t nq = c.L0 - k - 1;
+    CK(cudaStreamWaitEvent(s, w->ev_col[k], 0));   // block column k fully updated by step k-1
+    int info = 0;
+    if (mine) local([&] { info = dist_potrf_kk(c, w, G, k, s); });
+    try {
+      dist_agree(c, w, pending, info, pmsg, s);
+    } catch (...) {
+      drain();
+      throw;
+    }
+    if (info != 0) {
+      drain();
+      return false;
+    }
+    if (k + 1 == T) break;
+    const int buf = (int)(k & 1);
+    if (!mine && k >= 2) CK(cudaStreamWaitEvent(s, w->ev_upd[k - 2], 0));   // the buffer's last reader
+    double* Lkk = mine ? tile(c, G, k, k) : w->lkk[buf];
+    double* panel = mine ? tile(c, G, k, k + 1) : w->panel[buf];
+    const int64_t nq = T - k - 1;
     comm(c, comm_bcast(c, Lkk, (size_t)NN, false, o, s));
     comm(c, comm_bcast(c, panel, (size_t)(nq * NN), false, o, s));
-    dist_trsm_share(c, w, k, Lkk, panel, s);
+    local([&] { dist_trsm_share(c, w, k, Lkk, panel, s); });
     comm(c, comm_bcast_tiles(c, panel, (size_t)NN, nq, s));   // tile q from rank q mod N
-    dist_update(c, w, w->G, k, panel, s);
+    CK(cudaEventRecord(w->ev_pan[k], s));
+    CK(cudaStreamWaitEvent(w->upd, w->ev_pan[k], 0));
+    local([&] { dist_update(c, w->blas_upd, G, k, panel, k + 1, k + 2, w->upd); });   // column k+1 first
+    CK(cudaEventRecord(w->ev_col[k + 1], w->upd));
+    local([&] { dist_update(c, w->blas_upd, G, k, panel, k + 2, T, w->upd); });
+    CK(cudaEventRecord(w->ev_upd[k], w->upd));
   }
+  CK(cudaEventRecord(w->ev_upd[T], w->upd));
+  CK(cudaStreamWaitEvent(s, w->ev_upd[T], 0));   // later work on s sees the whole factor
+  int none = 0;
+  dist_agree(c, w, pending, none, pmsg, s);
   return true;
 }
 
 // x <- G^{-1} x with the distributed factor: the owner of column k does its triangular solve and
 // its panel's matrix-vector updates, then broadcasts the part of x it changed.
-void dist_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
+void dist_potrs(Ctx& c, Ipm* w, double* G, double* x, cudaStream_t s) {
   const int N = (int)c.Ntil;
   const int64_t T = c.L0;
   const double one = 1.0, mone = -1.0;
@@ -891,9 +965,9 @@ void dist_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
     const int o = owner(c, k);
     double* xk = x + k * N;
     if (c.cfg.rank == o) {
-      CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, N, tile(c, w, k, k), N, xk, 1));
+      CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, N, tile(c, G, k, k), N, xk, 1));
       for (int64_t i = k + 1; i < T; ++i)
-        CB(cublasDgemv(w->blas, CUBLAS_OP_N, N, N, &mone, tile(c, w, k, i), N, xk, 1, &one, x + i * N, 1));
+        CB(cublasDgemv(w->blas, CUBLAS_OP_N, N, N, &mone, tile(c, G, k, i), N, xk, 1, &one, x + i * N, 1));
       c.launches += T - k;
     }
     comm(c, comm_bcast(c, xk, (size_t)((T - k) * N), false, o, s));
@@ -903,8 +977,8 @@ void dist_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
     double* xk = x + k * N;
     if (c.cfg.rank == o) {
       for (int64_t i = k + 1; i < T; ++i)
-        CB(cublasDgemv(w->blas, CUBLAS_OP_T, N, N, &mone, tile(c, w, k, i), N, x + i * N, 1, &one, xk, 1));
-      CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, N, tile(c, w, k, k), N, xk, 1));
+        CB(cublasDgemv(w->blas, CUBLAS_OP_T, N, N, &mone, tile(c, G, k, i), N, x + i * N, 1, &one, xk, 1));
+      CB(cublasDtrsv(w->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, N, tile(c, G, k, k), N, xk, 1));
       c.launches += T - k;
     }
     comm(c, comm_bcast(c, xk, (size_t)N, false, o, s));
@@ -940,14 +1014,14 @@ double dist_regularise(Ctx& c, Ipm* w, cudaStream_t s) {
 }
 
 void solveG(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
-  if (w->dist) dist_potrs(c, w, x, s);
+  if (w->dist) dist_potrs(c, w, w->G, x, s);
   else if (w->tiled) tiled_potrs(c, w, x, s);
   else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, x, (int)c.K, w->info));
 }
 
 // Cholesky of the Schur complement (dense or tiled); false if not positive definite.
 bool factor(Ctx& c, Ipm* w, cudaStream_t s) {
-  if (w->dist) return dist_potrf(c, w, s);
+  if (w->dist) return dist_potrf(c, w, w->G, s);
   if (w->tiled) {
     try {
       tiled_potrf(c, w, s);
@@ -1121,90 +1195,69 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
 }
 
 // ---- the distributed factorisation with an in-process loopback in place of NCCL (tests) --------
-// All ranks' contexts live in this process on one device and run the SAME step functions as
-// dist_potrf / dist_potrs, one rank after another within each step; each broadcast is a device
-// copy from the owner's buffer into every other rank's.  This checks the partition, the local tile
-// indexing, the panel bookkeeping and the x exchange of the multi-rank path on one GPU (NCCL
-// refuses two ranks on one device); the NCCL calls themselves are the one-line comm_bcast.
+// All ranks' contexts live in this process on one device; each rank is a host thread with its own
+// stream running the SAME dist_potrf / dist_potrs as the NCCL path, the collectives going through the
+// loopback group (combine.cpp: barrier + device copies from the root's buffer) instead of NCCL.  This
+// checks the partition, the local tile indexing, the panel bookkeeping, the look-ahead ordering and the
+// x exchange of the multi-rank path on one GPU (NCCL refuses two ranks on one device).  x (K doubles):
+// b in, G^{-1} b out (every rank's copy is the same; rank 0's is returned).
 extern "C" polya_status polya_factor_solve_loopback(polya_ctx** ctxs, int32_t nranks, double* const* G_local, double* x,
                                                     void* stream) {
   if (!ctxs || nranks < 1 || !G_local || !x) return POLYA_EINVAL;
   for (int32_t r = 0; r < nranks; ++r) {
     if (!ctxs[r] || !G_local[r]) return POLYA_EINVAL;
     const Ctx& c = ctxs[r]->c;
-    if (c.cfg.shard != POLYA_SHARD_CYCLIC || c.cfg.nranks != nranks || c.cfg.rank != r || c.K != ctxs[0]->c.K)
+    if (c.cfg.shard != POLYA_SHARD_CYCLIC || c.cfg.nranks != nranks || c.cfg.rank != r || c.K != ctxs[0]->c.K ||
+        c.nccl)
       return POLYA_EINVAL;
   }
-  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t s0 = (cudaStream_t)stream;
   Ctx& c0 = ctxs[0]->c;
-  const int64_t T = c0.L0, N = c0.Ntil, NN = N * N, K = c0.K;
-  try {
-    std::vector<Ipm*> w(nranks);
-    for (int32_t r = 0; r < nranks; ++r) w[r] = ipm_ws(ctxs[r]->c);
-    for (int64_t k = 0; k < T; ++k) {
-      const int o = owner(c0, k);
-      if (dist_potrf_kk(ctxs[o]->c, w[o], G_local[o], k, s) != 0)
-        throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite (tile " + std::to_string(k) + ")"};
-      if (k + 1 == T) break;
-      const int64_t nq = T - k - 1;
-      std::vector<double*> Lkk(nranks), panel(nranks);
-      for (int32_t r = 0; r < nranks; ++r) {
-        Lkk[r] = r == o ? tile(ctxs[o]->c, G_local[o], k, k) : w[r]->lkk;
-        panel[r] = r == o ? tile(ctxs[o]->c, G_local[o], k, k + 1) : w[r]->panel;
+  if (cudaStreamSynchronize(s0) != cudaSuccess) return POLYA_ECUDA;   // G_local and x are ready
+  LoopGroup g;
+  g.n = nranks;
+  g.ptr.assign(nranks, nullptr);
+  g.host.resize(nranks);
+  std::vector<polya_status> st(nranks, POLYA_OK);
+  std::vector<std::string> msg(nranks);
+  std::vector<std::thread> th;
+  for (int32_t r = 0; r < nranks; ++r) ctxs[r]->c.loop = &g;
+  for (int32_t r = 0; r < nranks; ++r)
+    th.emplace_back([&, r] {
+      Ctx& c = ctxs[r]->c;
+      cudaStream_t s = nullptr;
+      try {
+        CK(cudaSetDevice(c.device));
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        Ipm* w = ipm_ws(c);
+        CK(cudaMemcpyAsync(w->tmpK, x, c.K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (!dist_potrf(c, w, G_local[r], s))
+          throw IpmFail{POLYA_ENOTPD, "Schur complement not positive definite"};
+        dist_potrs(c, w, G_local[r], w->tmpK, s);
+        CK(cudaStreamSynchronize(s));
+      } catch (const IpmFail& f) {
+        st[r] = f.s;
+        msg[r] = f.msg;
+        loop_abort(&g);
       }
-      for (int32_t r = 0; r < nranks; ++r) {
-        if (r == o) continue;   // the two broadcasts of the owner: L_kk and the raw panel
-        CK(cudaMemcpyAsync(Lkk[r], Lkk[o], (size_t)NN * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(panel[r], panel[o], (size_t)(nq * NN) * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      }
-      for (int32_t r = 0; r < nranks; ++r) dist_trsm_share(ctxs[r]->c, w[r], k, Lkk[r], panel[r], s);
-      for (int64_t q = 0; q < nq; ++q)   // solved tile q from rank q mod N to every other rank
-        for (int32_t r = 0; r < nranks; ++r)
-          if (r != q % nranks)
-            CK(cudaMemcpyAsync(panel[r] + q * NN, panel[q % nranks] + q * NN, (size_t)NN * sizeof(double),
-                               cudaMemcpyDeviceToDevice, s));
-      for (int32_t r = 0; r < nranks; ++r) dist_update(ctxs[r]->c, w[r], G_local[r], k, panel[r], s);
+      if (s) cudaStreamDestroy(s);
+    });
+  for (auto& t : th) t.join();
+  for (int32_t r = 0; r < nranks; ++r) ctxs[r]->c.loop = nullptr;
+  for (int32_t r = 0; r < nranks; ++r)   // the root cause first: an aborted peer reports ENCCL
+    if (st[r] != POLYA_OK && st[r] != POLYA_ENCCL) {
+      c0.last_error = msg[r];
+      return st[r];
     }
-    // the solves with one copy of x per rank (tmpK), exchanged like dist_potrs's broadcasts
-    const double one = 1.0, mone = -1.0;
-    for (int32_t r = 0; r < nranks; ++r) CK(cudaMemcpyAsync(w[r]->tmpK, x, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    auto send = [&](int o, int64_t off, int64_t cnt) {
-      for (int32_t r = 0; r < nranks; ++r)
-        if (r != o)
-          CK(cudaMemcpyAsync(w[r]->tmpK + off, w[o]->tmpK + off, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    };
-    for (int64_t k = 0; k < T; ++k) {
-      const int o = owner(c0, k);
-      Ctx& c = ctxs[o]->c;
-      Ipm* wo = w[o];
-      CB(cublasSetStream(wo->blas, s));
-      double* xo = wo->tmpK;
-      CB(cublasDtrsv(wo->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)N,
-                     tile(c, G_local[o], k, k), (int)N, xo + k * N, 1));
-      for (int64_t i = k + 1; i < T; ++i)
-        CB(cublasDgemv(wo->blas, CUBLAS_OP_N, (int)N, (int)N, &mone, tile(c, G_local[o], k, i), (int)N, xo + k * N, 1,
-                       &one, xo + i * N, 1));
-      send(o, k * N, (T - k) * N);
+  for (int32_t r = 0; r < nranks; ++r)
+    if (st[r] != POLYA_OK) {
+      c0.last_error = msg[r];
+      return st[r];
     }
-    for (int64_t k = T - 1; k >= 0; --k) {
-      const int o = owner(c0, k);
-      Ctx& c = ctxs[o]->c;
-      Ipm* wo = w[o];
-      CB(cublasSetStream(wo->blas, s));
-      double* xo = wo->tmpK;
-      for (int64_t i = k + 1; i < T; ++i)
-        CB(cublasDgemv(wo->blas, CUBLAS_OP_T, (int)N, (int)N, &mone, tile(c, G_local[o], k, i), (int)N, xo + i * N, 1,
-                       &one, xo + k * N, 1));
-      CB(cublasDtrsv(wo->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)N,
-                     tile(c, G_local[o], k, k), (int)N, xo + k * N, 1));
-      send(o, k * N, N);
-    }
-    CK(cudaMemcpyAsync(x, w[nranks - 1]->tmpK, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  } catch (const IpmFail& f) {
-    c0.last_error = f.msg;
-    return f.s;
-  }
+  Ipm* w0 = (Ipm*)c0.ipm;
+  if (cudaMemcpyAsync(x, w0->tmpK, c0.K * sizeof(double), cudaMemcpyDeviceToDevice, s0) != cudaSuccess ||
+      cudaStreamSynchronize(s0) != cudaSuccess)
+    return POLYA_ECUDA;
   return POLYA_OK;
 }
 

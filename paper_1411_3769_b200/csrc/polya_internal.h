@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -77,7 +79,8 @@ struct Ctx {
   int64_t npairs = 0, pair0 = 0, pair1 = 0;
   int64_t items_total = 0, item0 = 0, item1 = 0;
   int64_t b0 = 0, b1 = 0;  // this rank's Polya blocks (SHARD_BLOCKS; all blocks otherwise)
-  void* nccl = nullptr;    // ncclComm_t of polya_nccl_init (SHARD_BLOCKS combine)
+  void* nccl = nullptr;    // ncclComm_t of polya_nccl_init (SHARD_BLOCKS combine, SHARD_CYCLIC factorisation)
+  void* loop = nullptr;    // LoopGroup of polya_factor_solve_loopback (in place of NCCL, tests)
   std::vector<int64_t> pair_item_global;  // [npairs + 1]
   std::vector<int64_t> local_pairs;       // this rank's pairs (global indices, ascending)
   std::vector<int64_t> local_item;        // [npairs_local + 1] item prefix of the local pairs (kernel numbering)
@@ -155,9 +158,23 @@ cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
 cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s);
 cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
 cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t item0, int64_t item1, cudaStream_t s);
-// collectives of the distributed factorisation (combine.cpp; no-ops with one rank)
+// collectives of the distributed factorisation (combine.cpp; NCCL, or the loopback group of
+// polya_factor_solve_loopback; no-ops with one rank)
+struct LoopGroup {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int count = 0;
+  int64_t gen = 0;
+  bool abort = false;
+  std::vector<const void*> ptr;            // each rank's buffer of the current collective
+  std::vector<std::vector<double>> host;   // all-reduce staging
+};
+bool loop_barrier(LoopGroup* g);
+void loop_abort(LoopGroup* g);
 cudaError_t comm_bcast(Ctx& c, void* buf, size_t count, bool is_int, int root, cudaStream_t s);
 cudaError_t comm_allreduce_sum(Ctx& c, double* buf, size_t count, cudaStream_t s);
+cudaError_t comm_allreduce_max(Ctx& c, double* buf, size_t count, cudaStream_t s);
 cudaError_t comm_bcast_tiles(Ctx& c, double* buf, size_t count, int64_t ntiles, cudaStream_t s);
 
 }  // namespace polya

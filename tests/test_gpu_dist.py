@@ -1,9 +1,11 @@
 """The distributed factorisation (SHARD_CYCLIC) on one GPU:
 
 * each rank's CYCLIC assembly is exactly the single-rank pair tiles of its pair rows h = r mod N;
-* polya_factor_solve_loopback -- all ranks' contexts in one process, the per-step functions of the
-  NCCL path with device copies for the broadcasts -- solves G x = b like a dense solve (1e-10) and
-  bit for bit like the one-rank factorisation, for N = 1..4 ranks;
+* polya_factor_solve_loopback -- all ranks' contexts in one process, one host thread per rank running
+  the same dist_potrf (with look-ahead) / dist_potrs as the NCCL path, the collectives through an
+  in-process group (barrier + device copies) -- solves G x = b like a dense solve (1e-10) and bit for
+  bit like the one-rank factorisation, for N = 1..4 ranks; a failure on one rank (an indefinite
+  diagonal tile met by its owner at a later step) reaches every rank through the per-step agreement;
 * polya_ipm_step with SHARD_CYCLIC (one rank, with and without a one-rank NCCL communicator)
   equals the single-GPU tiled step; the solve converges the same way.
 """
@@ -127,6 +129,26 @@ def test_loopback_reports_indefinite_G(pb):
     ctxs = [pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=2, shard=pb.SHARD_CYCLIC) for r in range(2)]
     X, W = synth.spd_blocks(cfg.n, ctxs[0].nblocks, rng)
     Gs = [-c.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES) for c in ctxs]
+    with pytest.raises(pb.PolyaError, match="not positive definite"):
+        pb.factor_solve_loopback(ctxs, Gs, _dev(rng.normal(size=ctxs[0].K)))
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_indefinite_tile_at_a_later_step(pb, world):
+    """The diagonal tile (1, 1) -- owned by rank 1 -- made indefinite: rank 0 factors step 0 and its
+    look-ahead update runs, rank 1's potrf fails at step 1, and the per-step all-reduce of {error, info}
+    brings every rank out of dist_potrf with the same verdict (no rank left waiting in a broadcast)."""
+    cfg = synth.CONFIGS[2]
+    rng = np.random.default_rng(5)
+    A = synth.vertex_matrices(cfg, rng)
+    ctxs = [pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=world, shard=pb.SHARD_CYCLIC)
+            for r in range(world)]
+    X, W = synth.spd_blocks(cfg.n, ctxs[0].nblocks, rng)
+    Gs = [c.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES) for c in ctxs]
+    N = ctxs[0].Ntil
+    Gs[1][0] -= 1e9 * torch.eye(N, dtype=torch.float64, device="cuda")   # rank 1's first tile is (1, 1)
     with pytest.raises(pb.PolyaError, match="not positive definite"):
         pb.factor_solve_loopback(ctxs, Gs, _dev(rng.normal(size=ctxs[0].K)))
     for c in ctxs:
