@@ -562,6 +562,8 @@ __global__ void k_diag_shift(double* __restrict__ G, int64_t K, int64_t Ntil, in
     G[diag_off(q, K, Ntil, L0, tiled)] += shift;
 }
 
+constexpr int64_t kSolveNB = 1024;   // row panels of the dense triangular solves (dense_potrs)
+
 struct Ipm {
   int64_t nb = 0, n = 0, K = 0;
   double *W = nullptr, *Rd = nullptr, *T1 = nullptr, *T2 = nullptr, *dX1 = nullptr, *dZ1 = nullptr, *dX2 = nullptr,
@@ -575,6 +577,11 @@ struct Ipm {
   double* panel[2] = {};       // dist, nranks > 1: the broadcast panel of step k ((L0-1) tiles), by k parity
   double* lkk[2] = {};         // dist, nranks > 1: the broadcast diagonal factor L_kk (one tile), by k parity
   double* stat = nullptr;      // dist: {local error, potrf info} of a step, max-reduced over the ranks
+  double* dinv = nullptr;      // dense: inverses of the kSolveNB diagonal blocks of the factor
+  double* eye = nullptr;       // dense: nblk identity blocks (the right-hand side of those trsm)
+  double* tsol = nullptr;      // dense: one block of the solve
+  const double** dptrA = nullptr;   // dense: device pointers of the diagonal blocks (batched trsm)
+  double** dptrB = nullptr;
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
   cublasHandle_t blas_upd = nullptr;   // dist: the trailing update's handle (own workspace), on `upd`
@@ -595,11 +602,13 @@ void polya_ipm_free(polya::Ctx& c) {
   if (!w) return;
   double* ps[] = {w->W, w->Rd, w->T1, w->T2, w->dX1, w->dZ1, w->dX2, w->dZ2, w->G, w->O1, w->O2,
                   w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work, w->panel[0], w->panel[1],
-                  w->lkk[0], w->lkk[1], w->stat};
+                  w->lkk[0], w->lkk[1], w->stat, w->dinv, w->eye, w->tsol};
   for (double* p : ps)
     if (p) cudaFree(p);
   if (w->info) cudaFree(w->info);
   if (w->fail) cudaFree(w->fail);
+  if (w->dptrA) cudaFree((void*)w->dptrA);
+  if (w->dptrB) cudaFree(w->dptrB);
   if (w->sol) cusolverDnDestroy(w->sol);
   if (w->blas) cublasDestroy(w->blas);
   if (w->blas_upd) cublasDestroy(w->blas_upd);
@@ -671,6 +680,26 @@ Ipm* ipm_ws(Ctx& c) {
       v->resize(c.L0 + 1);
       for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+  }
+  if (!w->tiled) {   // dense_potrs: diagonal-block inverses (~ K x kSolveNB doubles: 0.4 GB at config 4)
+    const int64_t NB = kSolveNB, nblk = (c.K + NB - 1) / NB;
+    CK(cudaMalloc(&w->dinv, (size_t)(nblk * NB * NB) * sizeof(double)));
+    CK(cudaMalloc(&w->eye, (size_t)(nblk * NB * NB) * sizeof(double)));
+    CK(cudaMalloc(&w->tsol, (size_t)NB * sizeof(double)));
+    std::vector<double> I((size_t)(NB * NB), 0.0);
+    for (int64_t q = 0; q < NB; ++q) I[(size_t)(q * NB + q)] = 1.0;
+    for (int64_t b = 0; b < nblk; ++b)
+      CK(cudaMemcpy(w->eye + b * NB * NB, I.data(), I.size() * sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<const double*> pa(nblk);
+    std::vector<double*> pb(nblk);
+    for (int64_t b = 0; b < nblk; ++b) {
+      pa[b] = w->G + b * NB * c.K + b * NB;
+      pb[b] = w->dinv + b * NB * NB;
+    }
+    CK(cudaMalloc((void**)&w->dptrA, nblk * sizeof(double*)));
+    CK(cudaMalloc((void**)&w->dptrB, nblk * sizeof(double*)));
+    CK(cudaMemcpy((void*)w->dptrA, pa.data(), nblk * sizeof(double*), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(w->dptrB, pb.data(), nblk * sizeof(double*), cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&w->tb, (size_t)c.nb * sizeof(double)));
   CK(cudaMalloc(&w->part, (size_t)kScalarBlocks * 3 * sizeof(double)));
@@ -1013,10 +1042,64 @@ double dist_regularise(Ctx& c, Ipm* w, cudaStream_t s) {
   return eps;
 }
 
+// x <- G^{-1} x with the dense factor (column-major lower L, leading dimension K), blocked by column
+// panels of kSolveNB: forward t = L_kk^{-1} x_k, x_k = t, x_{k+1..} -= L_{k+1..,k} t; backward
+// x_k -= L_{k+1..,k}^T x_{k+1..}, x_k = L_kk^{-T} x_k -- every step a gemv (the panel gemvs stream the
+// factor once per pass; the diagonal inverses, formed once per factorisation by trsm against I, make
+// the diagonal solves parallel).  cuSOLVER's dpotrs with one right-hand side is level-2 trsv, a chain
+// of K/32 dependent 32-row steps: 10.8 ms per solve at config 4; a blocked variant that kept trsv on
+// 4096-row diagonal blocks still spent 16.6 ms of a step in that chain.
+void dense_potrs(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
+  const int64_t K = c.K, NB = kSolveNB, nblk = (K + NB - 1) / NB;
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  CB(cublasSetStream(w->blas, s));
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t k0 = b * NB;
+    const int nb = (int)std::min<int64_t>(NB, K - k0), rest = (int)(K - k0 - nb);
+    const double* Dinv = w->dinv + b * NB * NB;   // column-major nb x nb, ld NB
+    CB(cublasDgemv(w->blas, CUBLAS_OP_N, nb, nb, &one, Dinv, (int)NB, x + k0, 1, &zero, w->tsol, 1));
+    CK(cudaMemcpyAsync(x + k0, w->tsol, nb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (rest > 0)
+      CB(cublasDgemv(w->blas, CUBLAS_OP_N, rest, nb, &mone, w->G + k0 * K + k0 + nb, (int)K, x + k0, 1, &one,
+                     x + k0 + nb, 1));
+    c.launches += rest > 0 ? 2 : 1;
+  }
+  for (int64_t b = nblk - 1; b >= 0; --b) {
+    const int64_t k0 = b * NB;
+    const int nb = (int)std::min<int64_t>(NB, K - k0), rest = (int)(K - k0 - nb);
+    const double* Dinv = w->dinv + b * NB * NB;
+    if (rest > 0)
+      CB(cublasDgemv(w->blas, CUBLAS_OP_T, rest, nb, &mone, w->G + k0 * K + k0 + nb, (int)K, x + k0 + nb, 1, &one,
+                     x + k0, 1));
+    CB(cublasDgemv(w->blas, CUBLAS_OP_T, nb, nb, &one, Dinv, (int)NB, x + k0, 1, &zero, w->tsol, 1));
+    CK(cudaMemcpyAsync(x + k0, w->tsol, nb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    c.launches += rest > 0 ? 2 : 1;
+  }
+}
+
+// Inverses of the diagonal kSolveNB blocks of the dense factor (after a successful potrf): Dinv_b =
+// L_bb^{-1} by trsm against the identity (column-major, ld NB; the strictly upper part is zero).
+void dense_diag_inverses(Ctx& c, Ipm* w, cudaStream_t s) {
+  const int64_t K = c.K, NB = kSolveNB, nblk = (K + NB - 1) / NB, full = K / NB;
+  const double one = 1.0;
+  CB(cublasSetStream(w->blas, s));
+  CK(cudaMemcpyAsync(w->dinv, w->eye, (size_t)(nblk * NB * NB) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (full > 0)   // the full blocks in one batched call (pointer arrays built with the workspace)
+    CB(cublasDtrsmBatched(w->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)NB,
+                          (int)NB, &one, w->dptrA, (int)K, w->dptrB, (int)NB, (int)full));
+  if (full < nblk) {   // the ragged last block
+    const int64_t k0 = full * NB;
+    const int nb = (int)(K - k0);
+    CB(cublasDtrsm(w->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, nb, nb, &one,
+                   w->G + k0 * K + k0, (int)K, w->dinv + full * NB * NB, (int)NB));
+  }
+  c.launches += 2;
+}
+
 void solveG(Ctx& c, Ipm* w, double* x, cudaStream_t s) {
   if (w->dist) dist_potrs(c, w, w->G, x, s);
   else if (w->tiled) tiled_potrs(c, w, x, s);
-  else CS(cusolverDnDpotrs(w->sol, CUBLAS_FILL_MODE_LOWER, (int)c.K, 1, w->G, (int)c.K, x, (int)c.K, w->info));
+  else dense_potrs(c, w, x, s);
 }
 
 // Cholesky of the Schur complement (dense or tiled); false if not positive definite.
@@ -1035,7 +1118,9 @@ bool factor(Ctx& c, Ipm* w, cudaStream_t s) {
   int hinfo = 0;
   CK(cudaMemcpyAsync(&hinfo, w->info, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  return hinfo == 0;
+  if (hinfo != 0) return false;
+  dense_diag_inverses(c, w, s);
+  return true;
 }
 
 polya_status call(polya_status st, Ctx& c) {
