@@ -212,10 +212,13 @@ polya_status polya_schur(polya_ctx* ctx, const double* X_dev, const double* Zinv
 
 /* The two halves of polya_schur, for callers that stream G out while it is assembled:
  * polya_schur_prepare pads X, Z^{-1} and runs the SCM precompute of this rank (U, V, Q, R; kernel K3);
- * polya_schur_assemble then assembles this rank's local pairs [pair_begin, pair_end) (0-based among
- * pair0 .. pair1-1; G_dev is the same buffer / layout as for polya_schur and only those pairs' entries
- * are written).  polya_schur = prepare + assemble(0, pair1 - pair0).  Inputs must not change between
- * the prepare and the assembles.  Stream-ordered.  Errors: EINVAL (bad range / layout), ECUDA.     */
+ * polya_schur_assemble then assembles this rank's local pairs [pair_begin, pair_end), 0-based among
+ * its npairs_local local pairs (polya_dims; = pair0 .. pair1-1 except with SHARD_CYCLIC, whose local
+ * pairs are the pair rows h = rank mod nranks); G_dev is the same buffer / layout as for polya_schur
+ * and only those pairs' entries are written.  polya_schur = prepare + assemble(0, npairs_local).
+ * Inputs must not change between the prepare and the assembles.  Stream-ordered; the assembles of
+ * one context share its work counter, so they must be serialised on one stream (no two in flight
+ * on different streams).  Errors: EINVAL (bad range / layout), ECUDA.                           */
 polya_status polya_schur_prepare(polya_ctx* ctx, const double* X_dev, const double* Zinv_dev, void* stream);
 polya_status polya_schur_assemble(polya_ctx* ctx, double* G_dev, int layout, int64_t pair_begin, int64_t pair_end,
                                   void* stream);
