@@ -280,6 +280,17 @@ def run_gpu(args, cfg, cid):
 
     for _ in range(args.warmup):
         step()
+    if args.graph:   # the whole step as one CUDA graph (the library's calls are stream-ordered and capturable)
+        if blocks:
+            raise SystemExit("--graph: not with --shard blocks")
+        torch.cuda.synchronize()
+        ctx.set_timing(False)   # the phase events are not recorded inside the graph: time the whole step
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        step = graph.replay   # noqa: F811
+        for _ in range(args.warmup):
+            step()
     barrier()
     clk = ClockSampler(local)
     launches0 = ctx.launch_count()
@@ -294,8 +305,11 @@ def run_gpu(args, cfg, cid):
         e0.record()
         step()
         e1.record()
-        p, a = ctx.timing()                     # waits for this step's schur events
         e1.synchronize()
+        if args.graph:   # the step as a whole (the assembly dominates it beyond config 2)
+            p, a = 0.0, e0.elapsed_time(e1)
+        else:
+            p, a = ctx.timing()                 # this step's schur events
         step_ms.append(e0.elapsed_time(e1))
         pre_ms.append(p)
         asm_ms.append(a)
@@ -487,6 +501,7 @@ def run_gpu(args, cfg, cid):
                            "ReduceScatter on a comm stream overlapping the next group)" if blocks else
                            "polya_schur (precompute + assembly)"),
                        "layout": "G pair tiles (upper, row-panel ready)",
+                       "cuda_graph": bool(args.graph),
                        "parallelism": (f"Polya-block shards x{world} + NCCL ReduceScatter of partial G" if blocks
                                        else f"column-cyclic pair-tile shards x{world} (distributed factorisation)"
                                        if cyclic else f"output-tile shards x{world}"),
@@ -526,6 +541,9 @@ def main():
                     help="tiles: output-tile sharding, no data-path collective (default); blocks: the paper's "
                          "Polya-block sharding with the partial G summed by NCCL ReduceScatter; cyclic: "
                          "column-cyclic pair tiles, the layout of the distributed factorisation (IPM leg at any N)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the step (apply + adjoint + schur) once as a CUDA graph and replay it (small configs "
+                         "are launch-bound)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ipm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
