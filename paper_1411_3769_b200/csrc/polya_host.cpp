@@ -676,6 +676,25 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     c.st.pair_h2 = dupload(qh2);
     c.st.pair_kbeg = dupload(kbeg);
     c.st.pair_item = dupload(pitem);
+    {  // schedule of the whole share: local pairs by decreasing padded k-list (stable), their items in order
+      std::vector<int32_t> order;
+      for (int64_t q = 0; q < c.npairs_local; ++q)
+        if (std::min(c.item1, c.local_item[q + 1]) > std::max(c.item0, c.local_item[q])) order.push_back((int32_t)q);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t b) { return kbeg[a + 1] - kbeg[a] > kbeg[b + 1] - kbeg[b]; });
+      std::vector<int64_t> lo, pre{0};
+      for (int32_t q : order) {
+        const int64_t a = std::max(c.item0, c.local_item[q]), b = std::min(c.item1, c.local_item[q + 1]);
+        lo.push_back(a);
+        pre.push_back(pre.back() + (b - a));
+      }
+      c.st.nsched = (int64_t)order.size();
+      if (c.st.nsched > 0) {
+        c.st.sched_pl = dupload(order);
+        c.st.sched_lo = dupload(lo);
+        c.st.sched_prefix = dupload(pre);
+      }
+    }
     {
       std::vector<int2> kd(kL.size());
       for (size_t i = 0; i < kL.size(); ++i) kd[i] = make_int2(kL[i], kR[i]);
@@ -764,7 +783,7 @@ void free_ctx(Ctx& c) {
                 c.d_items_T, c.d_terms_T, c.d_sc_dst, c.d_sc_src, c.d_sc_w, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
                 c.st.pair_kbeg, c.st.pair_item, c.st.kdesc,
-                c.st.cls_a, c.st.cls_b, c.st.counter, c.d_coef, c.d_ws_items, c.d_ws_terms, c.d_items_T0,
+                c.st.cls_a, c.st.cls_b, c.st.counter, c.st.sched_pl, c.st.sched_lo, c.st.sched_prefix, c.d_coef, c.d_ws_items, c.d_ws_terms, c.d_items_T0,
                 c.d_terms_T0, c.d_items_S0, c.d_terms_S0, c.d_CL};
   for (void* p : ps)
     if (p) cudaFree(p);

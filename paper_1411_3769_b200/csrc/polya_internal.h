@@ -48,6 +48,10 @@ struct SchurTables {
   int32_t* cls_a = nullptr;       // [ncls] chunk index i of class (i <= j)
   int32_t* cls_b = nullptr;       // [ncls] chunk index j
   unsigned long long* counter = nullptr;  // dynamic work counter
+  int32_t* sched_pl = nullptr;    // [nsched] schedule of the rank's whole share: pairs by decreasing k-list
+  int64_t* sched_lo = nullptr;    // [nsched] first item of the pair in [item0, item1)
+  int64_t* sched_prefix = nullptr;  // [nsched + 1] pulled-index prefix
+  int64_t nsched = 0;
 };
 
 struct Ctx {

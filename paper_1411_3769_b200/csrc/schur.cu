@@ -78,6 +78,12 @@ struct SchurArgs {
   const int64_t* pair_item;
   const int2* kdesc;
   int64_t item0, item1;
+  // optional schedule (full-range launches): pulled index -> item, pairs in decreasing k-list length
+  // (longest items first: the last wave is made of short ones), a pair's items consecutive
+  const int32_t* sched_pl;        // [nsched] local pair of schedule entry r
+  const int64_t* sched_lo;        // [nsched] its first item in [item0, item1)
+  const int64_t* sched_prefix;    // [nsched + 1] pulled-index prefix
+  int nsched;
   unsigned long long* counter;
   double* G;
   int layout;
@@ -204,6 +210,22 @@ __device__ __forceinline__ ItemInfo decode_item(const SchurArgs& p, int64_t item
   it.kb = __ldg(p.pair_kbeg + lo);
   it.nstage = (int)((__ldg(p.pair_kbeg + lo + 1) - it.kb) / KB);   // k-lists are padded to whole stages
   return it;
+}
+
+// The item of pulled index idx (< item1 - item0): item0 + idx, or through the schedule, with the
+// local pair as the decode hint (r: the schedule entry of the previous pull, tried first).
+__device__ __forceinline__ int64_t sched_item(const SchurArgs& p, int64_t idx, int& hint, int& r) {
+  if (!p.sched_prefix) return p.item0 + idx;
+  if (!(r >= 0 && r < p.nsched && __ldg(p.sched_prefix + r) <= idx && idx < __ldg(p.sched_prefix + r + 1))) {
+    int lo = 0, hi = p.nsched;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(p.sched_prefix + mid) <= idx) lo = mid; else hi = mid;
+    }
+    r = lo;
+  }
+  hint = __ldg(p.sched_pl + r);
+  return __ldg(p.sched_lo + r) + (idx - __ldg(p.sched_prefix + r));
 }
 
 // What the producer tells the consumers at the first stage of every item (and the end sentinel).
@@ -393,22 +415,27 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
     const int sr = lane >> 2, sc2 = lane & 3;
     uint32_t cnt = 0;
     unsigned long long got = 0;
+    const int64_t total = p.item1 - p.item0;
+    int sr_ = -1, hint = -1;   // schedule entry and pair of the last pull
     if (lane == 0) got = atomicAdd(p.counter, 1ULL);
-    int64_t item = p.item0 + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+    int64_t idx = (int64_t)__shfl_sync(0xffffffffu, got, 0);
+    int64_t item = idx < total ? sched_item(p, idx, hint, sr_) : p.item1;
     ItemInfo it{};
     int2 dfirst = make_int2(0, 0);
     if (item < p.item1) {
-      it = decode_item(p, item, -1);
+      it = decode_item(p, item, hint);
       if (lane < KB) dfirst = __ldg(p.kdesc + it.kb + lane);
       if (lane == 0) got = atomicAdd(p.counter, 1ULL);
     }
     while (item < p.item1) {
       // next item: index (requested one item ago), decode and first descriptors, in flight now
-      const int64_t item_n = p.item0 + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+      const int64_t idx_n = (int64_t)__shfl_sync(0xffffffffu, got, 0);
+      int hint_n = it.pl;
+      const int64_t item_n = idx_n < total ? sched_item(p, idx_n, hint_n, sr_) : p.item1;
       ItemInfo it_n{};
       int2 dfirst_n = make_int2(0, 0);
       if (item_n < p.item1) {
-        it_n = decode_item(p, item_n, it.pl);
+        it_n = decode_item(p, item_n, hint_n);
         if (lane < KB) dfirst_n = __ldg(p.kdesc + it_n.kb + lane);
         if (lane == 0) got = atomicAdd(p.counter, 1ULL);
       }
@@ -609,6 +636,14 @@ cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, 
   a.cls_a = c.st.cls_a; a.cls_b = c.st.cls_b; a.pair_h = c.st.pair_h; a.pair_h2 = c.st.pair_h2;
   a.pair_kbeg = c.st.pair_kbeg; a.pair_item = c.st.pair_item; a.kdesc = c.st.kdesc;
   a.item0 = i0; a.item1 = i1; a.counter = c.st.counter;
+  // the whole share with few items per CTA (config 3; a rank's share at N = 8): longest items first, so the
+  // last wave is made of short ones.  With hundreds of items per CTA the tail is negligible and the
+  // pair-major order's L2 reuse across neighbouring pairs wins (config 5: +1.2 % with the schedule).
+  const bool full = i0 == c.item0 && i1 == c.item1 && c.st.nsched > 0 && (i1 - i0) < 128 * c.k4_ctas;
+  a.sched_pl = full ? c.st.sched_pl : nullptr;
+  a.sched_lo = full ? c.st.sched_lo : nullptr;
+  a.sched_prefix = full ? c.st.sched_prefix : nullptr;
+  a.nsched = full ? (int)c.st.nsched : 0;
   a.G = G; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil; a.nmats = c.nmats;
   k_schur<<<(unsigned)want, NT, kSmemBytes, s>>>(a);
   ++c.launches;
