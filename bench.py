@@ -257,6 +257,9 @@ def run_gpu(args, cfg, cid):
     npl = ctx.dims["npairs_local"]
     wg_rank = ctx.dims["useful_flops_schur"]
     wg_total = sum_over_ranks(wg_rank)
+    wg_one = pb.plan(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)["useful_flops_schur"]   # the whole problem, one rank
+    if abs(wg_total - wg_one) > 1e-9 * wg_one:
+        raise SystemExit(f"bench.py: the ranks' shares sum to W_G = {wg_total:.6e}, the problem has {wg_one:.6e}")
 
     Xd = torch.from_numpy(X).to(dev)
     Wd = torch.from_numpy(W).to(dev)
@@ -496,6 +499,7 @@ def run_gpu(args, cfg, cid):
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded synth/ generators; SURVEY 8(d))",
             "config": {"workload": workload_name(cfg, cid), "K": K, "nblocks": ctx.nblocks, "L0": ctx.L0,
+                       "W_G": wg_one, "W_G_sum_over_ranks": wg_total,
                        "step": "polya_apply + polya_adjoint + " + (
                            "polya_schur_reduce (precompute + assembly by tile groups, each group's NCCL "
                            "ReduceScatter on a comm stream overlapping the next group)" if blocks else
