@@ -253,6 +253,15 @@ def run_gpu(args, cfg, cid):
         if world > 1:
             dist.broadcast_object_list(uid, src=0)
         ctx.nccl_init(uid[0])
+    p2p = blocks and args.combine == "p2p"
+    if p2p:   # fused combine: exchange the receive slots' IPC handles, K4 stores into the owners' slots
+        mine = ctx.p2p_export()
+        hs = [None] * world
+        if world > 1:
+            dist.all_gather_object(hs, mine)
+        else:
+            hs = [mine]
+        ctx.p2p_import(hs)
     K, N = ctx.K, ctx.Ntil
     npl = ctx.dims["npairs_local"]
     wg_rank = ctx.dims["useful_flops_schur"]
@@ -275,7 +284,9 @@ def run_gpu(args, cfg, cid):
     def step():
         Bt = ctx.apply(y)
         yv = ctx.adjoint(Xd)
-        if blocks:   # pipelined: each tile group's ReduceScatter overlaps the next group's assembly
+        if p2p:      # fused: the assembly writes each partial tile into its owner's slot, owners sum
+            ctx.schur_reduce_p2p(Xd, Wd, out=Grecv)
+        elif blocks:   # pipelined: each tile group's ReduceScatter overlaps the next group's assembly
             ctx.schur_reduce(Xd, Wd, out=Grecv)
         else:
             ctx.schur(Xd, Wd, G=G, layout=pb.G_PAIR_TILES)
@@ -359,7 +370,10 @@ def run_gpu(args, cfg, cid):
             ctx.apply(y)
             ctx.adjoint(Xd)
             if blocks:
-                ctx.schur_reduce(Xd, Wd, out=Grecv)
+                if p2p:
+                    ctx.schur_reduce_p2p(Xd, Wd, out=Grecv)
+                else:
+                    ctx.schur_reduce(Xd, Wd, out=Grecv)
                 Gh.copy_(Grecv, non_blocking=True)
                 e1.record(comp)
             else:
@@ -396,7 +410,9 @@ def run_gpu(args, cfg, cid):
             y.copy_(yh, non_blocking=True)
             ctx.apply(y, out=Bt)
             yv = ctx.adjoint(Xd)
-            if blocks:
+            if p2p:
+                ctx.schur_reduce_p2p(Xd, Wd, out=Grecv)
+            elif blocks:
                 ctx.schur_reduce(Xd, Wd, out=Grecv)
             else:
                 ctx.schur(Xd, Wd, G=G, layout=pb.G_PAIR_TILES)
@@ -501,6 +517,8 @@ def run_gpu(args, cfg, cid):
             "config": {"workload": workload_name(cfg, cid), "K": K, "nblocks": ctx.nblocks, "L0": ctx.L0,
                        "W_G": wg_one, "W_G_sum_over_ranks": wg_total,
                        "step": "polya_apply + polya_adjoint + " + (
+                           "polya_schur_reduce_p2p (precompute + assembly storing each partial tile into its "
+                           "owner's slot over peer memory + the owners' ordered sums)" if p2p else
                            "polya_schur_reduce (precompute + assembly by tile groups, each group's NCCL "
                            "ReduceScatter on a comm stream overlapping the next group)" if blocks else
                            "polya_schur (precompute + assembly)"),
@@ -545,6 +563,9 @@ def main():
                     help="tiles: output-tile sharding, no data-path collective (default); blocks: the paper's "
                          "Polya-block sharding with the partial G summed by NCCL ReduceScatter; cyclic: "
                          "column-cyclic pair tiles, the layout of the distributed factorisation (IPM leg at any N)")
+    ap.add_argument("--combine", default="nccl", choices=["nccl", "p2p"],
+                    help="--shard blocks: the pipelined NCCL reduce-scatters (default) or the fused P2P combine "
+                         "(K4 stores each partial tile into its owner's slot over NVLink peer memory)")
     ap.add_argument("--graph", action="store_true",
                     help="capture the step (apply + adjoint + schur) once as a CUDA graph and replay it (small configs "
                          "are launch-bound)")

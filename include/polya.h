@@ -291,8 +291,29 @@ polya_status polya_reduce_G(polya_ctx* ctx, const double* Gpart_dev, double* Gre
 polya_status polya_schur_reduce(polya_ctx* ctx, const double* X_dev, const double* Zinv_dev, double* Grecv_dev,
                                 void* stream);
 polya_status polya_get_combine_timing(polya_ctx* ctx, float* ms_exposed);
+/* Fused P2P combine (SHARD_BLOCKS; the compute step and the collective in one kernel): the assembly
+ * kernel K4 stores every tile of this rank's partial G straight into the tile's owner's receive slot
+ * over NVLink peer memory (the owner / position of a tile as in polya_dims.combine_tiles), then each
+ * owner sums its nranks slots in rank order into Grecv (same layout as polya_reduce_G) -- no separate
+ * reduce-scatter, the transfer runs inside the assembly tile by tile.
+ * polya_p2p_export: allocates this rank's receive slots (nranks x own tiles + flags, library-owned)
+ *   and writes its 64-byte CUDA IPC handle; the caller exchanges the handles (e.g. all_gather).
+ * polya_p2p_import: handles = nranks x 64 bytes in rank order (this rank's entry ignored); opens the
+ *   peers' slots (peer access) and builds the destination tables.
+ * polya_p2p_loopback: test hook -- the nranks contexts of one process on one device wired directly.
+ * polya_schur_reduce_p2p: phases bit 1 = precompute + assembly into the owners' slots + a system-scope
+ *   release of this rank's flag in every owner; bit 2 = wait for every source's flag, then the sum.
+ *   A rank calls it with phases = 3; the loopback test runs bit 1 for every context, then bit 2 (no
+ *   kernel waits on one launched after it on the same device).  Grecv: reduce_count doubles.
+ * Errors: EINVAL (not SHARD_BLOCKS, not imported, null pointers), ENOMEM, ECUDA.                   */
+polya_status polya_p2p_export(polya_ctx* ctx, char handle_out[64]);
+polya_status polya_p2p_import(polya_ctx* ctx, const char* handles);
+polya_status polya_p2p_loopback(polya_ctx** ctxs, int32_t nranks);
+polya_status polya_schur_reduce_p2p(polya_ctx* ctx, const double* X_dev, const double* Zinv_dev, double* Grecv_dev,
+                                    int phases, void* stream);
 /* polya_set_combine_tiles: override t (polya_dims.combine_tiles; 0 = automatic ~2 GiB groups), e.g.
- * for a finer overlap; all ranks must use the same t.  SHARD_BLOCKS only.  Errors: EINVAL. */
+ * for a finer overlap; all ranks must use the same t.  Frees the combine's slots (a P2P combine must
+ * be exported / imported again).  SHARD_BLOCKS only.  Errors: EINVAL. */
 polya_status polya_set_combine_tiles(polya_ctx* ctx, int64_t tiles);
 
 /* ---- beyond one iteration: non-homogeneous systems, parameter boxes, solve, verdict ------------

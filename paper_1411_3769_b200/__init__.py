@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 __all__ = ["lib", "Polya", "PolyaError", "G_FULL", "G_PAIR_TILES", "SHARD_TILES", "SHARD_BLOCKS", "SHARD_CYCLIC",
-           "EXPORTS", "LIB_PATH", "plan", "nccl_unique_id", "homogenize", "simplex_map", "factor_solve_loopback"]
+           "EXPORTS", "LIB_PATH", "plan", "nccl_unique_id", "homogenize", "simplex_map", "factor_solve_loopback",
+           "p2p_loopback"]
 
 # POLYA_LIB overrides the library path (timing-experiment variants built by tools/schur_exp.py)
 LIB_PATH = os.environ.get("POLYA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolya.so")
@@ -25,7 +26,8 @@ EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents",
            "polya_get_timing", "polya_nccl_unique_id", "polya_nccl_init", "polya_reduce_G", "polya_homogenize",
            "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization", "polya_schur_prepare",
            "polya_schur_assemble", "polya_setup_general", "polya_factor_solve_loopback", "polya_schur_reduce",
-           "polya_get_combine_timing", "polya_set_combine_tiles"]
+           "polya_get_combine_timing", "polya_set_combine_tiles", "polya_p2p_export", "polya_p2p_import",
+           "polya_p2p_loopback", "polya_schur_reduce_p2p"]
 
 
 class PolyaError(RuntimeError):
@@ -104,6 +106,10 @@ def lib():
     L.polya_schur_reduce.argtypes = [vp, vp, vp, vp, vp]
     L.polya_get_combine_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
     L.polya_set_combine_tiles.argtypes = [vp, i64]
+    L.polya_p2p_export.argtypes = [vp, vp]
+    L.polya_p2p_import.argtypes = [vp, vp]
+    L.polya_p2p_loopback.argtypes = [ctypes.POINTER(vp), i32]
+    L.polya_schur_reduce_p2p.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp]
     L.polya_homogenize.argtypes = [i32, i32, i32, vp, vp, vp, vp]
     L.polya_simplex_map.argtypes = [i32, i32, i32, vp, vp, vp, vp]
     L.polya_ipm_solve.argtypes = [vp, ctypes.POINTER(_IpmState), ctypes.POINTER(_SolveOpts), ctypes.POINTER(_SolveResult),
@@ -157,6 +163,16 @@ def factor_solve_loopback(ctxs, G_local, x, stream=None):
         raise PolyaError(f"polya_factor_solve_loopback: {lib().polya_strerror(st).decode()} "
                          f"({lib().polya_last_error(ctxs[0]._h).decode()})")
     return x
+
+
+def p2p_loopback(ctxs):
+    """polya_p2p_loopback: wire the P2P combine of the contexts of one process (test hook)."""
+    n = len(ctxs)
+    hs = (ctypes.c_void_p * n)(*[c._h.value for c in ctxs])
+    st = lib().polya_p2p_loopback(hs, n)
+    if st != 0:
+        raise PolyaError(f"polya_p2p_loopback: {lib().polya_strerror(st).decode()} "
+                         f"({lib().polya_last_error(ctxs[0]._h).decode()})")
 
 
 def homogenize(terms, l):
@@ -373,6 +389,30 @@ class Polya:
         d = _Dims()
         self._check(lib().polya_dims_get(self._h, ctypes.byref(d)), "polya_dims_get")
         self.dims = {k: getattr(d, k) for k, _ in _Dims._fields_}
+
+    def p2p_export(self):
+        """polya_p2p_export: this rank's 64-byte IPC handle of its receive slots (fused P2P combine)."""
+        buf = ctypes.create_string_buffer(64)
+        self._check(lib().polya_p2p_export(self._h, buf), "polya_p2p_export")
+        return bytes(buf.raw)
+
+    def p2p_import(self, handles):
+        """polya_p2p_import: every rank's handle, in rank order."""
+        blob = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles), 64 * len(handles))
+        self._check(lib().polya_p2p_import(self._h, blob), "polya_p2p_import")
+
+    def schur_reduce_p2p(self, X, Zinv, out=None, phases=3, stream=None):
+        """polya_schur_reduce_p2p: the assembly writing each partial tile into its owner's slot over peer
+        memory (phases bit 1) and the owner's ordered sum of the slots (bit 2)."""
+        import torch
+        if out is None and phases & 2:
+            out = torch.empty(self.dims["reduce_count"], dtype=torch.float64, device=X.device)
+        nbn = self.nblocks * self.bn ** 2
+        self._check(lib().polya_schur_reduce_p2p(self._h, _dev_ptr(X, nbn, "X") if phases & 1 else None,
+                                                 _dev_ptr(Zinv, nbn, "Zinv") if phases & 1 else None,
+                                                 _dev_ptr(out, self.dims["reduce_count"], "Grecv") if phases & 2 else None,
+                                                 int(phases), _stream_ptr(stream)), "polya_schur_reduce_p2p")
+        return out
 
     def combine_timing(self):
         a = ctypes.c_float()

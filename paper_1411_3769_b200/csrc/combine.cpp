@@ -161,8 +161,159 @@ extern "C" polya_status polya_set_combine_tiles(polya_ctx* ctx, int64_t tiles) {
   return POLYA_OK;
 }
 
+// ---- fused P2P combine (SHARD_BLOCKS): K4 writes each of this rank's partial tiles straight into
+// its owner's receive slot over NVLink peer memory (the epilogue's stores go to the peer; no
+// separate collective), then every owner sums its nranks slots in rank order.  Owner and position of
+// a pair tile follow the tile groups of combine_shape, so Grecv has the layout of polya_reduce_G.
+namespace {
+inline void p2p_place(const Ctx& c, int64_t p, int64_t t, int* owner, int64_t* q) {
+  const int64_t N = c.cfg.nranks, g = p / (N * t), w = p % (N * t);
+  *owner = (int)(w / t);
+  *q = g * t + w % t;
+}
+polya_status p2p_tables(Ctx& c, const std::vector<double*>& base) {
+  int64_t t = 0, groups = 0;
+  combine_shape(c, &t, &groups);
+  const int64_t NN = c.Ntil * c.Ntil, N = c.cfg.nranks, own = groups * t;
+  std::vector<double*> tp(c.npairs_local);
+  for (int64_t pl = 0; pl < c.npairs_local; ++pl) {
+    int o;
+    int64_t q;
+    p2p_place(c, c.local_pairs[pl], t, &o, &q);
+    tp[pl] = base[o] + (c.cfg.rank * own + q) * NN;
+  }
+  std::vector<int*> fp(N);
+  for (int64_t o = 0; o < N; ++o) fp[o] = reinterpret_cast<int*>(base[o] + N * own * NN) + c.cfg.rank;
+  if (cudaMalloc(&c.d_tile_ptr, tp.size() * sizeof(double*)) != cudaSuccess ||
+      cudaMalloc(&c.d_flag_ptr, fp.size() * sizeof(int*)) != cudaSuccess ||
+      cudaMemcpy(c.d_tile_ptr, tp.data(), tp.size() * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c.d_flag_ptr, fp.data(), fp.size() * sizeof(int*), cudaMemcpyHostToDevice) != cudaSuccess) {
+    c.last_error = "polya_p2p: destination tables";
+    return POLYA_ENOMEM;
+  }
+  c.p2p_ready = true;
+  return POLYA_OK;
+}
+}  // namespace
+
+extern "C" polya_status polya_p2p_export(polya_ctx* ctx, char handle_out[64]) {
+  if (!ctx) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (c.cfg.shard != POLYA_SHARD_BLOCKS) {
+    c.last_error = "polya_p2p_export needs SHARD_BLOCKS";
+    return POLYA_EINVAL;
+  }
+  if (!c.p2p_buf) {
+    int64_t t = 0, groups = 0;
+    combine_shape(c, &t, &groups);
+    c.p2p_own = groups * t;
+    const size_t bytes = (size_t)(c.cfg.nranks * c.p2p_own * c.Ntil * c.Ntil) * sizeof(double) + 256;
+    if (cudaMalloc(&c.p2p_buf, bytes) != cudaSuccess) {
+      c.last_error = "polya_p2p_export: receive slots";
+      return POLYA_ENOMEM;
+    }
+    cudaMemset(reinterpret_cast<char*>(c.p2p_buf) + bytes - 256, 0, 256);   // the flags
+  }
+  if (handle_out) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t hnd;
+    if (cudaIpcGetMemHandle(&hnd, c.p2p_buf) != cudaSuccess) {
+      c.last_error = "cudaIpcGetMemHandle failed";
+      return POLYA_ECUDA;
+    }
+    std::memcpy(handle_out, &hnd, 64);
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_p2p_import(polya_ctx* ctx, const char* handles) {
+  if (!ctx || !handles) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (!c.p2p_buf) {
+    c.last_error = "polya_p2p_import before polya_p2p_export";
+    return POLYA_EINVAL;
+  }
+  std::vector<double*> base(c.cfg.nranks);
+  for (int r = 0; r < c.cfg.nranks; ++r) {
+    if (r == c.cfg.rank) {
+      base[r] = c.p2p_buf;
+      continue;
+    }
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, handles + 64 * r, 64);
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      c.last_error = "cudaIpcOpenMemHandle failed (peer access over NVLink needed)";
+      return POLYA_ECUDA;
+    }
+    c.p2p_opened.push_back(p);
+    base[r] = (double*)p;
+  }
+  return p2p_tables(c, base);
+}
+
+extern "C" polya_status polya_p2p_loopback(polya_ctx** ctxs, int32_t nranks) {
+  if (!ctxs || nranks < 1) return POLYA_EINVAL;
+  std::vector<double*> base(nranks);
+  for (int32_t r = 0; r < nranks; ++r) {
+    if (!ctxs[r] || ctxs[r]->c.cfg.rank != r || ctxs[r]->c.cfg.nranks != nranks) return POLYA_EINVAL;
+    polya_status st = polya_p2p_export(ctxs[r], nullptr);
+    if (st != POLYA_OK) return st;
+    base[r] = ctxs[r]->c.p2p_buf;
+  }
+  for (int32_t r = 0; r < nranks; ++r) {
+    polya_status st = p2p_tables(ctxs[r]->c, base);
+    if (st != POLYA_OK) return st;
+  }
+  return POLYA_OK;
+}
+
+extern "C" polya_status polya_schur_reduce_p2p(polya_ctx* ctx, const double* X, const double* Zinv, double* Grecv,
+                                               int phases, void* stream) {
+  if (!ctx || (phases & 1 && (!X || !Zinv)) || (phases & 2 && !Grecv) || !(phases & 3)) return POLYA_EINVAL;
+  Ctx& c = ctx->c;
+  if (!c.p2p_ready) {
+    c.last_error = "polya_schur_reduce_p2p before polya_p2p_import / polya_p2p_loopback";
+    return POLYA_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t NN = c.Ntil * c.Ntil, N = c.cfg.nranks;
+  if (phases & 1) {   // assemble into the owners' slots, then signal every owner
+    polya_status st = polya_schur_prepare(ctx, X, Zinv, stream);
+    if (st != POLYA_OK) return st;
+    ++c.p2p_epoch;
+    cudaError_t e = launch_schur(c, nullptr, POLYA_G_PAIR_TILES, c.item0, c.item1, s, c.d_tile_ptr);
+    if (e == cudaSuccess && c.timing) e = cudaEventRecord(c.ev[2], s);
+    if (e == cudaSuccess) e = launch_p2p_signal(c.d_flag_ptr, (int)N, c.p2p_epoch, s);
+    if (e != cudaSuccess) {
+      c.last_error = std::string("polya_schur_reduce_p2p: ") + cudaGetErrorString(e);
+      return POLYA_ECUDA;
+    }
+  }
+  if (phases & 2) {   // wait for every source's signal, sum the slots in rank order
+    const int* flags = reinterpret_cast<const int*>(c.p2p_buf + N * c.p2p_own * NN);
+    cudaError_t e = launch_p2p_wait(flags, (int)N, c.p2p_epoch, s);
+    if (e == cudaSuccess) e = launch_p2p_sum(c.p2p_buf, (int)N, c.p2p_own * NN, Grecv, s);
+    if (e == cudaSuccess && c.timing) e = cudaEventRecord(c.ev[3], s);
+    if (e != cudaSuccess) {
+      c.last_error = std::string("polya_schur_reduce_p2p: ") + cudaGetErrorString(e);
+      return POLYA_ECUDA;
+    }
+  }
+  return POLYA_OK;
+}
+
 namespace polya {
 void combine_free(Ctx& c) {
+  if (c.d_tile_ptr) cudaFree(c.d_tile_ptr);
+  if (c.d_flag_ptr) cudaFree(c.d_flag_ptr);
+  c.d_tile_ptr = nullptr;
+  c.d_flag_ptr = nullptr;
+  for (void* p : c.p2p_opened) cudaIpcCloseMemHandle(p);
+  c.p2p_opened.clear();
+  if (c.p2p_buf) cudaFree(c.p2p_buf);
+  c.p2p_buf = nullptr;
+  c.p2p_ready = false;
   for (auto& p : c.comb_slot) {
     if (p) cudaFree(p);
     p = nullptr;

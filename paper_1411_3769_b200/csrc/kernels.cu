@@ -336,4 +336,45 @@ cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---- the fused P2P combine of the block-sharded Schur complement (combine.cpp) ------------------
+namespace {
+__global__ void k_p2p_signal(int* const* flags, int n, int epoch) {
+  const int r = threadIdx.x;
+  if (r < n) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(flags[r]), "r"(epoch) : "memory");
+  }
+}
+__global__ void k_p2p_wait(const int* flags, int n, int epoch) {
+  for (int r = 0; r < n; ++r)
+    for (;;) {
+      int v;
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(flags + r) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(256);
+    }
+}
+__global__ void k_p2p_sum(const double* __restrict__ slots, int n, int64_t count, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = __ldcv(slots + i);   // written by peers: bypass L1
+    for (int r = 1; r < n; ++r) v += __ldcv(slots + r * count + i);   // rank order
+    out[i] = v;
+  }
+}
+}  // namespace
+
+cudaError_t launch_p2p_signal(int* const* flag_ptrs, int n, int epoch, cudaStream_t s) {
+  k_p2p_signal<<<1, 32 * ((n + 31) / 32), 0, s>>>(flag_ptrs, n, epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_wait(const int* flags, int n, int epoch, cudaStream_t s) {
+  k_p2p_wait<<<1, 1, 0, s>>>(flags, n, epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_sum(const double* slots, int n, int64_t count, double* out, cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 16);
+  k_p2p_sum<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(slots, n, count, out);
+  return cudaGetLastError();
+}
+
 }  // namespace polya

@@ -130,6 +130,15 @@ struct Ctx {
   // a dedicated comm stream, slot events (allocated on first use)
   double* comb_slot[2] = {nullptr, nullptr};
   int64_t comb_t = 0;                  // polya_set_combine_tiles (0: automatic, ~2 GiB groups)
+  // fused P2P combine (polya_p2p_*): this rank's receive slots [nranks][own tiles] + nranks flags, the
+  // per-pair destination table (a slot in the owner's buffer), the owners' flag addresses for this rank
+  double* p2p_buf = nullptr;
+  int64_t p2p_own = 0;                 // tiles each rank owns (groups x combine_tiles, padding included)
+  double** d_tile_ptr = nullptr;
+  int** d_flag_ptr = nullptr;
+  std::vector<void*> p2p_opened;       // peers' buffers opened by IPC (closed at destroy)
+  int p2p_epoch = 0;
+  bool p2p_ready = false;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t comb_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // assembled[2], reduced[2]
   std::string last_error;
@@ -161,7 +170,12 @@ cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, in
 cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
 cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s);
 cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
-cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t item0, int64_t item1, cudaStream_t s);
+cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t item0, int64_t item1, cudaStream_t s,
+                         double* const* tile_ptr = nullptr);
+// the P2P combine (kernels.cu): signal the owners, wait for every source, sum the slots in rank order
+cudaError_t launch_p2p_signal(int* const* flag_ptrs, int n, int epoch, cudaStream_t s);
+cudaError_t launch_p2p_wait(const int* flags, int n, int epoch, cudaStream_t s);
+cudaError_t launch_p2p_sum(const double* slots, int n, int64_t count, double* out, cudaStream_t s);
 // collectives of the distributed factorisation (combine.cpp; NCCL, or the loopback group of
 // polya_factor_solve_loopback; no-ops with one rank)
 struct LoopGroup {

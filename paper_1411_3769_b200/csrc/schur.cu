@@ -86,6 +86,7 @@ struct SchurArgs {
   int nsched;
   unsigned long long* counter;
   double* G;
+  double* const* tile_ptr;   // optional per-local-pair tile destination (the P2P combine: a peer's slot)
   int layout;
   int64_t K, Ntil;
   int64_t nmats;   // arena matrices (bounds checks of the POLYA_BOUNDS_CHECK build)
@@ -506,7 +507,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
       mbar_wait(full + slot, ph);
     }
     const SlotInfo it = s_info[cnt % NSTAGE];
-    if (it.item >= p.item1) break;
+    if (it.item >= p.item1) {
+      if (p.tile_ptr) __threadfence_system();   // P2P combine: the stores to peer memory before the signal
+      break;
+    }
     const bool dS = (it.ci == it.cj), dT = (it.ck == it.cl);
     const int tb = icount & 1;
     ++icount;
@@ -560,7 +564,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
     const bool same_cls = diag_pair && (it.sc == it.tc);
     const bool fullG = (p.layout == POLYA_G_FULL);
     const int64_t rowbase = (int64_t)it.h * p.Ntil, colbase = (int64_t)it.h2 * p.Ntil;
-    double* tile = p.G + (int64_t)it.pl * p.Ntil * p.Ntil;
+    double* tile = p.tile_ptr ? p.tile_ptr[it.pl] : p.G + (int64_t)it.pl * p.Ntil * p.Ntil;
     const int4 none = make_int4(-1, 0, 0, 0);
     auto passes = [&](auto diag_tag) {
       constexpr bool DIAG = decltype(diag_tag)::value;
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
 
 }  // namespace
 
-cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, cudaStream_t s) {
+cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, cudaStream_t s, double* const* tile_ptr) {
   if (i1 <= i0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(c.st.counter, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
@@ -644,7 +648,7 @@ cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t i0, int64_t i1, 
   a.sched_lo = full ? c.st.sched_lo : nullptr;
   a.sched_prefix = full ? c.st.sched_prefix : nullptr;
   a.nsched = full ? (int)c.st.nsched : 0;
-  a.G = G; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil; a.nmats = c.nmats;
+  a.G = G; a.tile_ptr = tile_ptr; a.layout = layout; a.K = c.K; a.Ntil = c.Ntil; a.nmats = c.nmats;
   k_schur<<<(unsigned)want, NT, kSmemBytes, s>>>(a);
   ++c.launches;
   return cudaGetLastError();

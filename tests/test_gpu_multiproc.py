@@ -4,8 +4,8 @@ scaling run has eight).
 
 Per rank, in its own process on its own GPU:
 * SHARD_BLOCKS: the rank's partial G over its Polya blocks, summed by polya_reduce_G
-  (ncclReduceScatter) into row-panel ranges -- the concatenated panels equal the one-rank G to 1e-12
-  and the literal oracle (Eq. T2) to 1e-10;
+  (ncclReduceScatter), by the pipelined polya_schur_reduce and by the fused P2P combine (K4 storing
+  into the owners' slots over NVLink) -- all equal the literal oracle (Eq. T2) to 1e-10;
 * SHARD_TILES: each rank's work items written into a zeroed K x K G; the sum over ranks is the
   one-rank G bit for bit (disjoint entries) and the oracle to 1e-10;
 * SHARD_CYCLIC: three polya_ipm_step iterations with the distributed factorisation match the
@@ -26,7 +26,7 @@ pytestmark = pytest.mark.gpu
 WORLD = 2
 
 
-def _rank_main(rank, world, q_uid, q_out, cid):
+def _rank_main(rank, world, q_uid, q_out, q_hnd, cid):
     import torch
 
     import paper_1411_3769_b200 as pb
@@ -54,6 +54,19 @@ def _rank_main(rank, world, q_uid, q_out, cid):
     cb.set_combine_tiles(1)                                       # pipelined: one tile per rank and group
     out["blocks_pipe"] = cb.schur_reduce(Xd, Wd).cpu().numpy()
     out["combine_tiles"] = cb.dims["combine_tiles"]
+    # fused P2P combine: K4 stores into the owners' slots over NVLink peer memory
+    mine = cb.p2p_export()
+    for _ in range(world - 1):          # one copy for every other rank
+        q_hnd.put((rank, mine))
+    hs = {rank: mine}
+    while len(hs) < world:
+        rr, hh = q_hnd.get()
+        if rr == rank:
+            q_hnd.put((rr, hh))
+            continue
+        hs[rr] = hh
+    cb.p2p_import([hs[r] for r in range(world)])
+    out["blocks_p2p"] = cb.schur_reduce_p2p(Xd, Wd).cpu().numpy()
     torch.cuda.synchronize()
     cb.close()
     # output-tile sharding
@@ -85,8 +98,8 @@ def test_two_ranks_blocks_tiles_cyclic(cid):
         pytest.skip(f"needs {WORLD} GPUs (found {torch.cuda.device_count()})")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    q_uid, q_out = ctx.Queue(), ctx.Queue()
-    procs = [ctx.Process(target=_rank_main, args=(r, WORLD, q_uid, q_out, cid)) for r in range(WORLD)]
+    q_uid, q_out, q_hnd = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, WORLD, q_uid, q_out, q_hnd, cid)) for r in range(WORLD)]
     for p in procs:
         p.start()
     outs = sorted([q_out.get(timeout=600) for _ in range(WORLD)], key=lambda o: o["rank"])
@@ -118,8 +131,10 @@ def test_two_ranks_blocks_tiles_cyclic(cid):
     t_auto = -(-(P.L0 * (P.L0 + 1) // 2) // WORLD)     # small tiles: one group of ceil(npairs / N)
     whole = tiles_of("blocks_panel", t_auto)
     pipe = tiles_of("blocks_pipe", outs[0]["combine_tiles"])
-    assert rel(whole, tiles_ref) <= 1e-10 and rel(pipe, tiles_ref) <= 1e-10
+    p2p = tiles_of("blocks_p2p", outs[0]["combine_tiles"])
+    assert rel(whole, tiles_ref) <= 1e-10 and rel(pipe, tiles_ref) <= 1e-10 and rel(p2p, tiles_ref) <= 1e-10
     assert np.array_equal(whole, pipe)          # same partials, same NCCL sums
+    assert rel(p2p, pipe) <= 1e-13              # rank-order sums vs NCCL's order
     Gt = sum(o["tiles_G"] for o in outs)
     assert rel(Gt, Gref) <= 1e-10 and np.array_equal(Gt, Gt.T)
     if cid != 2:      # the oracle's dense IPM step is minutes at config 3

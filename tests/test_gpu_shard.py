@@ -176,3 +176,42 @@ def test_pipelined_combine_needs_communicator_for_several_ranks(pb):
     with pytest.raises(pb.PolyaError):
         t.schur_reduce(Xd, Wd)                      # SHARD_TILES: nothing to combine
     t.close()
+
+
+@pytest.mark.parametrize("cfg,world,tiles", [(synth.CONFIGS[2], 2, 0), (synth.CONFIGS[2], 3, 1),
+                                             (synth.small_config(12, 3, 2, 1, 2), 5, 1), (synth.CONFIGS[3], 4, 2)],
+                         ids=lambda v: getattr(v, "name", str(v)))
+def test_fused_p2p_combine_loopback(pb, cfg, world, tiles):
+    """The fused P2P combine (polya_schur_reduce_p2p): K4 of every rank stores its partial tiles straight
+    into the owners' receive slots, each owner sums its slots in rank order.  On one GPU the ranks are
+    contexts wired by polya_p2p_loopback, phase 1 (assembly + signal) for all of them before phase 2
+    (wait + sum).  Every rank's result is bit for bit the rank-order sum of the ranks' partial G tiles
+    (polya_schur per rank), in the tile-group layout of polya_reduce_G; a second call (next epoch) too."""
+    A, X, W = _inputs(cfg)
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    ctxs = [pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A, rank=r, nranks=world, shard=pb.SHARD_BLOCKS)
+            for r in range(world)]
+    for c in ctxs:
+        c.set_combine_tiles(tiles)
+    parts = [c.schur(Xd, Wd, layout=pb.G_PAIR_TILES).cpu().numpy() for c in ctxs]
+    total = parts[0].copy()
+    for q in parts[1:]:
+        total += q                      # rank order, as the owners sum their slots
+    pb.p2p_loopback(ctxs)
+    N = ctxs[0].Ntil
+    NN = N * N
+    t = ctxs[0].dims["combine_tiles"]
+    npairs = ctxs[0].dims["npairs"]
+    for _ in range(2):
+        for c in ctxs:
+            c.schur_reduce_p2p(Xd, Wd, phases=1)
+        outs = [c.schur_reduce_p2p(Xd, Wd, phases=2).cpu().numpy() for c in ctxs]
+        for r, out in enumerate(outs):
+            assert out.size == ctxs[r].dims["reduce_count"]
+            for slot in range(out.size // NN):
+                g, j = divmod(slot, t)
+                p = g * world * t + r * t + j
+                if p < npairs:
+                    assert np.array_equal(out[slot * NN:(slot + 1) * NN], total[p * NN:(p + 1) * NN]), (r, slot)
+    for c in ctxs:
+        c.close()
