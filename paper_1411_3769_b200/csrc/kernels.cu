@@ -192,6 +192,19 @@ __global__ void __launch_bounds__(256) k_gemm(double* __restrict__ arena, int64_
       const int i = i0 + wr + mi * 8 + g, j = j0 + wc + nj * 8 + 2 * t;
       if (i < np && j < np) *reinterpret_cast<double2*>(C + (int64_t)i * np + j) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
     }
+  if (it.ct_id >= 0) {   // the transpose as well (8 lanes of a row group store 64 contiguous bytes)
+    double* Ct = arena + (int64_t)it.ct_id * ms;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const int i = i0 + wr + mi * 8 + g, j = j0 + wc + nj * 8 + 2 * t;
+        if (i < np && j < np) {
+          Ct[(int64_t)j * np + i] = acc[mi][nj][0];
+          Ct[(int64_t)(j + 1) * np + i] = acc[mi][nj][1];
+        }
+      }
+  }
 }
 
 // V_h(y) (Eq. 30) for every h into the arena (n = order of P; zero beyond it, reading R19).

@@ -528,19 +528,16 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
                                    {(int32_t)(c.id_Abar + t), (int32_t)(c.id_X + b)}, {(int32_t)(c.id_Abar + t), (int32_t)(c.id_W + b)}};
         const int64_t dst[4] = {c.id_U, c.id_V, c.id_Ut, c.id_Vt};
         for (int k = 0; k < 4; ++k) {
-          it.push_back({(int32_t)(dst[k] + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+          it.push_back({(int32_t)(dst[k] + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
           tm.push_back({ids[k][0], ids[k][1], 0, 0, 1.0});
         }
         continue;
       }
-      it.push_back({(int32_t)(c.id_U + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      // X, W symmetric (polya_schur's contract), so X H^T = U^T and W H^T = V^T: stored by the same items
+      it.push_back({(int32_t)(c.id_U + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, (int32_t)(c.id_Ut + t)});
       tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_X + b), 0, 0, 1.0});
-      it.push_back({(int32_t)(c.id_V + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      it.push_back({(int32_t)(c.id_V + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, (int32_t)(c.id_Vt + t)});
       tm.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_W + b), 0, 0, 1.0});
-      it.push_back({(int32_t)(c.id_Ut + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
-      tm.push_back({(int32_t)(c.id_X + b), (int32_t)(c.id_H + t), 1, 0, 1.0});
-      it.push_back({(int32_t)(c.id_Vt + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
-      tm.push_back({(int32_t)(c.id_W + b), (int32_t)(c.id_H + t), 1, 0, 1.0});
     }
     c.n_items_UV = (int64_t)it.size();
     c.d_items_UV = dupload(it);
@@ -549,7 +546,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     it.clear(); tm.clear();
     if (c.gen) {
       for (int64_t t = 0; t < nnzH; ++t) {
-        it.push_back({(int32_t)(c.id_XA + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        it.push_back({(int32_t)(c.id_XA + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
         tm.push_back({(int32_t)(c.id_Xt + c.L + c.Hm[t]), (int32_t)(c.id_Abar + t), 1, 0, 1.0});
       }
       c.n_items_T0 = (int64_t)it.size();
@@ -558,7 +555,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
       it.clear(); tm.clear();
     }
     for (int64_t t = 0; t < nnzH; ++t) {
-      it.push_back({(int32_t)(c.id_T + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+      it.push_back({(int32_t)(c.id_T + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
       if (c.gen)
         tm.push_back({(int32_t)(c.id_B + t), (int32_t)(c.id_XA + t), 0, 0, 1.0});
       else
@@ -571,7 +568,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     it.clear(); tm.clear();
     if (c.gen) {
       for (int64_t t = 0; t < nnzH; ++t) {
-        it.push_back({(int32_t)(c.id_VB + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        it.push_back({(int32_t)(c.id_VB + t), (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
         tm.push_back({(int32_t)(c.id_Vy + c.Hh[t]), (int32_t)(c.id_B + t), 0, 0, 1.0});
       }
       c.n_items_S0 = (int64_t)it.size();
@@ -591,7 +588,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
           tm.push_back({(int32_t)(c.id_Vy + h), (int32_t)(c.id_H + t), 0, 0, 1.0});
         }
       }
-      it.push_back({(int32_t)(c.id_S + m), b0, (int32_t)tm.size(), 0});
+      it.push_back({(int32_t)(c.id_S + m), b0, (int32_t)tm.size(), -1});
     }
     c.n_items_S = (int64_t)it.size();
     c.d_items_S = dupload(it);
@@ -630,9 +627,9 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
                                           {(int32_t)(c.id_Ut + q1), B2, (int32_t)(c.id_Vt + q2), B1}};
               for (int k = 0; k < 4; ++k) {
                 const int32_t idL = (int32_t)(c.id_Q + 4 * q + k), idR = (int32_t)(c.id_R + 4 * q + k);
-                it.push_back({idL, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+                it.push_back({idL, (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
                 tm.push_back({spec[k][0], spec[k][1], 1, 0, 1.0});
-                it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+                it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
                 tm.push_back({spec[k][2], spec[k][3], 1, 0, 1.0});
                 kL.push_back(idL); kR.push_back(idR);
               }
@@ -642,9 +639,9 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
         }
         const int32_t idQ = (int32_t)(c.id_Q + q), idR = (int32_t)(c.id_R + q);
         // Q_{hh'} = U_h H_{h'}^T,  R_{h'h} = V_{h'} H_h^T
-        it.push_back({idQ, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        it.push_back({idQ, (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
         tm.push_back({(int32_t)(c.id_U + th), (int32_t)(c.id_H + th2), 1, 0, 1.0});
-        it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, 0});
+        it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
         tm.push_back({(int32_t)(c.id_V + th2), (int32_t)(c.id_H + th), 1, 0, 1.0});
         ++q;
         // T1 = U_{h'}^T[b1,c1] V_h^T[d1,a1]; T2 = X[b1,c1] R_{h'h}[d1,a1];

@@ -24,9 +24,10 @@ struct GemmTerm {
   int32_t pad_;
   double alpha;
 };
-// One output matrix of a batched GEMM: C[c_id] = sum_{t in [tbeg,tend)} terms[t].
+// One output matrix of a batched GEMM: C[c_id] = sum_{t in [tbeg,tend)} terms[t]; if ct_id >= 0 its
+// transpose is also stored to C[ct_id].
 struct GemmItem {
-  int32_t c_id, tbeg, tend, pad_;
+  int32_t c_id, tbeg, tend, ct_id;
 };
 
 // dst = sum_terms w * coef[src] (or its transpose): the generalised form's A_t, A_t^T, B_t (set-up).

@@ -264,8 +264,9 @@ __device__ __forceinline__ double gval(const double* Gs, int4 r, int4 c) {
 // item's nstage ring stages, then folded into Gs.  MMA rows are M-tiles (p, q) of 8 rows
 // g -> (x, y) = (2p + (g & 1), 4q + (g >> 1)), columns N-tiles (p', q') the same way over (z, w).
 // Full chunks: 8 M-tiles, warp row wm (of the 2 x 2 warp grid) takes q = wm, p = 0..3; a ragged x
-// chunk (<= 4 valid x) needs p < 2 only (q = wm, p = 0..1), a ragged y chunk (<= 4 valid y) q = 0
-// only (p = 2 wm + 0..1), both one tile (q = 0, p = wm) -- invalid rows are never multiplied.  A
+// chunk (<= 4 valid x) needs p < 2 only (q = wm, p = 0..1), one with 5-6 valid x p < 3, a ragged y
+// chunk (<= 4 valid y) q = 0 only (p = 2 wm + 0..1), both one tile (q = 0, p = wm) -- invalid rows
+// (x, z) are never multiplied (a y / w chunk with 5-7 valid values keeps its q = 1 tiles whole).  A
 // warp's tiles differ in p only, so their fragments sit at +512-byte steps of one lane offset.
 template <int MI, int NJ, int RY, int RW>
 __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
@@ -357,12 +358,14 @@ __device__ __forceinline__ void orient(const SchurArgs& p, double* smem, double*
 }
 
 // (M side, N side) code -> instantiation: code 0: 8 tiles (4 per warp), 1: 4 tiles of a ragged x / z
-// chunk, 2: 4 tiles of a ragged y / w chunk, 3: 2 tiles (both ragged).
+// chunk, 2: 4 tiles of a ragged y / w chunk, 3: 2 tiles (both ragged), 4: 6 tiles of an x / z chunk
+// with 5-6 valid values (p < 3: rows x = 6, 7 are never formed).
 #define ORIENT_M(MC, MI, RY)                                                                          \
-  case MC * 4 + 0: orient<MI, 4, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
-  case MC * 4 + 1: orient<MI, 2, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
-  case MC * 4 + 2: orient<MI, 2, RY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
-  case MC * 4 + 3: orient<MI, 1, RY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break;
+  case MC * 5 + 0: orient<MI, 4, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 5 + 1: orient<MI, 2, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 5 + 2: orient<MI, 2, RY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 5 + 3: orient<MI, 1, RY, 1>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break; \
+  case MC * 5 + 4: orient<MI, 3, RY, 0>(p, smem, Gs, full, empty, cnt, nstage, o, first, pbar, nph); break;
 __device__ __forceinline__   // inlined: the out-of-line call cost 1.7 ms (cfg 4) and 34 ms (cfg 5)
 void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uint64_t* full,
                                              uint64_t* empty, uint32_t& cnt, int nstage, int o, bool first,
@@ -372,6 +375,7 @@ void orient_dispatch(int code, const SchurArgs& p, double* smem, double* Gs, uin
     ORIENT_M(1, 2, 0)
     ORIENT_M(2, 2, 1)
     ORIENT_M(3, 1, 1)
+    ORIENT_M(4, 3, 0)
   }
 }
 #undef ORIENT_M
@@ -552,8 +556,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
       // multiplying 8-row tiles that are half zeros
       const bool rY = (n - cY * Q) <= 4, rW = (n - cW * Q) <= 4;   // packed MMA rows / columns
       const bool rX = (n - cX * Q) <= 4, rZ = (n - cZ * Q) <= 4;   // only 4 x (z) values exist
-      const int mcode = rY ? (rX ? 3 : 2) : (rX ? 1 : 0), ncode = rW ? (rZ ? 3 : 2) : (rZ ? 1 : 0);
-      orient_dispatch(mcode * 4 + ncode, p, smem, Gs, full, empty, cnt, it.nstage, o, first, &s_pbar, nph);
+      const bool sX = (n - cX * Q) <= 6, sZ = (n - cZ * Q) <= 6;   // only 6: x (z) = 6, 7 never formed
+      const int mcode = rY ? (rX ? 3 : 2) : (rX ? 1 : (sX ? 4 : 0));
+      const int ncode = rW ? (rZ ? 3 : 2) : (rZ ? 1 : (sZ ? 4 : 0));
+      orient_dispatch(mcode * 5 + ncode, p, smem, Gs, full, empty, cnt, it.nstage, o, first, &s_pbar, nph);
       first = false;
     }
     if (SCHUR_EXP & 3) continue;   // timing experiment: no epilogue

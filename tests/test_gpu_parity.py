@@ -49,6 +49,8 @@ SMALL = [synth.CONFIGS[1], synth.CONFIGS["1u"], synth.CONFIGS[2],
          synth.small_config(12, 3, 2, 1, 2),      # np = 16: two chunks, ragged tail of 4
          synth.small_config(9, 2, 1, 2, 1),       # ragged tail of 1
          synth.small_config(20, 2, 2, 1, 1),      # three chunks, ragged tail of 4
+         synth.small_config(14, 2, 2, 1, 1),      # ragged tail of 6 (rows x, z = 6, 7 never formed)
+         synth.small_config(13, 3, 1, 1, 1),      # ragged tail of 5
          synth.small_config(1, 3, 1, 1, 1),       # n = 1 (single padded chunk)
          synth.small_config(5, 1, 0, 2, 3),       # l = 1, dp = 0 (K = Ntil)
          synth.small_config(6, 3, 2, 0, 0)]       # d1 = d2 = 0: pairs with no common block
