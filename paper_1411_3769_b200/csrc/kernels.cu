@@ -207,6 +207,128 @@ __global__ void __launch_bounds__(256) k_gemm(double* __restrict__ arena, int64_
   }
 }
 
+// K3b: row-gathered GEMM for the SCM precompute (standard form, np <= 128).  U_t = H_t X_m for all t of
+// one block m share X_m, and Q_{hh'} = U_h H_{h'}^T for all h paired with h' (one m) share H_{h'}: a group
+// stacks the rows of its left operands (np rows each) and a CTA computes 64 stacked rows x all np columns
+// (8 warps: 4 x 16 rows, 2 column halves of <= 8 8x8 tiles; 32 accumulators per thread), so the output
+// tile is never ragged in the row direction except at a group's end and the column split is within one
+// tile of even (np = 104: 7 + 6 tiles) -- vs 64x64 tiles of one np x np output, where np = 104 leaves
+// 34 % of the warp tiles beyond np.  K streamed in chunks of 16 through a 3-stage cp.async ring, the
+// conflict-free layouts of k_gemm ([i][k] stride 20; [k][j] stride 132 or, transposed, [j][k] stride 20).
+constexpr int RT = 64;                  // stacked rows per CTA
+constexpr int RBN = 132;                // [k][j] row stride (= 4 mod 16), np <= 128
+constexpr int RABUF = RT * AS;          // 1280
+constexpr int RBBUF = 128 * AS > GK * RBN ? 128 * AS : GK * RBN;   // 2560 / 2112
+constexpr size_t kRgSmem = (size_t)GST * (RABUF + RBBUF) * sizeof(double);   // 92,160 bytes
+template <bool TRANS>
+__global__ void __launch_bounds__(256, 2) k_rgemm(double* __restrict__ arena, int64_t ms, int np,
+                                                  const RgGroup* __restrict__ groups, const RgEnt* __restrict__ ents,
+                                                  const RgTile* __restrict__ tiles) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;
+  double* Bs = gsm + GST * RABUF;
+  const RgTile tl = tiles[blockIdx.x];
+  const RgGroup gr = groups[tl.group];
+  const int rows = (gr.eend - gr.ebeg) * np;   // stacked rows of the group
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int nt8 = np >> 3, nh = (nt8 + 1) >> 1;
+  const int jc0 = wn * nh, ncw = wn ? nt8 - nh : nh;   // the warp's column tiles [jc0, jc0 + ncw)
+  const double* B = arena + (int64_t)gr.b_id * ms;
+  // the two stacked A rows this thread copies (fixed over the K loop)
+  const double* arow[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int R = tl.r0 + ((tid + r * 256) >> 3);
+    arow[r] = nullptr;
+    if (R < rows) {
+      const int e = R / np;
+      arow[r] = arena + (int64_t)ents[gr.ebeg + e].a_id * ms + (int64_t)(R - e * np) * np;
+    }
+  }
+  const int nkc = (np + GK - 1) / GK;
+  auto issue = [&](int c, int buf) {
+    const int k0 = c * GK;
+    double* as = As + buf * RABUF;
+    double* bs = Bs + buf * RBBUF;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int q = tid + r * 256, i = q >> 3, kc = (q & 7) * 2;
+      const bool v = arow[r] != nullptr && k0 + kc < np;
+      cp16z(&as[i * AS + kc], v ? arow[r] + k0 + kc : B, v);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int q = tid + r * 256;
+      if (!TRANS) {   // B rows k0..k0+15, columns 0..np-1
+        const int k = q >> 6, jc = (q & 63) * 2;
+        const bool v = k0 + k < np && jc < np;
+        cp16z(&bs[k * RBN + jc], v ? B + (int64_t)(k0 + k) * np + jc : B, v);
+      } else {        // op(B)[k][j] = B[j][k]: rows j of B, columns k0..k0+15
+        const int j = q >> 3, kc = (q & 7) * 2;
+        const bool v = j < np && k0 + kc < np;
+        cp16z(&bs[j * AS + kc], v ? B + (int64_t)j * np + k0 + kc : B, v);
+      }
+    }
+  };
+  double acc[2][8][2] = {};
+  bool mv[2];   // warp-uniform: the 8-row tile holds stacked rows of the group (not the padding of its last tile)
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) mv[mi] = tl.r0 + wm * 16 + mi * 8 < rows;
+#pragma unroll
+  for (int p = 0; p < GST - 1; ++p) {
+    if (p < nkc) issue(p, p);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int c = 0; c < nkc; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GST - 2) : "memory");
+    __syncthreads();   // chunk c landed for every thread; the buffer of chunk c-1 is free
+    if (c + GST - 1 < nkc) issue(c + GST - 1, (c + GST - 1) % GST);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const double* as = As + (c % GST) * RABUF;
+    const double* bs = Bs + (c % GST) * RBBUF;
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      if (c * GK + ks * 4 >= np) break;   // np is a multiple of 8: the last chunk may hold 2 k-steps only
+      double a[2], b[8];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) a[mi] = as[(wm * 16 + mi * 8 + g) * AS + ks * 4 + t];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < ncw) {
+          const int col = (jc0 + j) * 8 + g;
+          b[j] = TRANS ? bs[col * AS + ks * 4 + t] : bs[(ks * 4 + t) * RBN + col];
+        }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < ncw) {
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+            if (mv[mi]) dmma(acc[mi][j][0], acc[mi][j][1], a[mi], b[j]);
+        }
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) {
+    const int R = tl.r0 + wm * 16 + mi * 8 + g;
+    if (R >= rows) continue;
+    const int e = R / np, row = R - e * np;
+    const RgEnt en = ents[gr.ebeg + e];
+    double* C = arena + (int64_t)en.c_id * ms;
+    double* Ct = en.ct_id >= 0 ? arena + (int64_t)en.ct_id * ms : nullptr;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < ncw) {
+        const int col = (jc0 + j) * 8 + 2 * t;
+        *reinterpret_cast<double2*>(C + (int64_t)row * np + col) = make_double2(acc[mi][j][0], acc[mi][j][1]);
+        if (Ct) {
+          Ct[(int64_t)col * np + row] = acc[mi][j][0];
+          Ct[(int64_t)(col + 1) * np + row] = acc[mi][j][1];
+        }
+      }
+  }
+}
+
 // V_h(y) (Eq. 30) for every h into the arena (n = order of P; zero beyond it, reading R19).
 __global__ void k_vmap(double* __restrict__ arena, int64_t ms, int np, int n, int64_t Ntil,
                        const double* __restrict__ y, int64_t id_Vy) {
@@ -325,6 +447,21 @@ cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, in
     k_gemm<<<grid, 256, kGemmSmem, s>>>(c.arena, c.mstride, (int)c.np, items + off, terms, tiles);
     ++c.launches;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rgemm(Ctx& c, int phase, cudaStream_t s) {
+  const int64_t nt = c.n_rg_tile[phase];
+  if (nt == 0) return cudaSuccess;
+  // transB is uniform per launch: phase 0 (U, V) multiplies by X, W; phase 1 (Q, R) by H^T
+  cudaError_t e = cudaFuncSetAttribute(phase ? k_rgemm<true> : k_rgemm<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRgSmem);
+  if (e != cudaSuccess) return e;
+  if (phase)
+    k_rgemm<true><<<(unsigned)nt, 256, kRgSmem, s>>>(c.arena, c.mstride, (int)c.np, c.d_rg_grp[1], c.d_rg_ent[1], c.d_rg_tile[1]);
+  else
+    k_rgemm<false><<<(unsigned)nt, 256, kRgSmem, s>>>(c.arena, c.mstride, (int)c.np, c.d_rg_grp[0], c.d_rg_ent[0], c.d_rg_tile[0]);
+  ++c.launches;
   return cudaGetLastError();
 }
 

@@ -108,6 +108,20 @@ T* dupload(const std::vector<T>& v) {
   return p;
 }
 
+// K3b descriptors of one precompute launch: the groups, their entries and the 64-row tiles of each group.
+void rg_upload(Ctx& c, int phase, const std::vector<RgGroup>& grp, const std::vector<RgEnt>& ent) {
+  std::vector<RgTile> tiles;
+  for (size_t g = 0; g < grp.size(); ++g) {
+    const int64_t rows = (int64_t)(grp[g].eend - grp[g].ebeg) * c.np;
+    if (rows > INT32_MAX) throw Fail{POLYA_EOVERFLOW, "precompute group too large"};
+    for (int64_t r0 = 0; r0 < rows; r0 += 64) tiles.push_back({(int32_t)g, (int32_t)r0});
+  }
+  c.d_rg_grp[phase] = dupload(grp);
+  c.d_rg_ent[phase] = dupload(ent);
+  c.d_rg_tile[phase] = dupload(tiles);
+  c.n_rg_tile[phase] = (int64_t)tiles.size();
+}
+
 // The generalised form's input terms (polya_setup_general, reading R18).
 struct GenInput {
   int32_t nterms;
@@ -542,6 +556,24 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     c.n_items_UV = (int64_t)it.size();
     c.d_items_UV = dupload(it);
     c.d_terms_UV = dupload(tm);
+    c.rg = !c.gen && c.np <= 128;
+    if (c.rg) {   // K3b groups: U_t, V_t of one block m share X_m, W_m (U^T, V^T by transposed stores)
+      std::vector<std::vector<int32_t>> per_m((size_t)c.M);
+      for (int64_t t = 0; t < nnzH; ++t)
+        if (owned((int32_t)(c.L + c.Hm[t]))) per_m[(size_t)c.Hm[t]].push_back((int32_t)t);
+      std::vector<RgGroup> grp;
+      std::vector<RgEnt> ent;
+      for (int64_t m = 0; m < c.M; ++m) {
+        if (per_m[(size_t)m].empty()) continue;
+        for (int w = 0; w < 2; ++w) {
+          const int32_t e0 = (int32_t)ent.size();
+          for (int32_t t : per_m[(size_t)m])
+            ent.push_back({(int32_t)(c.id_H + t), (int32_t)((w ? c.id_V : c.id_U) + t), (int32_t)((w ? c.id_Vt : c.id_Ut) + t), 0});
+          grp.push_back({(int32_t)((w ? c.id_W : c.id_X) + c.L + m), 0, e0, (int32_t)ent.size()});
+        }
+      }
+      rg_upload(c, 0, grp, ent);
+    }
     // adjoint: T_t = H_t Xt_{L+m}; generalised T_t = B_t (Xt_{L+m} A_t) (two passes)
     it.clear(); tm.clear();
     if (c.gen) {
@@ -599,6 +631,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
   {
     std::vector<int32_t> qh, qh2, kL, kR;
     std::vector<int64_t> kbeg, pitem;
+    std::vector<std::vector<RgEnt>> rgQ(c.rg ? (size_t)nnzH : 0), rgR(c.rg ? (size_t)nnzH : 0);   // K3b, by H operand
     std::vector<GemmItem> it;
     std::vector<GemmTerm> tm;
     int64_t q = 0;
@@ -639,6 +672,10 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
         }
         const int32_t idQ = (int32_t)(c.id_Q + q), idR = (int32_t)(c.id_R + q);
         // Q_{hh'} = U_h H_{h'}^T,  R_{h'h} = V_{h'} H_h^T
+        if (c.rg) {
+          rgQ[(size_t)th2].push_back({(int32_t)(c.id_U + th), idQ, -1, 0});
+          rgR[(size_t)th].push_back({(int32_t)(c.id_V + th2), idR, -1, 0});
+        }
         it.push_back({idQ, (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
         tm.push_back({(int32_t)(c.id_U + th), (int32_t)(c.id_H + th2), 1, 0, 1.0});
         it.push_back({idR, (int32_t)tm.size(), (int32_t)tm.size() + 1, -1});
@@ -666,6 +703,18 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
       pitem.push_back(c.local_item[lp + 1]);
     }
     c.nk_local = (int64_t)kL.size();
+    if (c.rg) {   // K3b groups: the Q (R) of one H_{t} operand (one h, one block m) share it
+      std::vector<RgGroup> grp;
+      std::vector<RgEnt> ent;
+      for (int64_t t = 0; t < nnzH; ++t)
+        for (auto* lst : {&rgQ[(size_t)t], &rgR[(size_t)t]}) {
+          if (lst->empty()) continue;
+          const int32_t e0 = (int32_t)ent.size();
+          ent.insert(ent.end(), lst->begin(), lst->end());
+          grp.push_back({(int32_t)(c.id_H + t), 1, e0, (int32_t)ent.size()});
+        }
+      rg_upload(c, 1, grp, ent);
+    }
     c.n_items_QR = (int64_t)it.size();
     c.d_items_QR = dupload(it);
     c.d_terms_QR = dupload(tm);
@@ -776,6 +825,11 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
 }
 
 void free_ctx(Ctx& c) {
+  for (int ph = 0; ph < 2; ++ph) {
+    if (c.d_rg_grp[ph]) cudaFree(c.d_rg_grp[ph]);
+    if (c.d_rg_ent[ph]) cudaFree(c.d_rg_ent[ph]);
+    if (c.d_rg_tile[ph]) cudaFree(c.d_rg_tile[ph]);
+  }
   void* ps[] = {c.arena, c.dA, c.dHw, c.d_items_UV, c.d_terms_UV, c.d_items_QR, c.d_terms_QR,
                 c.d_items_T, c.d_terms_T, c.d_sc_dst, c.d_sc_src, c.d_sc_w, c.d_items_S, c.d_terms_S, c.d_bP_beg, c.d_bP_h, c.d_bP_w,
                 c.d_hP_beg, c.d_hP_j, c.d_hP_w, c.d_hL_beg, c.d_hL_t, c.d_hL_m, c.st.pair_h, c.st.pair_h2,
@@ -1071,8 +1125,13 @@ extern "C" polya_status polya_schur_prepare(polya_ctx* ctx, const double* X, con
     CU(launch_pad_copy(c, X, c.id_X, c.nb, 0, s));
     CU(launch_pad_copy(c, Zinv, c.id_W, c.nb, 0, s));
     CU(launch_scale_copy(c, s));
-    CU(launch_gemm(c, c.d_items_UV, c.d_terms_UV, c.n_items_UV, s));
-    CU(launch_gemm(c, c.d_items_QR, c.d_terms_QR, c.n_items_QR, s));
+    if (c.rg) {
+      CU(launch_rgemm(c, 0, s));
+      CU(launch_rgemm(c, 1, s));
+    } else {
+      CU(launch_gemm(c, c.d_items_UV, c.d_terms_UV, c.n_items_UV, s));
+      CU(launch_gemm(c, c.d_items_QR, c.d_terms_QR, c.n_items_QR, s));
+    }
     if (c.timing) CU(cudaEventRecord(c.ev[1], s));
   } catch (const Fail& f) {
     return fail(ctx, f);

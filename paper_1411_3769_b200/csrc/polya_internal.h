@@ -30,6 +30,19 @@ struct GemmItem {
   int32_t c_id, tbeg, tend, ct_id;
 };
 
+// Row-gathered GEMM (kernel K3b, the SCM precompute of the standard form with np <= 128): a group shares
+// one right operand op(B[b_id]) and stacks the rows of its entries' A matrices; each entry's rows of
+// A op(B) go to C[c_id] (and, if ct_id >= 0, transposed to C[ct_id]).  A tile = 64 stacked rows of a group.
+struct RgGroup {
+  int32_t b_id, transB, ebeg, eend;
+};
+struct RgEnt {
+  int32_t a_id, c_id, ct_id, pad_;
+};
+struct RgTile {
+  int32_t group, r0;
+};
+
 // dst = sum_terms w * coef[src] (or its transpose): the generalised form's A_t, A_t^T, B_t (set-up).
 struct WsumItem {
   int32_t dst, beg, end, trans;
@@ -105,6 +118,10 @@ struct Ctx {
   // batched gemm descriptors
   GemmItem* d_items_UV = nullptr; GemmTerm* d_terms_UV = nullptr; int64_t n_items_UV = 0;
   GemmItem* d_items_QR = nullptr; GemmTerm* d_terms_QR = nullptr; int64_t n_items_QR = 0;
+  // K3b row-gathered form of the same two launches (standard form, np <= 128): [0] U, V (+ U^T, V^T), [1] Q, R
+  RgGroup* d_rg_grp[2] = {nullptr, nullptr}; RgEnt* d_rg_ent[2] = {nullptr, nullptr};
+  RgTile* d_rg_tile[2] = {nullptr, nullptr}; int64_t n_rg_tile[2] = {0, 0};
+  bool rg = false;
   GemmItem* d_items_T = nullptr; GemmTerm* d_terms_T = nullptr; int64_t n_items_T = 0;
   GemmItem* d_items_S = nullptr; GemmTerm* d_terms_S = nullptr; int64_t n_items_S = 0;
   GemmItem* d_items_T0 = nullptr; GemmTerm* d_terms_T0 = nullptr; int64_t n_items_T0 = 0;  // generalised: XA_t
@@ -168,6 +185,7 @@ cudaError_t launch_pad_copy(Ctx& c, const double* src, int64_t id0, int64_t coun
 cudaError_t launch_scale_copy(Ctx& c, cudaStream_t s);
 cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, int64_t nitems,
                         cudaStream_t s);
+cudaError_t launch_rgemm(Ctx& c, int phase, cudaStream_t s);
 cudaError_t launch_vmap(Ctx& c, const double* y, cudaStream_t s);
 cudaError_t launch_apply_out(Ctx& c, const double* y, double* out, cudaStream_t s);
 cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
