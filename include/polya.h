@@ -302,10 +302,14 @@ polya_status polya_get_combine_timing(polya_ctx* ctx, float* ms_exposed);
  *   peers' slots (peer access) and builds the destination tables.
  * polya_p2p_loopback: test hook -- the nranks contexts of one process on one device wired directly.
  * polya_schur_reduce_p2p: phases bit 1 = precompute + assembly into the owners' slots + a system-scope
- *   release of this rank's flag in every owner; bit 2 = wait for every source's flag, then the sum.
- *   A rank calls it with phases = 3; the loopback test runs bit 1 for every context, then bit 2 (no
- *   kernel waits on one launched after it on the same device).  Grecv: reduce_count doubles.
- * Errors: EINVAL (not SHARD_BLOCKS, not imported, null pointers), ENOMEM, ECUDA.                   */
+ *   release of this rank's flag in every owner; bit 2 = wait for every source's flag, the sum, then an
+ *   acknowledgement to every source.  From its second call on, bit 1 first waits for every owner's
+ *   acknowledgement of the previous call, so a fast rank never overwrites a slot its owner is still
+ *   summing.  A rank calls it with phases = 3; the loopback test runs bit 1 for every context, then
+ *   bit 2 (no kernel waits on one launched after it on the same device).  Grecv: reduce_count doubles.
+ *   A wait that is not satisfied within 60 s traps (the call's stream then reports a CUDA error)
+ *   instead of hanging on a peer that died.
+ * Errors: EINVAL (not SHARD_BLOCKS, more than 32 ranks, not imported, null pointers), ENOMEM, ECUDA. */
 polya_status polya_p2p_export(polya_ctx* ctx, char handle_out[64]);
 polya_status polya_p2p_import(polya_ctx* ctx, const char* handles);
 polya_status polya_p2p_loopback(polya_ctx** ctxs, int32_t nranks);

@@ -182,12 +182,20 @@ polya_status p2p_tables(Ctx& c, const std::vector<double*>& base) {
     p2p_place(c, c.local_pairs[pl], t, &o, &q);
     tp[pl] = base[o] + (c.cfg.rank * own + q) * NN;
   }
-  std::vector<int*> fp(N);
-  for (int64_t o = 0; o < N; ++o) fp[o] = reinterpret_cast<int*>(base[o] + N * own * NN) + c.cfg.rank;
+  // ready: owner o's flag for this rank (the slot is written); ack: source o's flag for this rank (this
+  // rank, as owner, has summed o's slot, which o may then overwrite)
+  std::vector<int*> fp(N), ap(N);
+  for (int64_t o = 0; o < N; ++o) {
+    fp[o] = reinterpret_cast<int*>(base[o] + N * own * NN) + c.cfg.rank;
+    ap[o] = reinterpret_cast<int*>(base[o] + N * own * NN) + kP2pAck + c.cfg.rank;
+  }
+  if (tp.empty()) tp.push_back(nullptr);
   if (cudaMalloc(&c.d_tile_ptr, tp.size() * sizeof(double*)) != cudaSuccess ||
       cudaMalloc(&c.d_flag_ptr, fp.size() * sizeof(int*)) != cudaSuccess ||
+      cudaMalloc(&c.d_ack_ptr, ap.size() * sizeof(int*)) != cudaSuccess ||
       cudaMemcpy(c.d_tile_ptr, tp.data(), tp.size() * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(c.d_flag_ptr, fp.data(), fp.size() * sizeof(int*), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaMemcpy(c.d_flag_ptr, fp.data(), fp.size() * sizeof(int*), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c.d_ack_ptr, ap.data(), ap.size() * sizeof(int*), cudaMemcpyHostToDevice) != cudaSuccess) {
     c.last_error = "polya_p2p: destination tables";
     return POLYA_ENOMEM;
   }
@@ -199,8 +207,8 @@ polya_status p2p_tables(Ctx& c, const std::vector<double*>& base) {
 extern "C" polya_status polya_p2p_export(polya_ctx* ctx, char handle_out[64]) {
   if (!ctx) return POLYA_EINVAL;
   Ctx& c = ctx->c;
-  if (c.cfg.shard != POLYA_SHARD_BLOCKS) {
-    c.last_error = "polya_p2p_export needs SHARD_BLOCKS";
+  if (c.cfg.shard != POLYA_SHARD_BLOCKS || c.cfg.nranks > kP2pAck) {
+    c.last_error = "polya_p2p_export needs SHARD_BLOCKS and at most 32 ranks";
     return POLYA_EINVAL;
   }
   if (!c.p2p_buf) {
@@ -278,22 +286,33 @@ extern "C" polya_status polya_schur_reduce_p2p(polya_ctx* ctx, const double* X, 
   }
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t NN = c.Ntil * c.Ntil, N = c.cfg.nranks;
+  const int* flags = reinterpret_cast<const int*>(c.p2p_buf + N * c.p2p_own * NN);
   if (phases & 1) {   // assemble into the owners' slots, then signal every owner
     polya_status st = polya_schur_prepare(ctx, X, Zinv, stream);
     if (st != POLYA_OK) return st;
-    ++c.p2p_epoch;
-    cudaError_t e = launch_schur(c, nullptr, POLYA_G_PAIR_TILES, c.item0, c.item1, s, c.d_tile_ptr);
+    const int prev = c.p2p_epoch++;
+    cudaError_t e = cudaSuccess;
+    // the owners have summed the previous epoch's slots (their acks): only then overwrite them
+    if (prev > 0) {
+      e = launch_p2p_wait(flags + kP2pAck, (int)N, prev, s);
+      ++c.launches;
+    }
+    if (e == cudaSuccess) e = launch_schur(c, nullptr, POLYA_G_PAIR_TILES, c.item0, c.item1, s, c.d_tile_ptr);
     if (e == cudaSuccess && c.timing) e = cudaEventRecord(c.ev[2], s);
-    if (e == cudaSuccess) e = launch_p2p_signal(c.d_flag_ptr, (int)N, c.p2p_epoch, s);
+    if (e == cudaSuccess) {
+      e = launch_p2p_signal(c.d_flag_ptr, (int)N, c.p2p_epoch, s);
+      ++c.launches;
+    }
     if (e != cudaSuccess) {
       c.last_error = std::string("polya_schur_reduce_p2p: ") + cudaGetErrorString(e);
       return POLYA_ECUDA;
     }
   }
-  if (phases & 2) {   // wait for every source's signal, sum the slots in rank order
-    const int* flags = reinterpret_cast<const int*>(c.p2p_buf + N * c.p2p_own * NN);
+  if (phases & 2) {   // wait for every source's signal, sum the slots in rank order, acknowledge
     cudaError_t e = launch_p2p_wait(flags, (int)N, c.p2p_epoch, s);
     if (e == cudaSuccess) e = launch_p2p_sum(c.p2p_buf, (int)N, c.p2p_own * NN, Grecv, s);
+    if (e == cudaSuccess) e = launch_p2p_signal(c.d_ack_ptr, (int)N, c.p2p_epoch, s);
+    c.launches += 3;
     if (e == cudaSuccess && c.timing) e = cudaEventRecord(c.ev[3], s);
     if (e != cudaSuccess) {
       c.last_error = std::string("polya_schur_reduce_p2p: ") + cudaGetErrorString(e);
@@ -307,8 +326,11 @@ namespace polya {
 void combine_free(Ctx& c) {
   if (c.d_tile_ptr) cudaFree(c.d_tile_ptr);
   if (c.d_flag_ptr) cudaFree(c.d_flag_ptr);
+  if (c.d_ack_ptr) cudaFree(c.d_ack_ptr);
   c.d_tile_ptr = nullptr;
   c.d_flag_ptr = nullptr;
+  c.d_ack_ptr = nullptr;
+  c.p2p_epoch = 0;
   for (void* p : c.p2p_opened) cudaIpcCloseMemHandle(p);
   c.p2p_opened.clear();
   if (c.p2p_buf) cudaFree(c.p2p_buf);

@@ -495,12 +495,22 @@ __global__ void k_p2p_signal(int* const* flags, int n, int epoch) {
     asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(flags[r]), "r"(epoch) : "memory");
   }
 }
+// Spins until every flag reaches the epoch; a peer that never signals (it died, or a caller skipped a
+// phase) ends in a trap after kP2pTimeoutNs instead of a hang: the launch then fails with a CUDA error.
+constexpr unsigned long long kP2pTimeoutNs = 60ull * 1000000000ull;
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __global__ void k_p2p_wait(const int* flags, int n, int epoch) {
+  const unsigned long long t0 = globaltimer();
   for (int r = 0; r < n; ++r)
     for (;;) {
       int v;
       asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(flags + r) : "memory");
       if (v >= epoch) break;
+      if (globaltimer() - t0 > kP2pTimeoutNs) __trap();
       __nanosleep(256);
     }
 }

@@ -148,12 +148,14 @@ struct Ctx {
   // a dedicated comm stream, slot events (allocated on first use)
   double* comb_slot[2] = {nullptr, nullptr};
   int64_t comb_t = 0;                  // polya_set_combine_tiles (0: automatic, ~2 GiB groups)
-  // fused P2P combine (polya_p2p_*): this rank's receive slots [nranks][own tiles] + nranks flags, the
-  // per-pair destination table (a slot in the owner's buffer), the owners' flag addresses for this rank
+  // fused P2P combine (polya_p2p_*): this rank's receive slots [nranks][own tiles] + a flag block
+  // (ready[r] at int 0.., ack[o] at int kP2pAck..), the per-pair destination table (a slot in the
+  // owner's buffer), the owners' ready-flag addresses for this rank, the sources' ack-flag addresses
   double* p2p_buf = nullptr;
   int64_t p2p_own = 0;                 // tiles each rank owns (groups x combine_tiles, padding included)
   double** d_tile_ptr = nullptr;
   int** d_flag_ptr = nullptr;
+  int** d_ack_ptr = nullptr;
   std::vector<void*> p2p_opened;       // peers' buffers opened by IPC (closed at destroy)
   int p2p_epoch = 0;
   bool p2p_ready = false;
@@ -192,6 +194,7 @@ cudaError_t launch_adjoint_reduce(Ctx& c, double* y, cudaStream_t s);
 cudaError_t launch_schur(Ctx& c, double* G, int layout, int64_t item0, int64_t item1, cudaStream_t s,
                          double* const* tile_ptr = nullptr);
 // the P2P combine (kernels.cu): signal the owners, wait for every source, sum the slots in rank order
+constexpr int kP2pAck = 32;           // ints: the flag block holds ready[<= 32] then ack[<= 32]
 cudaError_t launch_p2p_signal(int* const* flag_ptrs, int n, int epoch, cudaStream_t s);
 cudaError_t launch_p2p_wait(const int* flags, int n, int epoch, cudaStream_t s);
 cudaError_t launch_p2p_sum(const double* slots, int n, int64_t count, double* out, cudaStream_t s);
