@@ -263,6 +263,37 @@ def test_schur_large_rows_entries_probes(pb, cfg_id, layout, nrows, npool, nent)
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("n", [125, 128, 130])
+def test_schur_precompute_size_boundary(pb, n):
+    """The SCM precompute switches kernels at np = 128 (K3b row-gathered GEMMs up to it, K3 batched GEMMs
+    beyond): n = 125 (np = 128, ragged tail of 5), 128 (np = 128, no tail), 130 (np = 136) -- whole
+    stratified rows, stratified entries and 2 probes of G against the literal Eq. T2."""
+    cfg = synth.small_config(n, 2, 1, 1, 1)
+    ctx, A, X, W = _setup(pb, cfg)
+    G = ctx.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES)
+    torch.cuda.synchronize()
+    P = osdp.build_problem(A, cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2)
+    rng = np.random.default_rng(5)
+    rows = _strat_indices(P, rng, 8)
+    ref = osdp.schur_rows(P, X, W, rows)
+    for r, i in enumerate(rows):
+        assert _rel(_tiles_row(G, i, P.L0, P.Ntil).cpu().numpy(), ref[r]) <= TOL, i
+    pool = sorted(set(_strat_indices(P, rng, 32)))
+    pairs = _sample_pairs(P, rng, 128, pool)
+    dref = dict(zip(pool, osdp.schur_entries(P, X, W, [(i, i) for i in pool])))
+    for (i, j), r in zip(pairs, osdp.schur_entries(P, X, W, pairs)):
+        got = _tiles_entry(G, i, j, P.L0, P.Ntil)
+        assert abs(got - r) <= TOL * np.sqrt(dref[i] * dref[j]), (i, j, got, r)
+    V = rng.normal(size=(2, P.K))
+    gv_ref = osdp.schur_probe(P, X, W, V)
+    for p in range(2):
+        gv = _tiles_matvec(G, _dev(V[p]), P.L0, P.Ntil).cpu().numpy()
+        assert _rel(gv, gv_ref[p]) <= TOL, p
+    del G
+    ctx.close()
+    torch.cuda.empty_cache()
+
+
 def test_schur_more_ranks_than_items(pb):
     """Config 1 has 3 work items; with 8 ranks most shares are empty (allowed): those ranks
     write nothing, polya_schur returns OK, and the union is still G bit for bit."""
