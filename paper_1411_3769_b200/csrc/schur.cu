@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
   __shared__ int s_nrc[2][2];                  // their counts (double-buffered by item parity)
   __shared__ uint64_t s_pbar;                  // consumer phase barrier (NCW arrivals per phase)
   __shared__ SlotInfo s_info[NSTAGE];      // item of the stage held by each ring slot (first stages)
+  __shared__ SlotInfo s_cur[NCW];          // each consumer warp's current item
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < 64) {  // diagonal order: consecutive entries have consecutive svec indices
@@ -510,7 +511,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
       const uint32_t slot = cnt % NSTAGE, ph = (cnt / NSTAGE) & 1;
       mbar_wait(full + slot, ph);
     }
-    const SlotInfo it = s_info[cnt % NSTAGE];
+    // the item's descriptor stays in shared memory (a per-warp copy: the ring slot's s_info may be
+    // rewritten for a later item while this one is still folding / writing), read where it is used,
+    // so that it holds no registers across the DMMA loops
+    if (lane == 0) s_cur[warp] = s_info[cnt % NSTAGE];
+    __syncwarp();
+    const volatile SlotInfo& it = s_cur[warp];
     if (it.item >= p.item1) {
       if (p.tile_ptr) __threadfence_system();   // P2P combine: the stores to peer memory before the signal
       break;
