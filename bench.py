@@ -63,6 +63,14 @@ def fp64_peak():
         return 148 * 64 * 2 * 1.965e9 / 1e12, "nominal 148 SM x 64 FP64 FMA/clk x 1.965 GHz"
 
 
+def hbm_peak():
+    """MEASURED_PEAKS.json's copy bandwidth (GB/s), else the profiling guide's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -430,6 +438,35 @@ def run_gpu(args, cfg, cid):
                                 "copies all of G back)"}
         del Gh, Gres, Bh, yvh
 
+    # ---- the per-iteration operators alone (HBM-bound for small n, FP64-bound for large):
+    # algorithmic FLOPs (2 n^3 per nonzero H_{h,m} product, 2 n^2 per beta term) and compulsory HBM bytes
+    # (inputs read once, outputs written once), each call timed with CUDA events after an L2 flush
+    operators = None
+    if flush is not None:
+        d = ctx.dims
+        n_ = cfg.n
+        ops = {"apply": (lambda: ctx.apply(y), 2 * n_ ** 3 * d["nnz_H"] + 2 * n_ * n_ * d["nnz_beta"],
+                         8 * (K + d["nnz_H"] * n_ * n_ + ctx.nblocks * n_ * n_)),
+               "adjoint": (lambda: ctx.adjoint(Xd), 2 * n_ ** 3 * d["nnz_H"] + 2 * N * (d["nnz_H"] + d["nnz_beta"]),
+                           8 * (ctx.nblocks * n_ * n_ + d["nnz_H"] * n_ * n_ + K))}
+        operators = {"peaks": {"fp64_tflops": fp64_peak()[0], "hbm_gbs": hbm_peak()[0], "hbm_source": hbm_peak()[1]}}
+        FP64_PEAK, HBM_PEAK = fp64_peak()[0], hbm_peak()[0]
+        for name, (fn, flops, nbytes) in ops.items():
+            ts = []
+            for _ in range(5):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            t = max_over_ranks(statistics.median(ts))
+            operators[name] = {"ms": t, "tflops": flops / (t * 1e-3) / 1e12, "gbs": nbytes / (t * 1e-3) / 1e9,
+                               "frac_fp64": flops / (t * 1e-3) / 1e12 / FP64_PEAK, "frac_hbm": nbytes / (t * 1e-3) / 1e9 / HBM_PEAK,
+                               "algorithmic_flops": flops, "compulsory_bytes": nbytes}
+
     # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step) at every N: one rank uses the
     # dense (or, for config 5, tiled) factorisation; N > 1 ranks factor G distributed (SHARD_CYCLIC:
     # column-cyclic pair tiles, NCCL panel broadcasts) ----
@@ -547,6 +584,7 @@ def run_gpu(args, cfg, cid):
             "gpu_launches_per_step": launches_per_step,
             "clocks": clocks,
             "ipm_iteration": ipm,
+            "operators": operators,
         }
         print(json.dumps(line), flush=True)
     barrier()

@@ -453,14 +453,17 @@ cudaError_t launch_gemm(Ctx& c, const GemmItem* items, const GemmTerm* terms, in
 cudaError_t launch_rgemm(Ctx& c, int phase, cudaStream_t s) {
   const int64_t nt = c.n_rg_tile[phase];
   if (nt == 0) return cudaSuccess;
-  // transB is uniform per launch: phase 0 (U, V) multiplies by X, W; phase 1 (Q, R) by H^T
-  cudaError_t e = cudaFuncSetAttribute(phase ? k_rgemm<true> : k_rgemm<false>,
+  // transB is uniform per launch: phases 0 (U, V) and 2 (T) multiply by X, W; phase 1 (Q, R) by H^T
+  const bool trans = phase == 1;
+  cudaError_t e = cudaFuncSetAttribute(trans ? k_rgemm<true> : k_rgemm<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRgSmem);
   if (e != cudaSuccess) return e;
-  if (phase)
-    k_rgemm<true><<<(unsigned)nt, 256, kRgSmem, s>>>(c.arena, c.mstride, (int)c.np, c.d_rg_grp[1], c.d_rg_ent[1], c.d_rg_tile[1]);
+  if (trans)
+    k_rgemm<true><<<(unsigned)nt, 256, kRgSmem, s>>>(c.arena, c.mstride, (int)c.np, c.d_rg_grp[phase], c.d_rg_ent[phase],
+                                                      c.d_rg_tile[phase]);
   else
-    k_rgemm<false><<<(unsigned)nt, 256, kRgSmem, s>>>(c.arena, c.mstride, (int)c.np, c.d_rg_grp[0], c.d_rg_ent[0], c.d_rg_tile[0]);
+    k_rgemm<false><<<(unsigned)nt, 256, kRgSmem, s>>>(c.arena, c.mstride, (int)c.np, c.d_rg_grp[phase], c.d_rg_ent[phase],
+                                                       c.d_rg_tile[phase]);
   ++c.launches;
   return cudaGetLastError();
 }

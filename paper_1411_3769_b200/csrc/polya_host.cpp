@@ -596,6 +596,19 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
     c.n_items_T = (int64_t)it.size();
     c.d_items_T = dupload(it);
     c.d_terms_T = dupload(tm);
+    if (c.rg) {   // K3b groups of the adjoint: the T_t of one block m share sym(X_m)
+      std::vector<std::vector<int32_t>> per_m((size_t)c.M);
+      for (int64_t t = 0; t < nnzH; ++t) per_m[(size_t)c.Hm[t]].push_back((int32_t)t);
+      std::vector<RgGroup> grp;
+      std::vector<RgEnt> ent;
+      for (int64_t m = 0; m < c.M; ++m) {
+        if (per_m[(size_t)m].empty()) continue;
+        const int32_t e0 = (int32_t)ent.size();
+        for (int32_t t : per_m[(size_t)m]) ent.push_back({(int32_t)(c.id_H + t), (int32_t)(c.id_T + t), -1, 0});
+        grp.push_back({(int32_t)(c.id_Xt + c.L + m), 0, e0, (int32_t)ent.size()});
+      }
+      rg_upload(c, 2, grp, ent);
+    }
     // apply: S_m = sum_h V_h(y) H_{h,m}; generalised S_m = sum_t A_t (V_h(y) B_t) (two passes)
     it.clear(); tm.clear();
     if (c.gen) {
@@ -825,7 +838,7 @@ void build(Ctx& c, const double* A_host, bool device = true, const GenInput* gi 
 }
 
 void free_ctx(Ctx& c) {
-  for (int ph = 0; ph < 2; ++ph) {
+  for (int ph = 0; ph < Ctx::kRgPhases; ++ph) {
     if (c.d_rg_grp[ph]) cudaFree(c.d_rg_grp[ph]);
     if (c.d_rg_ent[ph]) cudaFree(c.d_rg_ent[ph]);
     if (c.d_rg_tile[ph]) cudaFree(c.d_rg_tile[ph]);
@@ -1108,7 +1121,10 @@ extern "C" polya_status polya_adjoint(polya_ctx* ctx, const double* X, double* y
   try {
     CU(launch_pad_copy(c, X, c.id_Xt, c.nb, 1, s));
     CU(launch_gemm(c, c.d_items_T0, c.d_terms_T0, c.n_items_T0, s));   // generalised form only
-    CU(launch_gemm(c, c.d_items_T, c.d_terms_T, c.n_items_T, s));
+    if (c.rg)
+      CU(launch_rgemm(c, 2, s));
+    else
+      CU(launch_gemm(c, c.d_items_T, c.d_terms_T, c.n_items_T, s));
     CU(launch_adjoint_reduce(c, y, s));
   } catch (const Fail& f) {
     return fail(ctx, f);

@@ -118,9 +118,11 @@ struct Ctx {
   // batched gemm descriptors
   GemmItem* d_items_UV = nullptr; GemmTerm* d_terms_UV = nullptr; int64_t n_items_UV = 0;
   GemmItem* d_items_QR = nullptr; GemmTerm* d_terms_QR = nullptr; int64_t n_items_QR = 0;
-  // K3b row-gathered form of the same two launches (standard form, np <= 128): [0] U, V (+ U^T, V^T), [1] Q, R
-  RgGroup* d_rg_grp[2] = {nullptr, nullptr}; RgEnt* d_rg_ent[2] = {nullptr, nullptr};
-  RgTile* d_rg_tile[2] = {nullptr, nullptr}; int64_t n_rg_tile[2] = {0, 0};
+  // K3b row-gathered launches (standard form, np <= 128): [0] U, V (+ U^T, V^T), [1] Q, R (op(B) = H^T),
+  // [2] the adjoint's T_t = H_t sym(X_m)
+  static constexpr int kRgPhases = 3;
+  RgGroup* d_rg_grp[kRgPhases] = {}; RgEnt* d_rg_ent[kRgPhases] = {};
+  RgTile* d_rg_tile[kRgPhases] = {}; int64_t n_rg_tile[kRgPhases] = {};
   bool rg = false;
   GemmItem* d_items_T = nullptr; GemmTerm* d_terms_T = nullptr; int64_t n_items_T = 0;
   GemmItem* d_items_S = nullptr; GemmTerm* d_terms_S = nullptr; int64_t n_items_S = 0;
