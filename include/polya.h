@@ -211,7 +211,8 @@ polya_status polya_schur(polya_ctx* ctx, const double* X_dev, const double* Zinv
                          double* G_dev, int layout, void* stream);
 
 /* The two halves of polya_schur, for callers that stream G out while it is assembled:
- * polya_schur_prepare pads X, Z^{-1} and runs the SCM precompute of this rank (U, V, Q, R; kernel K3);
+ * polya_schur_prepare pads X, Z^{-1} and runs the SCM precompute of this rank (U, V, Q, R; kernels K3 / K3b:
+ *   U^T, V^T are stored as transposes, which relies on the symmetry of X and Z^{-1});
  * polya_schur_assemble then assembles this rank's local pairs [pair_begin, pair_end), 0-based among
  * its npairs_local local pairs (polya_dims; = pair0 .. pair1-1 except with SHARD_CYCLIC, whose local
  * pairs are the pair rows h = rank mod nranks); G_dev is the same buffer / layout as for polya_schur
