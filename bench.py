@@ -289,15 +289,24 @@ def run_gpu(args, cfg, cid):
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # 256 MiB > 126 MB L2
     ctx.set_timing(True)
 
+    # B^T(y) and B(X) do not depend on G and share no workspace with the Schur assembly (separate arena
+    # slots): they run on a side stream next to the precompute/assembly and join before the step ends
+    side = torch.cuda.Stream(device=dev)
+    Bt_buf = torch.empty((ctx.nblocks, ctx.bn, ctx.bn), dtype=torch.float64, device=dev)
+    yv_buf = torch.empty(K, dtype=torch.float64, device=dev)
+
     def step():
-        Bt = ctx.apply(y)
-        yv = ctx.adjoint(Xd)
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        Bt = ctx.apply(y, out=Bt_buf, stream=side)
+        yv = ctx.adjoint(Xd, out=yv_buf, stream=side)
         if p2p:      # fused: the assembly writes each partial tile into its owner's slot, owners sum
             ctx.schur_reduce_p2p(Xd, Wd, out=Grecv)
         elif blocks:   # pipelined: each tile group's ReduceScatter overlaps the next group's assembly
             ctx.schur_reduce(Xd, Wd, out=Grecv)
         else:
             ctx.schur(Xd, Wd, G=G, layout=pb.G_PAIR_TILES)
+        cur.wait_stream(side)
         return Bt, yv
 
     for _ in range(args.warmup):
@@ -467,11 +476,77 @@ def run_gpu(args, cfg, cid):
                                "frac_fp64": flops / (t * 1e-3) / 1e12 / FP64_PEAK, "frac_hbm": nbytes / (t * 1e-3) / 1e9 / HBM_PEAK,
                                "algorithmic_flops": flops, "compulsory_bytes": nbytes}
 
+    def make_line(ipm, cpu):
+        peak, peak_src = fp64_peak()
+        achieved = wg_rank / (t_asm_rank * 1e-3) / 1e12
+        traffic = None
+        try:
+            nc = json.load(open(NCU_FILE))
+            if nc.get("config") == cid:
+                traffic = nc.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        return {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded synth/ generators; SURVEY 8(d))",
+            "config": {"workload": workload_name(cfg, cid), "K": K, "nblocks": ctx.nblocks, "L0": ctx.L0,
+                       "W_G": wg_one, "W_G_sum_over_ranks": wg_total,
+                       "step": "polya_apply + polya_adjoint (side stream) + " + (
+                           "polya_schur_reduce_p2p (precompute + assembly storing each partial tile into its "
+                           "owner's slot over peer memory + the owners' ordered sums)" if p2p else
+                           "polya_schur_reduce (precompute + assembly by tile groups, each group's NCCL "
+                           "ReduceScatter on a comm stream overlapping the next group)" if blocks else
+                           "polya_schur (precompute + assembly)"),
+                       "layout": "G pair tiles (upper, row-panel ready)",
+                       "cuda_graph": bool(args.graph),
+                       "parallelism": (f"Polya-block shards x{world} + NCCL ReduceScatter of partial G" if blocks
+                                       else f"column-cyclic pair-tile shards x{world} (distributed factorisation)"
+                                       if cyclic else f"output-tile shards x{world}"),
+                       "l2": "256 MiB memset between timed steps (outside the events); G write alone is "
+                             f"{npl * N * N * 8 / 1e9:.1f} GB/step"},
+            "breakdown_ms": {"schur_precompute": t_pre, "schur_assembly": t_asm,
+                             "combine_nccl_exposed": t_comb,
+                             "apply_adjoint_and_rest": t_step - t_pre - t_asm - t_comb, "setup_once_s": setup_s},
+            "tflops_schur_assembly_only": wg_total / (t_asm * 1e-3) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": "k_schur (K4, FP64 DMMA)", "achieved": achieved, "peak": peak,
+                         "unit": UNIT, "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_flops_per_launch": wg_rank, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            # e2e: the public calls of one Algorithm 2 iteration's operator work as the IPM makes them --
+            # host inputs in, the step's host-side results out, G consumed on the device by the
+            # factorisation; e2e_full_G: all of G back to the host as well (PCIe-bound)
+            "e2e": e2e_resident,
+            "e2e_full_G": e2e,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "gpu_launches_per_step": launches_per_step,
+            "clocks": clocks,
+            "ipm_iteration": ipm,
+            "operators": operators,
+        }
+
     # ---- seconds per IPM iteration (Algorithm 2 step via polya_ipm_step) at every N: one rank uses the
     # dense (or, for config 5, tiled) factorisation; N > 1 ranks factor G distributed (SHARD_CYCLIC:
     # column-cyclic pair tiles, NCCL panel broadcasts) ----
     ipm = None
+    watchdog = None
     if not args.no_ipm:
+        # The N > 1 IPM leg runs the library's own NCCL communicator (panel broadcasts of the distributed
+        # factorisation).  A hang there must not cost the Schur line measured above: after --ipm-timeout
+        # seconds every rank gives up on its own clock, rank 0 prints the line with the IPM leg marked as
+        # timed out, and all ranks exit.
+        import threading
+
+        def ipm_timed_out():
+            if rank == 0:
+                print(json.dumps(make_line({"error": f"IPM leg timed out after {args.ipm_timeout:.0f} s "
+                                                     f"({world} rank(s))", "n_ranks": world}, None)), flush=True)
+            sys.stderr.flush()
+            os._exit(0)
+
+        watchdog = threading.Timer(args.ipm_timeout, ipm_timed_out)
+        watchdog.daemon = True
+        watchdog.start()
         del G
         flush = None
         if blocks:
@@ -512,8 +587,13 @@ def run_gpu(args, cfg, cid):
                                  "dtrsm/dsyrk/dgemm) + blocked solves" if tiled else
                                  "cuSOLVER dpotrf + 2 dpotrs on the K x K SCM (FULL)"),
                "iteration_measured": 2, "gap": st["gap"], "tp": st["tp"], "td": st["td"]}
+        # the factorisation against the FP64 roofline: K^3/3 flops of the Cholesky of the K x K SCM
+        fl_chol = float(ictx.K) ** 3 / 3.0
+        ipm["factorisation_tflops"] = fl_chol / (ipm["ms_factorisation"] * 1e-3) / 1e12
+        ipm["factorisation_frac_fp64"] = ipm["factorisation_tflops"] / (fp64_peak()[0] * world)
         if ictx is not ctx:
             ictx.close()
+        watchdog.cancel()
 
     # ---- CPU oracle baseline (rank 0, N=1 only) ----
     cpu = None
@@ -538,55 +618,8 @@ def run_gpu(args, cfg, cid):
                "literal_entries_tflops": per_entry * ent / t_lit / 1e12,
                "literal_sample": f"{ent} literal G entries (Eq. T2, oracle.sdp.schur_entries) in {t_lit:.1f} s"}
 
-    peak, peak_src = fp64_peak()
-    achieved = wg_rank / (t_asm_rank * 1e-3) / 1e12
-    traffic = None
-    try:
-        nc = json.load(open(NCU_FILE))
-        if nc.get("config") == cid:
-            traffic = nc.get("dram_bytes_per_launch")
-    except Exception:
-        pass
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded synth/ generators; SURVEY 8(d))",
-            "config": {"workload": workload_name(cfg, cid), "K": K, "nblocks": ctx.nblocks, "L0": ctx.L0,
-                       "W_G": wg_one, "W_G_sum_over_ranks": wg_total,
-                       "step": "polya_apply + polya_adjoint + " + (
-                           "polya_schur_reduce_p2p (precompute + assembly storing each partial tile into its "
-                           "owner's slot over peer memory + the owners' ordered sums)" if p2p else
-                           "polya_schur_reduce (precompute + assembly by tile groups, each group's NCCL "
-                           "ReduceScatter on a comm stream overlapping the next group)" if blocks else
-                           "polya_schur (precompute + assembly)"),
-                       "layout": "G pair tiles (upper, row-panel ready)",
-                       "cuda_graph": bool(args.graph),
-                       "parallelism": (f"Polya-block shards x{world} + NCCL ReduceScatter of partial G" if blocks
-                                       else f"column-cyclic pair-tile shards x{world} (distributed factorisation)"
-                                       if cyclic else f"output-tile shards x{world}"),
-                       "l2": "256 MiB memset between timed steps (outside the events); G write alone is "
-                             f"{npl * N * N * 8 / 1e9:.1f} GB/step"},
-            "breakdown_ms": {"schur_precompute": t_pre, "schur_assembly": t_asm,
-                             "combine_nccl_exposed": t_comb,
-                             "apply_adjoint_and_rest": t_step - t_pre - t_asm - t_comb, "setup_once_s": setup_s},
-            "tflops_schur_assembly_only": wg_total / (t_asm * 1e-3) / 1e12,
-            "roofline": {"bound": "tensor", "kernel": "k_schur (K4, FP64 DMMA)", "achieved": achieved, "peak": peak,
-                         "unit": UNIT, "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_flops_per_launch": wg_rank, "peak_source": peak_src},
-            "cpu_baseline": cpu,
-            # e2e: the public calls of one Algorithm 2 iteration's operator work as the IPM makes them --
-            # host inputs in, the step's host-side results out, G consumed on the device by the
-            # factorisation; e2e_full_G: all of G back to the host as well (PCIe-bound)
-            "e2e": e2e_resident,
-            "e2e_full_G": e2e,
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-            "gpu_launches_per_step": launches_per_step,
-            "clocks": clocks,
-            "ipm_iteration": ipm,
-            "operators": operators,
-        }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(make_line(ipm, cpu)), flush=True)
     barrier()
     ctx.close()
     if world > 1:
@@ -615,9 +648,13 @@ def main():
     ap.add_argument("--no-ipm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ipm-timeout", type=float, default=None,
+                    help="seconds before the IPM leg gives up (default 180; 1800 for config 5)")
     args = ap.parse_args()
     cid = int(args.config) if args.config.isdigit() else args.config
     cfg = synth.CONFIGS[cid]
+    if args.ipm_timeout is None:
+        args.ipm_timeout = 1800.0 if cid == 5 else 180.0
     if args.impl == "reference":
         return run_reference(args, cfg, cid)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:

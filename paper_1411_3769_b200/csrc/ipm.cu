@@ -145,53 +145,107 @@ __device__ bool smem_chol(double* S, int n) {
   return true;
 }
 
-// W_b = Z_b^{-1} via Cholesky Z = L L^T, X = L^{-1} in place (from X L = I, column by column from
-// the last: X_ij = -(sum_{k=j+1..i} X_ik L_kj) / L_jj), then W = X^T X; exactly symmetric.
-// Shared memory: n^2 + n doubles (n <= 168).
+// W_b = Z_b^{-1} via Cholesky Z = L L^T, X = L^{-1} in place, then W = X^T X (exactly symmetric).
+// One CTA per block, every phase right-looking with one barrier per column: the Cholesky (column k's
+// rank-1 update of the trailing triangle with the column scaled on the fly; the stored column is scaled
+// during the next column's update, which does not touch it), the inverse (L X = I by rows: the update
+// of step k also finishes row k+1 of X), and X^T X in 2x2 register blocks.  Rows in shared memory with
+// an odd stride (n | 1 doubles), so the column reads of a half-warp hit distinct banks.
+// Shared memory: n (n | 1) + 3n doubles (n <= 168).
 // linv != 0: W_b = L^{-1} instead (lower triangle, zeros above; a NaN in W_b[0] if Z_b is not positive
 // definite), the congruence factor of the step length (step_len).
-__global__ void k_block_inv(int n, const double* __restrict__ Z, double* __restrict__ W, int* __restrict__ fail,
-                            int linv = 0) {
+__global__ void __launch_bounds__(512, 2) k_block_inv(int n, const double* __restrict__ Z, double* __restrict__ W,
+                                                   int* __restrict__ fail, int linv = 0) {
   extern __shared__ double sm[];
-  double* S = sm;           // n*n: L, then X = L^{-1} (lower)
-  double* col = sm + n * n; // n: the column of X being formed
+  const int ld = n | 1, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  double* S = sm;                  // n x ld: Z, then L (lower), then X = L^{-1} (lower)
+  double* dinv = S + n * ld;       // 1 / L_kk
+  double* colb = dinv + n;         // two buffers of a column of L (the inverse's right-looking update)
   const int64_t nn = (int64_t)n * n, b = blockIdx.x;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S[e] = Z[b * nn + e];
+  for (int i = warp; i < n; i += nw)
+    for (int j = lane; j < n; j += 32) S[i * ld + j] = Z[b * nn + (int64_t)i * n + j];
   __syncthreads();
-  if (!smem_chol(S, n)) {
-    if (threadIdx.x == 0) {
-      if (fail) atomicExch(fail, 1);
-      if (linv) W[b * nn] = __longlong_as_double(0x7ff8000000000000LL);
+  // ---- Cholesky, lower: L_kk = sqrt(p_k), L_ik = S_ik / L_kk, S_ij -= L_ik L_jk (k < j <= i)
+  double rs_prev = 0.0, sq_prev = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double piv = S[k * ld + k];
+    if (!(piv > 0.0)) {   // every thread read the same pivot: a uniform exit
+      if (tid == 0) {
+        if (fail) atomicExch(fail, 1);
+        if (linv) W[b * nn] = __longlong_as_double(0x7ff8000000000000LL);
+      }
+      return;
     }
-    return;
-  }
-  for (int j = n - 1; j >= 0; --j) {
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
-      double acc = 0.0;
-      for (int k = j + 1; k <= i; ++k) acc += S[i * n + k] * S[k * n + j];   // X_ik (k > j) * L_kj
-      col[i] = -acc / S[j * n + j];
+    const double sq = sqrt(piv), rs = 1.0 / sq;
+    for (int i = k + 1 + warp; i < n; i += nw) {
+      const double lik = S[i * ld + k] * rs;
+      for (int j = k + 1 + lane; j <= i; j += 32) S[i * ld + j] -= lik * (S[j * ld + k] * rs);
     }
+    if (k > 0) {   // column k-1 (read only by step k-1's update) takes its final scaling
+      for (int i = k + tid; i < n; i += nt) S[i * ld + k - 1] *= rs_prev;
+      if (tid == 0) { S[(k - 1) * ld + k - 1] = sq_prev; dinv[k - 1] = rs_prev; }
+    }
+    rs_prev = rs;
+    sq_prev = sq;
     __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) S[i * n + j] = col[i];
-    if (threadIdx.x == 0) S[j * n + j] = 1.0 / S[j * n + j];
+  }
+  if (tid == 0) { S[(n - 1) * ld + n - 1] = sq_prev; dinv[n - 1] = rs_prev; }
+  // ---- X = L^{-1}, lower, by rows: X_kj = B_kj / L_kk with B = I - sum_{m<k} L_km X_mj accumulated
+  // right-looking in the storage of L's consumed columns (position (r, j), j <= k < r, holds B_rj)
+  if (tid == 0) S[0] = dinv[0];
+  for (int r = 1 + tid; r < n; r += nt) colb[r] = S[r * ld];       // column 0 of L
+  __syncthreads();
+  for (int k = 0; k + 1 < n; ++k) {
+    const double* cur = colb + (k & 1) * n;
+    double* nxt = colb + ((k + 1) & 1) * n;
+    const int w = k + 1, cnt = (n - k - 1) * w;
+    const double dn = dinv[k + 1];
+    for (int e = tid; e < cnt; e += nt) {
+      const int q = e / w, j = e - q * w, r = k + 1 + q;
+      double v = (j == k ? 0.0 : S[r * ld + j]) - cur[r] * S[k * ld + j];
+      if (r == k + 1) v *= dn;   // row k+1 of X is final after this update
+      S[r * ld + j] = v;
+    }
+    for (int r = k + 2 + tid; r < n; r += nt) nxt[r] = S[r * ld + k + 1];   // column k+1 of L (untouched here)
+    if (tid == 0) S[(k + 1) * ld + k + 1] = dn;
     __syncthreads();
   }
   if (linv) {
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e / n, j = e - i * n;
-      W[b * nn + e] = j <= i ? S[e] : 0.0;
-    }
+    for (int i = warp; i < n; i += nw)
+      for (int j = lane; j < n; j += 32) W[b * nn + (int64_t)i * n + j] = j <= i ? S[i * ld + j] : 0.0;
     return;
   }
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e - i * n;
-    if (i > j) continue;
-    double s = 0.0;
-    for (int k = j; k < n; ++k) s += S[k * n + i] * S[k * n + j];  // (X^T X)_{ij}, k >= max(i,j)
-    W[b * nn + (int64_t)i * n + j] = s;
-    W[b * nn + (int64_t)j * n + i] = s;
+  for (int i = warp; i < n; i += nw)   // the strict upper triangle of X is zero
+    for (int j = i + 1 + lane; j < n; j += 32) S[i * ld + j] = 0.0;
+  __syncthreads();
+  // ---- W = X^T X: W_ij = sum_{m >= max(i,j)} X_mi X_mj, 2x2 blocks (I <= J) of (i, j) = (2I.., 2J..)
+  const int h = (n + 1) >> 1, nblk = h * (h + 1) / 2;
+  for (int e = tid; e < nblk; e += nt) {
+    int J = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);   // e = J (J + 1) / 2 + I, I <= J
+    while (J * (J + 1) / 2 > e) --J;
+    while ((J + 1) * (J + 2) / 2 <= e) ++J;
+    const int I = e - J * (J + 1) / 2;
+    const int i0 = 2 * I, i1 = i0 + 1, j0 = 2 * J, j1 = j0 + 1;
+    const bool vi = i1 < n, vj = j1 < n;
+    double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
+    for (int m = j0; m < n; ++m) {
+      const double* row = S + m * ld;
+      const double a0 = row[i0], a1 = vi ? row[i1] : 0.0, c0 = row[j0], c1 = vj ? row[j1] : 0.0;
+      w00 = fma(a0, c0, w00);
+      w01 = fma(a0, c1, w01);
+      w10 = fma(a1, c0, w10);
+      w11 = fma(a1, c1, w11);
+    }
+    double* Wb = W + b * nn;
+    Wb[(int64_t)i0 * n + j0] = w00;
+    Wb[(int64_t)j0 * n + i0] = w00;
+    if (vj) { Wb[(int64_t)i0 * n + j1] = w01; Wb[(int64_t)j1 * n + i0] = w01; }
+    if (vi) { Wb[(int64_t)i1 * n + j0] = w10; Wb[(int64_t)j0 * n + i1] = w10; }
+    if (vi && vj) { Wb[(int64_t)i1 * n + j1] = w11; Wb[(int64_t)j1 * n + i1] = w11; }
   }
 }
+
+size_t block_inv_smem(int64_t n) { return ((size_t)n * (size_t)(n | 1) + 3 * (size_t)n) * sizeof(double); }
 
 // Reading R5 as written: t_b = min(tcap, 1 / max(0, -lambda_min(M_b))), M_b = L_b^{-1} dS_b L_b^{-T}
 // (S_b = L_b L_b^T; M_b formed by k_block_inv(linv) + two k_bgemm).  One CTA per block: the symmetric
@@ -210,90 +264,124 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int q = 0; q < nw; ++q) s += red[q];
   return s;
 }
-__device__ __forceinline__ int sturm_count(int n, const double* d, const double* e, double lam) {
+// Number of eigenvalues of the symmetric tridiagonal T below lam (Sturm sequence of T - lam I); the
+// diagonal d_i = T[i * st], the off-diagonal e_i = T[i * st + 1] (the tridiagonal kept in place in the
+// reduced matrix: st = ld + 1).
+__device__ __forceinline__ int sturm_count(int n, const double* T, int st, double lam) {
   int cnt = 0;
-  double q = d[0] - lam;
+  double q = T[0] - lam;
   for (int i = 0;; ++i) {
     if (q == 0.0) q = -1e-300;
     cnt += q < 0.0;
     if (i + 1 == n) break;
-    q = (d[i + 1] - lam) - e[i] * e[i] / q;
+    const double ei = T[i * st + 1];
+    q = (T[(i + 1) * st] - lam) - ei * ei / q;
   }
   return cnt;
 }
-__global__ void __launch_bounds__(256) k_block_lmin(int n, const double* __restrict__ M, double tcap,
+// Shared-memory row stride of k_block_lmin: odd (conflict-free column reads) when it fits.
+__host__ __device__ inline int lmin_ld(int n) {
+  return ((int64_t)n * (n | 1) + 3 * n) * 8 + 512 <= 232448 ? (n | 1) : n;
+}
+size_t block_lmin_smem(int64_t n) { return ((size_t)n * lmin_ld((int)n) + 3 * (size_t)n) * sizeof(double); }
+
+__global__ void __launch_bounds__(512, 2) k_block_lmin(int n, const double* __restrict__ M, double tcap,
                                                     double* __restrict__ tout) {
   extern __shared__ double sm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double* P = sm;                           // packed lower: (i, j <= i) at i (i + 1) / 2 + j
-  double* v = P + (n * (n + 1)) / 2;
-  double* w = v + n;
-  double* d = w + n;
-  double* e = d + n;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int ld = lmin_ld(n);
+  double* A = sm;            // n x ld, full symmetric storage of sym(M_b)
+  double* p = A + n * ld;    // tau A v on the trailing block
+  double* vc = p + n;        // two buffers of the Householder vector
+  // the tridiagonal stays in place: d_k = A_kk (final after step k-1), e_k in A_{k,k+1} (the upper
+  // triangle of row k, dead once step k starts)
   __shared__ double red[32];
   __shared__ int s_j;
   const int64_t b = blockIdx.x, nn = (int64_t)n * n;
   const double* Mb = M + b * nn;
   int bad = 0;
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    const int i = idx / n, j = idx - i * n;
-    if (j > i) continue;
-    const double x = 0.5 * (Mb[(int64_t)i * n + j] + Mb[(int64_t)j * n + i]);
-    bad |= !isfinite(x);
-    P[i * (i + 1) / 2 + j] = x;
-  }
+  for (int i = warp; i < n; i += nw)
+    for (int j = lane; j < n; j += 32) {
+      const double x = 0.5 * (Mb[(int64_t)i * n + j] + Mb[(int64_t)j * n + i]);
+      bad |= !isfinite(x);
+      A[i * ld + j] = x;
+    }
   if (__syncthreads_or(bad)) {
     if (tid == 0) tout[b] = -1.0;   // S_b not positive definite: step_len falls back to k_block_tmax
     return;
   }
-  auto A = [&](int i, int j) -> double& { return i >= j ? P[i * (i + 1) / 2 + j] : P[j * (j + 1) / 2 + i]; };
+  // Householder (LAPACK dsytd2's reflections, A <- H A H, H = I - tau v v^T), two barriers per column.
+  // v is column k below the diagonal, in vc[k & 1] (written by the previous column's update, which
+  // finishes column k), with v_{k+1} = x_0 - e_k substituted where it is read.  The column norm and p^T v
+  // are reduced redundantly by every warp (shuffles).
+  for (int i = 1 + tid; i < n; i += nt) vc[i] = A[i * ld];
+  __syncthreads();
   for (int k = 0; k + 2 < n; ++k) {
-    // x = A[k+1.., k]; e_k = -sign(x_0) |x|; v = x - e_k e_1, tau = 2 / v^T v
+    const int k1 = k + 1;
+    double* v = vc + (k & 1) * n;
+    double* vn = vc + ((k + 1) & 1) * n;
     double xs = 0.0;
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) xs += A(i, k) * A(i, k);
-    const double a2 = block_sum(xs, red);
-    const double x0 = A(k + 1, k);
+    for (int i = k1 + lane; i < n; i += 32) xs = fma(v[i], v[i], xs);
+    for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+    const double a2 = xs, x0 = v[k1];
     const double alpha = sqrt(a2), ek = x0 >= 0.0 ? -alpha : alpha;
-    if (tid == 0) { d[k] = A(k, k); e[k] = ek; }
-    if (a2 == 0.0) continue;   // already reduced (uniform)
+    if (tid == 0) A[k * ld + k1] = ek;
+    if (a2 == 0.0) {   // already reduced (uniform): column k+1 for the next step
+      for (int i = k1 + 1 + tid; i < n; i += nt) vn[i] = A[i * ld + k1];
+      __syncthreads();
+      continue;
+    }
     const double v0 = x0 - ek, tau = 2.0 / (a2 - x0 * x0 + v0 * v0);
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) v[i] = i == k + 1 ? v0 : A(i, k);
-    __syncthreads();
-    // p = tau A v (rows k+1.., a warp per row), then w = p - (tau / 2)(p^T v) v
-    for (int i = k + 1 + warp; i < n; i += nw) {
-      double acc = 0.0;
-      for (int j = k + 1 + lane; j < n; j += 32) acc += A(i, j) * v[j];
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) w[i] = tau * acc;
+    // p_i = tau sum_j A_ij v_j (rows i > k, two threads per row: half-warps of 16 rows)
+    for (int base = k1 + warp * 16; base < n; base += nw * 16) {
+      const int i = base + (lane & 15), half = lane >> 4;
+      double a0 = 0.0, a1 = 0.0;
+      if (i < n) {
+        const double* Ai = A + i * ld;
+        if (half == 0) a0 = Ai[k1] * v0;
+        int j = k1 + 1 + half;
+        for (; j + 2 < n; j += 4) {
+          a0 = fma(Ai[j], v[j], a0);
+          a1 = fma(Ai[j + 2], v[j + 2], a1);
+        }
+        if (j < n) a0 = fma(Ai[j], v[j], a0);
+      }
+      double acc = a0 + a1;
+      acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+      if (i < n && half == 0) p[i] = tau * acc;
     }
     __syncthreads();
-    double pv = 0.0;
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) pv += w[i] * v[i];
-    const double K = 0.5 * tau * block_sum(pv, red);
-    for (int i = k + 1 + tid; i < n; i += blockDim.x) w[i] -= K * v[i];
-    __syncthreads();
-    // A <- A - v w^T - w v^T on the trailing lower triangle
-    for (int i = k + 1 + warp; i < n; i += nw)
-      for (int j = k + 1 + lane; j <= i; j += 32) P[i * (i + 1) / 2 + j] -= v[i] * w[j] + w[i] * v[j];
+    double pv = (lane == 0) ? p[k1] * v0 : 0.0;
+    for (int i = k1 + 1 + lane; i < n; i += 32) pv = fma(p[i], v[i], pv);
+    for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+    const double Kc = 0.5 * tau * pv;
+    // A <- A - v w^T - w v^T on the trailing block (both triangles, bitwise symmetric), w = p - K v;
+    // column k+1 of the result is the next step's v
+    for (int i = k1 + warp; i < n; i += nw) {
+      const double vi = i == k1 ? v0 : v[i], wi = p[i] - Kc * vi;
+      double* Ai = A + i * ld;
+      for (int j = k1 + lane; j < n; j += 32) {
+        const double vj = j == k1 ? v0 : v[j], wj = p[j] - Kc * vj;
+        const double r = Ai[j] - __dadd_rn(__dmul_rn(vi, wj), __dmul_rn(wi, vj));
+        Ai[j] = r;
+        if (j == k1 && i > k1) vn[i] = r;
+      }
+    }
     __syncthreads();
   }
-  if (tid == 0) {
-    if (n >= 2) { d[n - 2] = A(n - 2, n - 2); e[n - 2] = A(n - 1, n - 2); }
-    d[n - 1] = A(n - 1, n - 1);
-  }
-  __syncthreads();
+  __syncthreads();   // e_{n-2} = A_{n-2,n-1} (the symmetric copy of the last reflection's result)
   // lambda_min >= 0: no bound on t (tcap); else multisection on [Gershgorin lower bound, 0]
-  if (sturm_count(n, d, e, 0.0) == 0) {
+  const int st = ld + 1;
+  if (sturm_count(n, A, st, 0.0) == 0) {
     if (tid == 0) tout[b] = tcap;
     return;
   }
   double lo = 0.0;
   {
     double g = 1e300;
-    for (int i = tid; i < n; i += blockDim.x)
-      g = fmin(g, d[i] - (i > 0 ? fabs(e[i - 1]) : 0.0) - (i + 1 < n ? fabs(e[i]) : 0.0));
+    for (int i = tid; i < n; i += nt)
+      g = fmin(g, A[i * st] - (i > 0 ? fabs(A[(i - 1) * st + 1]) : 0.0) - (i + 1 < n ? fabs(A[i * st + 1]) : 0.0));
     for (int o = 16; o > 0; o >>= 1) g = fmin(g, __shfl_xor_sync(0xffffffffu, g, o));
-    __syncthreads();
     if (lane == 0) red[warp] = g;
     __syncthreads();
     for (int q = 0; q < nw; ++q) lo = fmin(lo, red[q]);
@@ -301,15 +389,15 @@ __global__ void __launch_bounds__(256) k_block_lmin(int n, const double* __restr
   }
   double hi = 0.0;
   for (int round = 0; round < 12 && hi - lo > 4e-16 * fmax(fabs(lo), fabs(hi)); ++round) {
-    const double step = (hi - lo) / (double)(blockDim.x + 1);
+    const double step = (hi - lo) / (double)(nt + 1);
     const double lam = lo + step * (tid + 1);
-    const int below = sturm_count(n, d, e, lam) == 0;   // lam <= lambda_min
+    const int below = sturm_count(n, A, st, lam) == 0;   // lam <= lambda_min
     if (tid == 0) s_j = -1;
     __syncthreads();
     if (below) atomicMax(&s_j, tid);
     __syncthreads();
     const int j = s_j;
-    const double nlo = lo + step * (j + 1), nhi = j + 1 < (int)blockDim.x ? lo + step * (j + 2) : hi;
+    const double nlo = lo + step * (j + 1), nhi = j + 1 < nt ? lo + step * (j + 2) : hi;
     lo = nlo;
     hi = nhi;
     __syncthreads();
@@ -751,16 +839,16 @@ void vaxpby(Ctx& c, double a, const double* x, double b, const double* y, double
 // Scratch: T1 (L^{-1}), T2 (L^{-1} dS), dX2 (M) -- free at this point of the step.
 double step_len(Ctx& c, Ipm* w, const double* S, const double* dS, cudaStream_t s) {
   const double frac = 0.98, tcap = 1.0 / frac;
-  const size_t smi = ((size_t)c.n * c.n + c.n) * sizeof(double);
+  const size_t smi = block_inv_smem(c.n);
   CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
-  k_block_inv<<<(unsigned)c.nb, 128, smi, s>>>((int)c.n, S, w->T1, nullptr, 1);
+  k_block_inv<<<(unsigned)c.nb, 512, smi, s>>>((int)c.n, S, w->T1, nullptr, 1);
   ++c.launches;
   CK(cudaGetLastError());
   bgemm(c, w->T1, 0, dS, 0, w->T2, 1.0, 0.0, s);      // L^{-1} dS
   bgemm(c, w->T2, 0, w->T1, 1, w->dX2, 1.0, 0.0, s);  // M = L^{-1} dS L^{-T}
-  const size_t sm = ((size_t)c.n * (c.n + 1) / 2 + 4 * (size_t)c.n) * sizeof(double);
+  const size_t sm = block_lmin_smem(c.n);
   CK(cudaFuncSetAttribute(k_block_lmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_block_lmin<<<(unsigned)c.nb, 256, sm, s>>>((int)c.n, w->dX2, tcap, w->tb);
+  k_block_lmin<<<(unsigned)c.nb, 512, sm, s>>>((int)c.n, w->dX2, tcap, w->tb);
   ++c.launches;
   CK(cudaGetLastError());
   std::vector<double> tb(c.nb);
@@ -1153,9 +1241,9 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     // W = Z^-1
     CK(cudaMemsetAsync(w->fail, 0, sizeof(int), s));
     {
-      const size_t smi = ((size_t)c.n * c.n + c.n) * sizeof(double);
+      const size_t smi = block_inv_smem(c.n);
       CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
-      k_block_inv<<<(unsigned)c.nb, 128, smi, s>>>((int)c.n, Z, w->W, w->fail);
+      k_block_inv<<<(unsigned)c.nb, 512, smi, s>>>((int)c.n, Z, w->W, w->fail);
       ++c.launches;
       CK(cudaGetLastError());
     }
@@ -1407,9 +1495,9 @@ extern "C" polya_status polya_ipm_solve(polya_ctx* ctx, polya_ipm_state* st, con
       if (res->gap <= opt->eps && res->pinf <= opt->tol) {   // stopping rule
         // every Z block positive definite (reading R10): the blockwise Cholesky of k_block_inv
         CK(cudaMemsetAsync(w->fail, 0, sizeof(int), s));
-        const size_t smi = ((size_t)c.n * c.n + c.n) * sizeof(double);
+        const size_t smi = block_inv_smem(c.n);
         CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
-        k_block_inv<<<(unsigned)c.nb, 128, smi, s>>>((int)c.n, st->Z, w->W, w->fail);
+        k_block_inv<<<(unsigned)c.nb, 512, smi, s>>>((int)c.n, st->Z, w->W, w->fail);
         ++c.launches;
         CK(cudaGetLastError());
         int hfail = 0;

@@ -62,7 +62,8 @@ __host__ __device__ constexpr int stage_byte(int t, int x, int y) {
 constexpr size_t kSmemBytes = (NSTAGE * STAGE + Q * Q * Q * Q) * sizeof(double) + 3 * NSTAGE * sizeof(uint64_t);
 
 #ifndef SCHUR_EXP
-#define SCHUR_EXP 0   // tools-only timing variants (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either
+#define SCHUR_EXP 0   // tools-only timing variants (tools/schur_exp.py): 1 = no epilogue, 2 = no fold either,
+                     // 4 = no mirror stores, 8 = item blocks stored contiguously (traffic experiments)
 #endif                // (results wrong by construction: never a bench value)
 
 struct SchurArgs {
@@ -597,12 +598,19 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_schur(const SchurArgs p) {
           if (rw[u].x < 0) continue;
           POLYA_ASSERT(rw[u].x < p.Ntil && cA.x < p.Ntil && cB.x < p.Ntil && it.pl < p.npl);
           double* dst = fullG ? p.G + (rowbase + rw[u].x) * p.K + colbase : tile + (int64_t)rw[u].x * p.Ntil;
+          if (SCHUR_EXP & 8) {   // traffic experiment: the item's block contiguous (whole sectors), wrong G
+            const int64_t span = (int64_t)p.npl * p.Ntil * p.Ntil - 4096;
+            double* blk = p.G + (int64_t)(((unsigned long long)it.item * 4096ull) % (unsigned long long)span);
+            if (cA.x >= 0) st_g(blk + (r0 + u * NCW) * 64 + lane, vA[u]);
+            if (cB.x >= 0) st_g(blk + (r0 + u * NCW) * 64 + lane + 32, vB[u]);
+            continue;
+          }
           if (cA.x >= 0 && !(same_cls && rw[u].x > cA.x)) st_g(dst + cA.x, vA[u]);
           if (cB.x >= 0 && !(same_cls && rw[u].x > cB.x)) st_g(dst + cB.x, vB[u]);
         }
       }
     }
-    if (fullG || diag_pair) {  // pass 1: mirror entries G[t][s], lanes along the rows s
+    if ((fullG || diag_pair) && !(SCHUR_EXP & 12)) {  // pass 1: mirror entries G[t][s], lanes along the rows s
       const int4 rA = lane < nr ? s_rt[tb][lane] : none, rB = lane + 32 < nr ? s_rt[tb][lane + 32] : none;
       for (int c0 = warp; c0 < nc; c0 += 4 * NCW) {
         int4 cl[4];
