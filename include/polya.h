@@ -382,6 +382,15 @@ polya_status polya_verdict(polya_ctx* ctx, const double* y_dev, int32_t npts, co
 polya_status polya_factor_solve_loopback(polya_ctx** ctxs, int32_t nranks, double* const* G_local, double* x_dev,
                                          void* stream);
 
+/* Test hook of the IPM's blockwise kernels (reading R5): for nb blocks of order n
+ * (1 <= n <= 168; device stacks of nb row-major n x n doubles, caller-owned) computes W_b = S_b^{-1}
+ * (k_block_inv), Linv_b = L_b^{-1} with S_b = L_b L_b^T (lower, zeros above), M_b = L_b^{-1} dS_b
+ * L_b^{-T} and t_b = min(1/0.98, 1 / max(0, -lambda_min(sym M_b))) (k_block_lmin; -1 when S_b is not
+ * positive definite), and *fail (int32, device) = 1 if some S_b is not positive definite.
+ * Synchronous.  Errors: EINVAL (n out of range, null pointers), ECUDA. */
+polya_status polya_block_kernels_test(int32_t n, int64_t nb, const double* S_dev, const double* dS_dev, double* W_dev,
+                                      double* Linv_dev, double* M_dev, double* t_dev, int32_t* fail_dev, void* stream);
+
 /* Surfaces asynchronous errors (device synchronise + last-error check). */
 polya_status polya_sync(polya_ctx* ctx);
 const char* polya_strerror(polya_status s);

@@ -27,7 +27,7 @@ EXPORTS = ["polya_setup", "polya_dims_get", "polya_plan", "polya_get_exponents",
            "polya_simplex_map", "polya_ipm_solve", "polya_verdict", "polya_set_factorization", "polya_schur_prepare",
            "polya_schur_assemble", "polya_setup_general", "polya_factor_solve_loopback", "polya_schur_reduce",
            "polya_get_combine_timing", "polya_set_combine_tiles", "polya_p2p_export", "polya_p2p_import",
-           "polya_p2p_loopback", "polya_schur_reduce_p2p"]
+           "polya_p2p_loopback", "polya_schur_reduce_p2p", "polya_block_kernels_test"]
 
 
 class PolyaError(RuntimeError):
@@ -85,6 +85,7 @@ def lib():
     L.polya_setup.argtypes = [ctypes.POINTER(_Config), vp, ctypes.POINTER(vp)]
     L.polya_setup_general.argtypes = [ctypes.POINTER(_Config), i32, i32, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
     L.polya_factor_solve_loopback.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(vp), vp, vp]
+    L.polya_block_kernels_test.argtypes = [i32, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
     L.polya_dims_get.argtypes = [vp, ctypes.POINTER(_Dims)]
     L.polya_plan.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Dims)]
     L.polya_get_exponents.argtypes = [vp, ctypes.c_int, vp]
@@ -163,6 +164,23 @@ def factor_solve_loopback(ctxs, G_local, x, stream=None):
         raise PolyaError(f"polya_factor_solve_loopback: {lib().polya_strerror(st).decode()} "
                          f"({lib().polya_last_error(ctxs[0]._h).decode()})")
     return x
+
+
+def block_kernels_test(S, dS, stream=None):
+    """polya_block_kernels_test (test hook): the IPM's blockwise kernels on (nb, n, n) device stacks.
+    Returns (W = S^-1, L^-1, M = L^-1 dS L^-T, t, fail) with t_b = min(1/0.98, 1/max(0, -lambda_min(M_b)))
+    (-1 for a block whose S_b is not positive definite) and fail = 1 if some S_b is not."""
+    import torch
+    nb, n = int(S.shape[0]), int(S.shape[1])
+    W, Li, M = (torch.empty_like(S) for _ in range(3))
+    t = torch.empty(nb, dtype=torch.float64, device=S.device)
+    fail = torch.zeros(1, dtype=torch.int32, device=S.device)
+    st = lib().polya_block_kernels_test(n, nb, _dev_ptr(S, nb * n * n, "S"), _dev_ptr(dS, nb * n * n, "dS"),
+                                        _dev_ptr(W, None, "W"), _dev_ptr(Li, None, "Linv"), _dev_ptr(M, None, "M"),
+                                        _dev_ptr(t, nb, "t"), ctypes.c_void_p(fail.data_ptr()), _stream_ptr(stream))
+    if st != 0:
+        raise PolyaError(f"polya_block_kernels_test: {lib().polya_strerror(st).decode()}")
+    return W, Li, M, t, int(fail.item())
 
 
 def p2p_loopback(ctxs):

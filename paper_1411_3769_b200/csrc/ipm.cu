@@ -248,22 +248,12 @@ __global__ void __launch_bounds__(512, 2) k_block_inv(int n, const double* __res
 size_t block_inv_smem(int64_t n) { return ((size_t)n * (size_t)(n | 1) + 3 * (size_t)n) * sizeof(double); }
 
 // Reading R5 as written: t_b = min(tcap, 1 / max(0, -lambda_min(M_b))), M_b = L_b^{-1} dS_b L_b^{-T}
-// (S_b = L_b L_b^T; M_b formed by k_block_inv(linv) + two k_bgemm).  One CTA per block: the symmetric
-// part of M_b, packed lower in shared memory ((n^2 + n)/2 + 4n doubles, n <= 168), is reduced to
-// tridiagonal form by Householder reflections (A <- H A H, H = I - tau v v^T; LAPACK dsytd2's
-// algorithm), then lambda_min by multisection on the Sturm count of the tridiagonal (256 trial points
-// per round, one per thread).  Non-finite M_b (S_b not positive definite, e.g. a singular X on the
+// (S_b = L_b L_b^T; M_b formed by k_block_inv(linv) + two k_bgemm).  One CTA (512 threads) per block:
+// the symmetric part of M_b, in full storage in shared memory (n (n|1) + 3n doubles, n <= 168), is
+// reduced to tridiagonal form by Householder reflections (A <- H A H, H = I - tau v v^T; LAPACK
+// dsytd2's algorithm), then lambda_min by multisection on the Sturm count of the tridiagonal (512
+// trial points per round, one per thread).  Non-finite M_b (S_b not positive definite, e.g. a singular X on the
 // boundary of the cone): t_b = -1, for which step_len runs the bisection kernel k_block_tmax.
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int q = 0; q < nw; ++q) s += red[q];
-  return s;
-}
 // Number of eigenvalues of the symmetric tridiagonal T below lam (Sturm sequence of T - lam I); the
 // diagonal d_i = T[i * st], the off-diagonal e_i = T[i * st + 1] (the tridiagonal kept in place in the
 // reduced matrix: st = ld + 1).
@@ -1362,6 +1352,43 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     }
   } catch (const IpmFail& f) {
     c.last_error = f.msg;
+    return f.s;
+  }
+  return POLYA_OK;
+}
+
+// ---- test hook: the IPM's blockwise kernels on caller-given block stacks -----------------------
+// W = S^{-1} (k_block_inv), L^{-1} (k_block_inv, L^{-1} mode), M = L^{-1} dS L^{-T} (two k_bgemm) and
+// t_b = min(1/0.98, 1/max(0, -lambda_min(M_b))) (k_block_lmin) -- the kernels step_len and the W of
+// polya_ipm_step run, at any block order n <= 168, so their parity and the maximum size are tested
+// directly (tests/test_gpu_block_kernels.py).
+extern "C" polya_status polya_block_kernels_test(int32_t n, int64_t nb, const double* S, const double* dS, double* W,
+                                                 double* Linv, double* M, double* t, int32_t* fail, void* stream) {
+  if (n < 1 || n > 168 || nb < 1 || !S || !dS || !W || !Linv || !M || !t || !fail) return POLYA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* T = nullptr;
+  auto ck = [&](cudaError_t e) {
+    if (e != cudaSuccess) throw IpmFail{POLYA_ECUDA, cudaGetErrorString(e)};
+  };
+  try {
+    const size_t nbytes = (size_t)nb * n * n * sizeof(double);
+    ck(cudaMalloc(&T, nbytes));
+    ck(cudaMemsetAsync(fail, 0, sizeof(int32_t), s));
+    const size_t smi = block_inv_smem(n), sml = block_lmin_smem(n);
+    ck(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
+    ck(cudaFuncSetAttribute(k_block_lmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sml));
+    k_block_inv<<<(unsigned)nb, 512, smi, s>>>(n, S, W, fail);
+    k_block_inv<<<(unsigned)nb, 512, smi, s>>>(n, S, Linv, nullptr, 1);
+    const int tiles = (n + 31) / 32;
+    dim3 grid((unsigned)(tiles * tiles), (unsigned)nb);
+    k_bgemm<<<grid, 128, 0, s>>>(n, Linv, 0, dS, 0, T, 1.0, 0.0, tiles);   // L^{-1} dS
+    k_bgemm<<<grid, 128, 0, s>>>(n, T, 0, Linv, 1, M, 1.0, 0.0, tiles);    // (L^{-1} dS) L^{-T}
+    k_block_lmin<<<(unsigned)nb, 512, sml, s>>>(n, M, 1.0 / 0.98, t);
+    ck(cudaGetLastError());
+    ck(cudaStreamSynchronize(s));
+    ck(cudaFree(T));
+  } catch (const IpmFail& f) {
+    if (T) cudaFree(T);
     return f.s;
   }
   return POLYA_OK;
