@@ -649,12 +649,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ipm-timeout", type=float, default=None,
-                    help="seconds before the IPM leg gives up (default 180; 1800 for config 5)")
+                    help="seconds before the IPM leg gives up (default 120; 1800 for config 5)")
     args = ap.parse_args()
     cid = int(args.config) if args.config.isdigit() else args.config
     cfg = synth.CONFIGS[cid]
     if args.ipm_timeout is None:
-        args.ipm_timeout = 1800.0 if cid == 5 else 180.0
+        args.ipm_timeout = 1800.0 if cid == 5 else 120.0
     if args.impl == "reference":
         return run_reference(args, cfg, cid)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
