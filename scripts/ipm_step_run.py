@@ -15,6 +15,8 @@ cid = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 cfg = synth.CONFIGS[cid]
 A = synth.vertex_matrices(cfg, np.random.default_rng(0))
 ctx = pb.Polya(cfg.n, cfg.l, cfg.dp, cfg.d1, cfg.d2, A)
+if os.environ.get("FACT"):   # polya_set_factorization mode (1 dense look-ahead, 3 dense one-call cuSOLVER, 2 tiled)
+    ctx.set_factorization(int(os.environ["FACT"]))
 X = torch.eye(cfg.n, dtype=torch.float64, device="cuda").repeat(ctx.nblocks, 1, 1).contiguous()
 Z = X.clone()
 y = torch.zeros(ctx.K, dtype=torch.float64, device="cuda")
