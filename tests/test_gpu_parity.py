@@ -263,11 +263,12 @@ def test_schur_large_rows_entries_probes(pb, cfg_id, layout, nrows, npool, nent)
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("n", [125, 128, 130])
+@pytest.mark.parametrize("n", [125, 128, 130, 168])
 def test_schur_precompute_size_boundary(pb, n):
     """The SCM precompute switches kernels at np = 128 (K3b row-gathered GEMMs up to it, K3 batched GEMMs
-    beyond): n = 125 (np = 128, ragged tail of 5), 128 (np = 128, no tail), 130 (np = 136) -- whole
-    stratified rows, stratified entries and 2 probes of G against the literal Eq. T2."""
+    beyond): n = 125 (np = 128, ragged tail of 5), 128 (np = 128, no tail), 130 (np = 136), and the
+    largest block order 168 (21 chunks) -- whole stratified rows, stratified entries and 2 probes of G
+    against the literal Eq. T2."""
     cfg = synth.small_config(n, 2, 1, 1, 1)
     ctx, A, X, W = _setup(pb, cfg)
     G = ctx.schur(_dev(X), _dev(W), layout=pb.G_PAIR_TILES)

@@ -168,3 +168,27 @@ def test_verdict_beyond_118_states(pb):
     assert ctx.verdict(torch.from_numpy(-ystar).cuda(), pts) == len(pts)
     assert not oipm.grid_check(P, -ystar, 12, 0)
     ctx.close()
+
+
+@pytest.mark.parametrize("stable", [True, False], ids=["stable", "unstable"])
+def test_solve_at_max_block_order(pb, stable):
+    """Block order n = 168, the IPM's shared-memory limit (k_block_inv / k_block_lmin at their largest
+    layouts, K4 with 21 index chunks, K = 28,392): a stable polytope (config-2 recipe) is certified and
+    the oracle's grid check accepts the GPU's certificate; with a vertex shifted by +3I (unstable) it is
+    not certified (Theorem 1 rules a certificate out)."""
+    from paper_1411_3769_b200 import robust
+    c = synth.small_config(168, 2, 1, 1, 1)
+    A = synth.vertex_matrices(c, np.random.default_rng(0))
+    if not stable:
+        A[1] = A[1] + 3.0 * np.eye(c.n)
+    ctx = pb.Polya(c.n, c.l, c.dp, c.d1, c.d2, A)
+    r = ctx.ipm_solve()
+    if stable:
+        assert r["converged"] and r["gap"] <= 1e-8 and r["pinf"] <= 1e-8, {k: r[k] for k in ("status", "gap", "pinf")}
+        assert ctx.verdict(r["y"], robust.simplex_points(c.l, 50, 0)) == 0
+        P = osdp.build_problem(A, c.n, c.l, c.dp, c.d1, c.d2)
+        assert oipm.grid_check(P, r["y"].cpu().numpy(), 50, 0)
+    else:
+        assert not r["converged"]
+    ctx.close()
+    torch.cuda.empty_cache()
