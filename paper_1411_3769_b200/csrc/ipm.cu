@@ -655,6 +655,9 @@ struct Ipm {
   double* panel[2] = {};       // dist, nranks > 1: the broadcast panel of step k ((L0-1) tiles), by k parity
   double* lkk[2] = {};         // dist, nranks > 1: the broadcast diagonal factor L_kk (one tile), by k parity
   double* stat = nullptr;      // dist: {local error, potrf info} of a step, max-reduced over the ranks
+  double *S1 = nullptr, *S2 = nullptr, *S3 = nullptr, *tb2 = nullptr;   // step_lens: the second chain's scratch
+  cudaStream_t sl = nullptr;                  // step_lens: the second chain's stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* dinv = nullptr;      // dense: inverses of the kSolveNB diagonal blocks of the factor
   double* eye = nullptr;       // dense: nblk identity blocks (the right-hand side of those trsm)
   double* tsol = nullptr;      // dense: one block of the solve
@@ -680,7 +683,7 @@ void polya_ipm_free(polya::Ctx& c) {
   if (!w) return;
   double* ps[] = {w->W, w->Rd, w->T1, w->T2, w->dX1, w->dZ1, w->dX2, w->dZ2, w->G, w->O1, w->O2,
                   w->dy1, w->dy2, w->tmpK, w->tb, w->part, w->dc, w->work, w->panel[0], w->panel[1],
-                  w->lkk[0], w->lkk[1], w->stat, w->dinv, w->eye, w->tsol};
+                  w->lkk[0], w->lkk[1], w->stat, w->dinv, w->eye, w->tsol, w->S1, w->S2, w->S3, w->tb2};
   for (double* p : ps)
     if (p) cudaFree(p);
   if (w->info) cudaFree(w->info);
@@ -691,6 +694,9 @@ void polya_ipm_free(polya::Ctx& c) {
   if (w->blas) cublasDestroy(w->blas);
   if (w->blas_upd) cublasDestroy(w->blas_upd);
   if (w->upd) cudaStreamDestroy(w->upd);
+  if (w->sl) cudaStreamDestroy(w->sl);
+  if (w->ev_fork) cudaEventDestroy(w->ev_fork);
+  if (w->ev_join) cudaEventDestroy(w->ev_join);
   for (auto* v : {&w->ev_pan, &w->ev_col, &w->ev_upd})
     for (auto e : *v) cudaEventDestroy(e);
   for (auto& e : w->ev)
@@ -739,7 +745,7 @@ Ipm* ipm_ws(Ctx& c) {
   w->nb = c.nb; w->n = c.n; w->K = c.K;
   w->tiled = want_tiled(c);
   const size_t st = (size_t)c.nb * c.n * c.n * sizeof(double), kv = (size_t)c.K * sizeof(double);
-  double** stacks[] = {&w->W, &w->Rd, &w->T1, &w->T2, &w->dX1, &w->dZ1, &w->dX2, &w->dZ2};
+  double** stacks[] = {&w->W, &w->Rd, &w->T1, &w->T2, &w->dX1, &w->dZ1, &w->dX2, &w->dZ2, &w->S1, &w->S2, &w->S3};
   for (double** p : stacks) CK(cudaMalloc(p, st));
   double** vecs[] = {&w->O1, &w->O2, &w->dy1, &w->dy2, &w->tmpK};
   for (double** p : vecs) CK(cudaMalloc(p, kv));
@@ -780,6 +786,10 @@ Ipm* ipm_ws(Ctx& c) {
     CK(cudaMemcpy(w->dptrB, pb.data(), nblk * sizeof(double*), cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&w->tb, (size_t)c.nb * sizeof(double)));
+  CK(cudaMalloc(&w->tb2, (size_t)c.nb * sizeof(double)));
+  CK(cudaStreamCreateWithFlags(&w->sl, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
   CK(cudaMalloc(&w->part, (size_t)kScalarBlocks * 3 * sizeof(double)));
   CK(cudaMalloc(&w->dc, (size_t)std::max<int64_t>(c.L, 1) * sizeof(double)));
   CK(cudaMemcpy(w->dc, c.c.data(), (size_t)c.L * sizeof(double), cudaMemcpyHostToDevice));
@@ -827,35 +837,60 @@ void vaxpby(Ctx& c, double a, const double* x, double b, const double* y, double
 
 // Reading R5: t = min(1, 0.98 t_max), t_max = min_b 1 / max(0, -lambda_min(L_b^{-1} dS_b L_b^{-T})).
 // Scratch: T1 (L^{-1}), T2 (L^{-1} dS), dX2 (M) -- free at this point of the step.
-double step_len(Ctx& c, Ipm* w, const double* S, const double* dS, cudaStream_t s) {
+// One chain of reading R5 on stream st: L^{-1} (k_block_inv), M = L^{-1} dS L^{-T} (two k_bgemm into the
+// scratch stacks Ta, Tb, M), per-block bound tb (k_block_lmin).
+void step_chain(Ctx& c, const double* S, const double* dS, double* Ta, double* Tb, double* M, double* tb, double tcap,
+                cudaStream_t st) {
+  k_block_inv<<<(unsigned)c.nb, 512, block_inv_smem(c.n), st>>>((int)c.n, S, Ta, nullptr, 1);
+  ++c.launches;
+  CK(cudaGetLastError());
+  bgemm(c, Ta, 0, dS, 0, Tb, 1.0, 0.0, st);   // L^{-1} dS
+  bgemm(c, Tb, 0, Ta, 1, M, 1.0, 0.0, st);    // M = L^{-1} dS L^{-T}
+  k_block_lmin<<<(unsigned)c.nb, 512, block_lmin_smem(c.n), st>>>((int)c.n, M, tcap, tb);
+  ++c.launches;
+  CK(cudaGetLastError());
+}
+
+// Reading R5 for both step lengths: t_p from (X, dX) and t_d from (Z, dZ), t = min(1, 0.98 t_max), t_max =
+// min_b 1 / max(0, -lambda_min(L_b^{-1} dS_b L_b^{-T})).  The two chains are independent and each fills
+// only ~70 % of the SM slots with latency-bound CTAs, so the second runs on w->sl (own scratch) beside the
+// first; one host synchronisation for both.  Scratch of the first: T1, T2, dX2 (free at this point).
+void step_lens(Ctx& c, Ipm* w, const double* X, const double* dX, const double* Z, const double* dZ, cudaStream_t s,
+               double& tp, double& td) {
   const double frac = 0.98, tcap = 1.0 / frac;
-  const size_t smi = block_inv_smem(c.n);
-  CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smi));
-  k_block_inv<<<(unsigned)c.nb, 512, smi, s>>>((int)c.n, S, w->T1, nullptr, 1);
-  ++c.launches;
-  CK(cudaGetLastError());
-  bgemm(c, w->T1, 0, dS, 0, w->T2, 1.0, 0.0, s);      // L^{-1} dS
-  bgemm(c, w->T2, 0, w->T1, 1, w->dX2, 1.0, 0.0, s);  // M = L^{-1} dS L^{-T}
-  const size_t sm = block_lmin_smem(c.n);
-  CK(cudaFuncSetAttribute(k_block_lmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_block_lmin<<<(unsigned)c.nb, 512, sm, s>>>((int)c.n, w->dX2, tcap, w->tb);
-  ++c.launches;
-  CK(cudaGetLastError());
-  std::vector<double> tb(c.nb);
+  CK(cudaFuncSetAttribute(k_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)block_inv_smem(c.n)));
+  CK(cudaFuncSetAttribute(k_block_lmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)block_lmin_smem(c.n)));
+  CK(cudaEventRecord(w->ev_fork, s));
+  CK(cudaStreamWaitEvent(w->sl, w->ev_fork, 0));
+  step_chain(c, X, dX, w->T1, w->T2, w->dX2, w->tb, tcap, s);
+  step_chain(c, Z, dZ, w->S1, w->S2, w->S3, w->tb2, tcap, w->sl);
+  CK(cudaEventRecord(w->ev_join, w->sl));
+  CK(cudaStreamWaitEvent(s, w->ev_join, 0));
+  std::vector<double> tb(2 * c.nb);
   CK(cudaMemcpyAsync(tb.data(), w->tb, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(tb.data() + c.nb, w->tb2, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (*std::min_element(tb.begin(), tb.end()) < 0.0) {   // a semidefinite S_b: bisection for those blocks
-    const size_t smb = (size_t)c.n * c.n * sizeof(double);
-    CK(cudaFuncSetAttribute(k_block_tmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-    k_block_tmax<<<(unsigned)c.nb, 256, smb, s>>>((int)c.n, S, dS, tcap, w->tb);
-    ++c.launches;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(tb.data(), w->tb, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+  double t[2];
+  for (int q = 0; q < 2; ++q) {
+    double* h = tb.data() + q * c.nb;
+    if (*std::min_element(h, h + c.nb) < 0.0) {   // a semidefinite S_b: bisection for those blocks
+      const double* S = q ? Z : X;
+      const double* dS = q ? dZ : dX;
+      double* d = q ? w->tb2 : w->tb;
+      const size_t smb = (size_t)c.n * c.n * sizeof(double);
+      CK(cudaFuncSetAttribute(k_block_tmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+      k_block_tmax<<<(unsigned)c.nb, 256, smb, s>>>((int)c.n, S, dS, tcap, d);
+      ++c.launches;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h, d, c.nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    double m = tcap;
+    for (int64_t i = 0; i < c.nb; ++i) m = std::min(m, h[i]);
+    t[q] = std::min(1.0, frac * m);
   }
-  double t = tcap;
-  for (double v : tb) t = std::min(t, v);
-  return std::min(1.0, frac * t);
+  tp = t[0];
+  td = t[1];
 }
 
 // ---- blocked Cholesky on the pair tiles --------------------------------------------------------
@@ -1314,8 +1349,8 @@ extern "C" polya_status polya_ipm_step(polya_ctx* ctx, polya_ipm_state* st, poly
     axpby(c, 1.0, w->dZ1, 1.0, w->dZ2, w->dZ1, nullptr, 0.0, s);
     vaxpby(c, 1.0, w->dy1, 1.0, w->dy2, w->dy1, s);
     // line search (R5) and update (R6)
-    const double tp = step_len(c, w, X, w->dX1, s);
-    const double td = step_len(c, w, Z, w->dZ1, s);
+    double tp = 0.0, td = 0.0;
+    step_lens(c, w, X, w->dX1, Z, w->dZ1, s, tp, td);
     if (!(tp > 0.0) || !(td > 0.0)) throw IpmFail{POLYA_ESTEP, "no admissible step"};
     axpby(c, 1.0, X, tp, w->dX1, X, nullptr, 0.0, s);
     axpby(c, 1.0, Z, td, w->dZ1, Z, nullptr, 0.0, s);
