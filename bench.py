@@ -220,6 +220,26 @@ def reduce_over_ranks(x, op, device, world):
     return float(t.item())
 
 
+def start_watchdog(seconds, emit, exit_fn=None):
+    """Daemon timer for a leg that may hang inside a collective: after `seconds` it calls emit() (rank 0
+    prints the JSON line with the leg marked as timed out) and ends the process with status 0 on its
+    own clock (os._exit: a thread blocked in NCCL cannot be unwound).  cancel() it when the leg ends."""
+    import threading
+
+    def fire():
+        try:
+            emit()
+        finally:
+            sys.stdout.flush()
+            sys.stderr.flush()
+            (exit_fn or os._exit)(0)
+
+    t = threading.Timer(seconds, fire)
+    t.daemon = True
+    t.start()
+    return t
+
+
 def run_gpu(args, cfg, cid):
     import torch
     import torch.distributed as dist
@@ -535,18 +555,11 @@ def run_gpu(args, cfg, cid):
         # factorisation).  A hang there must not cost the Schur line measured above: after --ipm-timeout
         # seconds every rank gives up on its own clock, rank 0 prints the line with the IPM leg marked as
         # timed out, and all ranks exit.
-        import threading
-
-        def ipm_timed_out():
-            if rank == 0:
-                print(json.dumps(make_line({"error": f"IPM leg timed out after {args.ipm_timeout:.0f} s "
-                                                     f"({world} rank(s))", "n_ranks": world}, None)), flush=True)
-            sys.stderr.flush()
-            os._exit(0)
-
-        watchdog = threading.Timer(args.ipm_timeout, ipm_timed_out)
-        watchdog.daemon = True
-        watchdog.start()
+        watchdog = start_watchdog(
+            args.ipm_timeout,
+            lambda: print(json.dumps(make_line({"error": f"IPM leg timed out after {args.ipm_timeout:g} s "
+                                                         f"({world} rank(s))", "n_ranks": world}, None)),
+                          flush=True) if rank == 0 else None)
         del G
         flush = None
         if blocks:

@@ -35,3 +35,21 @@ def test_gpus_flag_fails_loudly_without_enough_gpus():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
                          text=True, timeout=300, env={**os.environ, "WORLD_SIZE": "1"})
     assert out.returncode == 2 and "WORLD_SIZE=1" in out.stderr
+
+
+def test_ipm_watchdog_emits_and_exits():
+    """The N > 1 IPM leg's watchdog (bench.start_watchdog): when the leg outlives its timeout the line
+    is still emitted and the process ends with status 0; a cancelled watchdog never fires."""
+    import threading
+    sys.path.insert(0, ROOT)
+    import bench
+    fired, exited = [], threading.Event()
+    t = bench.start_watchdog(0.05, lambda: fired.append("line"), exit_fn=lambda code: (fired.append(code), exited.set()))
+    assert exited.wait(5.0)
+    assert fired == ["line", 0]
+    calls = []
+    t2 = bench.start_watchdog(0.2, lambda: calls.append(1), exit_fn=lambda code: calls.append(code))
+    t2.cancel()
+    t2.join(1.0)
+    assert calls == []
+    t.join(1.0)
